@@ -1,0 +1,128 @@
+"""fp64 CPU ORACLE for one decode-step attention layer over the hybrid cache.
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+`cpu_baseline` / `--impl reference` legs may import or call anything under `oracle/`.
+The product path (paper_2504_07494_b200/) never imports it and shares no code with it.
+
+What it computes (§2.1, Eq. 1-3; §3.1 "Opportunity I"):
+for each request i in the decode batch, with n_i >= 1 cached tokens INCLUDING the
+current one (the current token "attends to ... itself"):
+
+  1. K/V source.  KV mode (beta_i = 0): k_j, v_j are read from the cache.
+     Hidden mode (beta_i = 1): the cache holds the layer input x_j and
+         k_j = W_K x_j (+ b_K),   v_j = W_V x_j (+ b_V)              (Eq. 1)
+     for every cached j ("transform the cached input hidden vectors ... to required key
+     and value vectors").  No pre-projection normalisation: the paper specifies
+     none (reading R4); the bias is optional (reading R4).
+  2. Per head h (columns h*dh .. h*dh+dh-1 of d; reading R1):
+         s_j = scale * q_h . k_{j,h}                                 (Eq. 2)
+         a_j = exp(s_j - max s) / sum_m exp(s_m - max s)              (Eq. 2)
+         o_h = sum_j a_j v_{j,h}                                     (Eq. 3, P:131-133;
+                                                v_i in the paper is a typo for v_j, R2)
+     out_i = concat_h o_h  (before W_o, reading R3);  lse_{i,h} = max s + ln sum exp(s - max s).
+
+Everything is float64; inputs stored in bf16/fp32 are widened exactly.  The oracle does
+NOT round reconstructed K/V to the storage precision (reading R9): the GPU's rounding
+is part of the error the tolerance covers.
+
+Pins (tests/test_oracle_pins.py): 40-digit Decimal brute force, closed forms (W = I,
+permutation W, n = 1, q = 0, V = 1, bias shift), torch float64 SDPA, hybrid equivalence,
+softmax rows summing to 1.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+def _f64(a) -> np.ndarray:
+    """Exact widening of a torch / numpy array to float64."""
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().to(dtype=__import__("torch").float64).numpy()
+    return np.asarray(a, dtype=np.float64)
+
+
+def reconstruct_kv(X, W_K, W_V, b_K=None, b_V=None):
+    """Eq. 1 applied to every cached hidden state:
+    K = X W_K^T (+ b_K), V = X W_V^T (+ b_V).  X: [n, d]; W_K, W_V: [d, d] with
+    k = W_K x (rows of W are output features)."""
+    X, W_K, W_V = _f64(X), _f64(W_K), _f64(W_V)
+    K = X @ W_K.T
+    V = X @ W_V.T
+    if b_K is not None:
+        K = K + _f64(b_K)[None, :]
+    if b_V is not None:
+        V = V + _f64(b_V)[None, :]
+    return K, V
+
+
+def attend(q, K, V, n_heads: int, scale: float, return_probs: bool = False):
+    """Eq. 2-3 for ONE decode query over n cached tokens, per head.
+    q: [d]; K, V: [n, d].  Returns out [d], lse [H] (and probabilities [H, n])."""
+    q, K, V = _f64(q), _f64(K), _f64(V)
+    n, d = K.shape
+    assert n >= 1, "n_i >= 1: the current token is part of the context (P:135)"
+    dh = d // n_heads
+    out = np.empty(d)
+    lse = np.empty(n_heads)
+    probs = np.empty((n_heads, n))
+    for h in range(n_heads):
+        c = slice(h * dh, (h + 1) * dh)
+        s = scale * (K[:, c] @ q[c])          # s_j = q_h . k_{j,h} / sqrt(.)
+        m = s.max()
+        e = np.exp(s - m)
+        l = e.sum()
+        a = e / l                              # a_j, Eq. 2
+        out[c] = a @ V[:, c]                   # sum_j a_j v_{j,h}, Eq. 3 (pre-W_o)
+        lse[h] = m + np.log(l)
+        probs[h] = a
+    if return_probs:
+        return out, lse, probs
+    return out, lse
+
+
+def hidden_request_kv(X, W_KV, b_KV=None):
+    """Split the stacked [2d, d] W_KV = [W_K; W_V] (and [2d] bias) and rebuild K, V."""
+    W_KV = _f64(W_KV)
+    d = W_KV.shape[1]
+    bK = bV = None
+    if b_KV is not None:
+        b = _f64(b_KV)
+        bK, bV = b[:d], b[d:]
+    return reconstruct_kv(X, W_KV[:d], W_KV[d:], bK, bV)
+
+
+def decode_batch(requests: Sequence[dict], W_KV, n_heads: int, scale: float, b_KV=None):
+    """Hybrid-cache decode step for a batch.  Each request dict has 'q' [d] and either
+    'mode' 0 with 'K', 'V' [n, d] or 'mode' 1 with 'X' [n, d].
+    Returns out [n_req, d], lse [n_req, H]."""
+    outs, lses = [], []
+    for r in requests:
+        if r["mode"] == 1:
+            K, V = hidden_request_kv(r["X"], W_KV, b_KV)
+        else:
+            K, V = r["K"], r["V"]
+        o, l = attend(r["q"], K, V, n_heads, scale)
+        outs.append(o)
+        lses.append(l)
+    return np.stack(outs), np.stack(lses)
+
+
+def head_output(q_h, X, W_K_h, W_V_h, scale: float, b_K_h=None, b_V_h=None):
+    """One (request, head) of a hidden-mode request, rebuilding only that head's
+    dh columns (the same Eq. 1-3 restricted to head h; used to sample large configs)."""
+    K, V = reconstruct_kv(X, W_K_h, W_V_h, b_K_h, b_V_h)
+    o, l = attend(q_h, K, V, 1, scale)
+    return o, l[0]
+
+
+def max_rel_err(gpu, ref, n_heads: int) -> float:
+    """Normwise error per (request, head) row (reading R12):
+    max_{i,h,c} |gpu - ref| / max(max_c' |ref_{i,h,c'}|, 1e-6)."""
+    g = _f64(gpu)
+    r = _f64(ref)
+    g = g.reshape(g.shape[0], n_heads, -1)
+    r = r.reshape(r.shape[0], n_heads, -1)
+    denom = np.maximum(np.abs(r).max(axis=2, keepdims=True), 1e-6)
+    return float((np.abs(g - r) / denom).max()) if g.size else 0.0

@@ -1,0 +1,218 @@
+"""Pins the fp64 oracle to things other than itself (task rule ③).
+
+Each test names the passage / closed form it pins.  Together they are chosen so that a
+plausible mistake in oracle/hc_oracle.py (a dropped bias, a wrong sign in the softmax
+shift, a transposed W, a wrong head slice, a wrong scale, v_i instead of v_j) fails at
+least one of them.
+"""
+import math
+from decimal import Decimal, getcontext
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hc_oracle as O
+from synth import configs as C
+
+
+# ---------------------------------------------------------------- Decimal brute force
+def _dec_attend(q, K, V, H, scale):
+    """40-digit Decimal Eq. 2-3 written from the paper with plain loops."""
+    getcontext().prec = 40
+    n, d = len(K), len(q)
+    dh = d // H
+    sc = Decimal(repr(scale))
+    out, lse = [Decimal(0)] * d, []
+    for h in range(H):
+        cols = range(h * dh, (h + 1) * dh)
+        s = [sc * sum(Decimal(repr(float(q[c]))) * K[j][c] for c in cols) for j in range(n)]
+        m = max(s)
+        e = [(x - m).exp() for x in s]
+        z = sum(e)
+        for c in cols:
+            out[c] = sum(e[j] / z * V[j][c] for j in range(n))
+        lse.append(m + z.ln())
+    return out, lse
+
+
+def _dec_matrix(t):
+    return [[Decimal(repr(float(v))) for v in row] for row in t.tolist()]
+
+
+def _dec_recon(X, W, b):
+    """k_j = W x_j + b with Decimal sums (Eq. 1)."""
+    out = []
+    for x in X:
+        row = []
+        for wr, bb in zip(W, b):
+            row.append(sum(wv * xv for wv, xv in zip(wr, x)) + bb)
+        out.append(row)
+    return out
+
+
+@pytest.mark.parametrize("bias", [False, True])
+def test_oracle_vs_decimal_bruteforce_tiny(bias):
+    """tiny config (4 requests, d=32, 2x16 heads; KV and hidden) vs 40-digit Decimal.
+    Pins Eq. 1 (orientation of W, bias), Eq. 2 (scale, max shift, normalisation) and
+    Eq. 3 (v_j weighting) to 1e-13 relative."""
+    w = C.tiny(bias=bias)
+    d, H = w.shape.d, w.shape.H
+    W = w.w_kv()
+    b = w.b_kv()
+    Wd = _dec_matrix(W.double())
+    bd = [Decimal(repr(float(v))) for v in (b.tolist() if b is not None else [0.0] * (2 * d))]
+    for i in range(4):
+        q = w.q(i).double().numpy()
+        if w.modes[i] == C.MODE_KV:
+            K, V = w.kv(i)
+            Kd, Vd = _dec_matrix(K.double()), _dec_matrix(V.double())
+            req = {"mode": 0, "q": q, "K": K, "V": V}
+        else:
+            X = w.x(i)
+            Xd = _dec_matrix(X.double())
+            Kd = _dec_recon(Xd, Wd[:d], bd[:d])
+            Vd = _dec_recon(Xd, Wd[d:], bd[d:])
+            req = {"mode": 1, "q": q, "X": X}
+        out_ref, lse_ref = _dec_attend(q, Kd, Vd, H, w.scale)
+        out, lse = O.decode_batch([req], W, H, w.scale, b)
+        for c in range(d):
+            ref = float(out_ref[c])
+            assert abs(out[0, c] - ref) <= 1e-13 * max(1.0, abs(ref))
+        for h in range(H):
+            assert abs(lse[0, h] - float(lse_ref[h])) <= 1e-13 * max(1.0, abs(float(lse_ref[h])))
+
+
+# ---------------------------------------------------------------- closed forms
+def _rand(shape, seed, scale=1.0):
+    return np.random.default_rng(seed).normal(0, scale, size=shape)
+
+
+def test_identity_weights_reconstruct_exactly():
+    """W_K = W_V = I  =>  K = V = X exactly (Eq. 1 with identity maps)."""
+    X = _rand((7, 12), 0)
+    K, V = O.reconstruct_kv(X, np.eye(12), np.eye(12))
+    assert np.array_equal(K, X) and np.array_equal(V, X)
+
+
+def test_permutation_weights_permute_columns():
+    """W = permutation matrix P (k = P x)  =>  k_j[r] = x_j[perm[r]] exactly; catches W vs W^T."""
+    perm = np.random.default_rng(1).permutation(10)
+    P = np.zeros((10, 10))
+    P[np.arange(10), perm] = 1.0
+    X = _rand((5, 10), 2)
+    K, _ = O.reconstruct_kv(X, P, np.eye(10))
+    assert np.array_equal(K, X[:, perm])
+
+
+def test_single_token_returns_v1():
+    """n = 1: a_11 = 1 (Eq. 2), so out = v_1 (north_star invariant); hidden: W_V x_1 + b_V."""
+    d, H = 16, 4
+    q, K, V = _rand(d, 3), _rand((1, d), 4), _rand((1, d), 5)
+    out, lse = O.attend(q, K, V, H, 0.25)
+    assert np.allclose(out, V[0], rtol=0, atol=1e-15)
+    s = [0.25 * q[h * 4:(h + 1) * 4] @ K[0, h * 4:(h + 1) * 4] for h in range(H)]
+    assert np.allclose(lse, s, atol=1e-15)
+    X, W, b = _rand((1, d), 6), _rand((2 * d, d), 7), _rand(2 * d, 8)
+    out2, _ = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.25, b)
+    assert np.allclose(out2[0], W[d:] @ X[0] + b[d:], atol=1e-13)
+
+
+def test_zero_query_gives_mean_of_values():
+    """q = 0  =>  all scores equal  =>  a_j = 1/n  =>  out = mean_j v_j."""
+    d, n = 8, 9
+    out, lse = O.attend(np.zeros(d), _rand((n, d), 9), V := _rand((n, d), 10), 2, 0.5)
+    assert np.allclose(out, V.mean(axis=0), atol=1e-14)
+    assert np.allclose(lse, math.log(n), atol=1e-14)
+
+
+def test_constant_values_give_constant_output_and_probs_sum_to_one():
+    """V = 1  =>  out = sum_j a_j = 1 (softmax rows sum to 1, north_star invariant)."""
+    d, n, H = 16, 33, 2
+    out, lse, a = O.attend(_rand(d, 11, 3.0), _rand((n, d), 12), np.ones((n, d)), H, 1.0,
+                           return_probs=True)
+    assert np.allclose(out, 1.0, atol=1e-14)
+    assert np.allclose(a.sum(axis=1), 1.0, atol=1e-14)
+    assert (a > 0).all()
+
+
+def test_key_bias_is_a_per_head_score_shift():
+    """b_K adds q_h . b_K,h to every score of head h: output unchanged, lse shifted by
+    scale * q_h . b_K,h (catches a dropped / misplaced key bias and the max shift sign)."""
+    d, n, H, sc = 16, 20, 2, 0.3
+    X, W, q = _rand((n, d), 13), _rand((2 * d, d), 14, 0.25), _rand(d, 15)
+    bK = _rand(d, 16)
+    b = np.concatenate([bK, np.zeros(d)])
+    o0, l0 = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, sc)
+    o1, l1 = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, sc, b)
+    assert np.allclose(o0, o1, atol=1e-12)
+    shift = [sc * q[h * 8:(h + 1) * 8] @ bK[h * 8:(h + 1) * 8] for h in range(H)]
+    assert np.allclose(l1[0] - l0[0], shift, atol=1e-12)
+
+
+def test_large_scale_selects_argmax_value():
+    """scale -> large with a unique maximal score  =>  out -> v_argmax (Eq. 2 limit)."""
+    d, n = 8, 6
+    q, K, V = _rand(d, 17), _rand((n, d), 18), _rand((n, d), 19)
+    j = int(np.argmax(K @ q))
+    out, _ = O.attend(q, K, V, 1, 1e4)
+    assert np.allclose(out, V[j], atol=1e-9)
+
+
+def test_matches_torch_sdpa_float64_multihead():
+    """Library routine: all-KV batch with H heads == torch SDPA (float64, one query).
+    Pins the head slicing (columns h*dh..h*dh+dh-1) and the explicit scale."""
+    d, H, n = 48, 3, 17
+    q, K, V = _rand(d, 20), _rand((n, d), 21), _rand((n, d), 22)
+    sc = 1.0 / math.sqrt(d // H)
+    out, _ = O.attend(q, K, V, H, sc)
+    tq = torch.tensor(q).view(1, H, 1, d // H)
+    tk = torch.tensor(K).view(n, H, d // H).transpose(0, 1).unsqueeze(0)
+    tv = torch.tensor(V).view(n, H, d // H).transpose(0, 1).unsqueeze(0)
+    ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, scale=sc)
+    assert np.allclose(out, ref.reshape(d).numpy(), atol=1e-13)
+
+
+def test_hybrid_equivalence_against_torch_projection():
+    """hidden(X) == KV(K = X W_K^T + b_K, V = X W_V^T + b_V) (north_star invariant),
+    with the twin K/V computed by torch float64 rather than by the oracle."""
+    d, n, H = 32, 21, 2
+    X, W, b, q = _rand((n, d), 23), _rand((2 * d, d), 24, 0.2), _rand(2 * d, 25, 0.02), _rand(d, 26)
+    tX, tW, tb = torch.tensor(X), torch.tensor(W), torch.tensor(b)
+    KV = torch.nn.functional.linear(tX, tW, tb).numpy()
+    oh, lh = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.25, b)
+    ok, lk = O.decode_batch([{"mode": 0, "q": q, "K": KV[:, :d], "V": KV[:, d:]}], W, H, 0.25)
+    assert np.allclose(oh, ok, atol=1e-13) and np.allclose(lh, lk, atol=1e-13)
+
+
+def test_lse_matches_scipy_logsumexp():
+    from scipy.special import logsumexp
+    d, n, H, sc = 16, 40, 4, 0.7
+    q, K, V = _rand(d, 27), _rand((n, d), 28), _rand((n, d), 29)
+    _, lse = O.attend(q, K, V, H, sc)
+    for h in range(H):
+        c = slice(h * 4, (h + 1) * 4)
+        assert abs(lse[h] - logsumexp(sc * K[:, c] @ q[c])) < 1e-13
+
+
+def test_order_of_tokens_is_irrelevant():
+    """Attention without positional terms is permutation-invariant over keys (block
+    indirection may store tokens anywhere; SURVEY §8(c) 'Block indirection')."""
+    d, n = 16, 25
+    q, K, V = _rand(d, 30), _rand((n, d), 31), _rand((n, d), 32)
+    p = np.random.default_rng(33).permutation(n)
+    a, la = O.attend(q, K, V, 2, 0.4)
+    b, lb = O.attend(q, K[p], V[p], 2, 0.4)
+    assert np.allclose(a, b, atol=1e-14) and np.allclose(la, lb, atol=1e-14)
+
+
+def test_max_rel_err_definition():
+    ref = np.array([[1.0, -2.0, 0.5, 0.25]])
+    gpu = ref + np.array([[0.0, 0.02, 0.0, 0.0025]])
+    # head 0 cols (1,-2): 0.02/2 = 0.01 ; head 1 cols (0.5,0.25): 0.0025/0.5 = 0.005
+    assert abs(O.max_rel_err(gpu, ref, 2) - 0.01) < 1e-15
+
+
+def test_zero_context_is_rejected():
+    with pytest.raises(AssertionError):
+        O.attend(np.zeros(4), np.zeros((0, 4)), np.zeros((0, 4)), 1, 1.0)
