@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Bench: one decode-step attention layer over the hybrid cache (Apt-Serve's hot path).
+
+Metric (BASELINE.json): decode-attention req-layers/s (+ HBM GB/s and tensor-core
+utilisation vs the roofline).  One step = one hc_decode_attention call over one batch:
+K/V reconstruction of hidden-mode requests (tcgen05 GEMM), split-K attention over KV and
+rebuilt K/V, split combine.  Default workload: cfg4 = OPT-66B layer shape, 256 requests,
+long contexts (lognormal, <= 4096), 50% hidden, bf16, on one B200.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg4|cfg2|cfg3|cfg5:<h>]
+  python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank processes its own
+full batch of the same recipe (request ids offset by rank), no data-path collective
+(task rule ⑤); the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def workload_from(name: str):
+    from synth import configs as C
+    return C.by_name(name)
+
+
+def algorithmic(w):
+    """bytes and FLOPs the method must move / compute (bf16: s = 2)."""
+    d, s = w.shape.d, w.elem_bytes
+    kv_tok = w.n_tokens(0)
+    hid_tok = w.n_tokens(1)
+    n_req = len(w.n)
+    bytes_ = kv_tok * 2 * d * s + hid_tok * d * s + (2 * d * d * s + 2 * d * 4 if hid_tok else 0) + 2 * n_req * d * s
+    flops = 4 * d * d * hid_tok
+    return bytes_, flops, kv_tok, hid_tok
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sms, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ============================================================================ reference arm
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+    from threadpoolctl import threadpool_info
+
+    from oracle import hc_oracle as O
+    from synth.configs import MODE_HIDDEN, MODE_KV
+
+    w = workload_from(args.config)
+    d, H = w.shape.d, w.shape.H
+    rs = np.random.default_rng(1234)
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
+    W = None
+    if hid:
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        W = w.w_kv(device=dev).cpu()   # synth is bit-identical on any device (tests/test_synth_device)
+    picks = []
+    for s in range(args.warmup + args.steps):
+        step = []
+        if kv:
+            step.append(int(rs.choice(kv)))
+        if hid:
+            step.append(int(rs.choice(hid)))
+        picks.append(step)
+    Wd = O._f64(W) if W is not None else None
+    t_total, n_done = 0.0, 0
+    for s, step in enumerate(picks):
+        reqs = []
+        for i in step:
+            r = {"q": w.q(i), "mode": w.modes[i]}
+            if w.modes[i] == MODE_KV:
+                r["K"], r["V"] = w.kv(i)
+            else:
+                r["X"] = w.x(i)
+            reqs.append(r)
+        t0 = time.perf_counter()
+        O.decode_batch(reqs, Wd, H, w.scale, w.b_kv())
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            t_total += dt
+            n_done += len(step)
+    cores = max([tp.get("num_threads", 1) for tp in threadpool_info()] + [1])
+    value = n_done / t_total if t_total > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "shape": w.shape.name, "n_req": len(w.n), "note": w.note},
+        "cpu_baseline": {"value": value, "unit": "req-layers/s", "cores": cores, "kind": "oracle",
+                         "sample": f"per step 1 KV + 1 hidden request of {w.name} drawn with seed 1234 "
+                                   f"(full heads, fp64 numpy oracle)"},
+        "e2e": {"value": value, "unit": "req-layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "decode-attention req-layers/s (hybrid KV/hidden cache, one layer)"
+
+
+# ============================================================================ CPU baseline
+def cpu_baseline(w, budget_s: float = 20.0):
+    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
+    import numpy as np
+    import torch
+    from threadpoolctl import threadpool_info
+
+    from oracle import hc_oracle as O
+    from synth.configs import MODE_HIDDEN, MODE_KV
+
+    H = w.shape.H
+    rs = np.random.default_rng(99)
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
+    Wd = O._f64(w.w_kv(device="cuda").cpu()) if hid else None
+    b = w.b_kv()
+    order = []
+    # alternate KV / hidden picks in the workload's proportion until the budget is spent
+    pool_kv, pool_h = list(rs.permutation(kv)) if kv else [], list(rs.permutation(hid)) if hid else []
+    t_used, n_kv, n_h = 0.0, 0, 0
+    t_kv, t_h = 0.0, 0.0
+    while t_used < budget_s and (pool_kv or pool_h):
+        for src, is_h in ((pool_kv, False), (pool_h, True)):
+            if not src or t_used >= budget_s:
+                continue
+            i = int(src.pop())
+            r = {"q": w.q(i), "mode": w.modes[i]}
+            if is_h:
+                r["X"] = w.x(i)
+            else:
+                r["K"], r["V"] = w.kv(i)
+            t0 = time.perf_counter()
+            O.decode_batch([r], Wd, H, w.scale, b)
+            dt = time.perf_counter() - t0
+            t_used += dt
+            if is_h:
+                n_h, t_h = n_h + 1, t_h + dt
+            else:
+                n_kv, t_kv = n_kv + 1, t_kv + dt
+            order.append(i)
+    # whole-batch extrapolation in the workload's own mix: per-request mean times
+    frac_h = len(hid) / len(w.n)
+    per_req = (1 - frac_h) * (t_kv / max(1, n_kv)) + frac_h * (t_h / max(1, n_h))
+    cores = max([tp.get("num_threads", 1) for tp in threadpool_info()] + [1])
+    return {"value": 1.0 / per_req if per_req > 0 else 0.0, "unit": "req-layers/s", "cores": cores,
+            "kind": "oracle",
+            "sample": f"{n_kv} KV + {n_h} hidden requests of {w.name} (seed 99, full heads, fp64 numpy), "
+                      f"{t_used:.1f} s; value = 1 / (mix-weighted mean time per request)"}
+
+
+# ============================================================================ main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hc", choices=["hc", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--split-tokens", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="run only N untimed steps (for ncu); prints nothing")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_07494_b200 import build as hb
+    hb.build()
+    from paper_2504_07494_b200 import hc
+    from synth import configs as C
+    from tests import hc_testlib as T
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w0 = workload_from(args.config)
+    w = C.shard_for_rank(w0, rank, world)
+    pool = T.make_pool(w, device=local, split_tokens=args.split_tokens)
+    T.fill(pool, w, device=local)
+    q = T.queries(w, device=local)
+    ids = list(w.req_ids)
+    n_req = len(ids)
+    out = torch.empty((n_req, w.shape.d), dtype=w.torch_dtype, device="cuda")
+    lse = torch.empty((n_req, w.shape.H), dtype=torch.float32, device="cuda")
+    ws = pool.workspace(ids)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        hc.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, stream)
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            step()
+        torch.cuda.synchronize()
+        return 0
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = pool.last_launch_count()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    pool.set_profiling(True)
+    pool.kernel_times()  # clear
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    kt = pool.kernel_times()
+    pool.set_profiling(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n_req / (ms / 1e3)
+
+    # ---- end to end through the public API: pinned host q -> device, decode, out -> host
+    e2e = None
+    if not args.no_e2e:
+        q_host = q.cpu().pin_memory()
+        out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+        q_dev = torch.empty_like(q)
+        for _ in range(2):
+            q_dev.copy_(q_host, non_blocking=True)
+            hc.hc_decode_attention(pool.handle, ids, q_dev, w.scale, out, lse, ws, stream)
+            out_host.copy_(out, non_blocking=True)
+            lse_host.copy_(lse, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            q_dev.copy_(q_host, non_blocking=True)
+            hc.hc_decode_attention(pool.handle, ids, q_dev, w.scale, out, lse, ws, stream)
+            out_host.copy_(out, non_blocking=True)
+            lse_host.copy_(lse, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": world * n_req / (ms_e2e / 1e3), "unit": "req-layers/s",
+               "h2d_bytes_per_step": q.numel() * q.element_size(),
+               "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size(),
+               "ms_per_step": ms_e2e}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peak_src = load_peaks()
+    B_alg, F_alg, kv_tok, hid_tok = algorithmic(w)
+    calls = max(1, kt["calls"])
+    t_rec, t_att, t_comb, t_up = (kt["recon_ms"] / calls, kt["attn_ms"] / calls, kt["combine_ms"] / calls,
+                                  kt["upload_ms"] / calls)
+    d, s = w.shape.d, w.elem_bytes
+    hbm = peaks["hbm_gbs"]
+    tf_burst, tf_sus = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    kernels = {
+        "recon_gemm": {"ms": t_rec, "bound": "tensor", "unit": "TFLOP/s",
+                       "achieved": (F_alg / (t_rec / 1e3) / 1e12) if t_rec > 0 else None,
+                       "flops_per_launch": F_alg},
+        "attention": {"ms": t_att, "bound": "hbm", "unit": "GB/s",
+                      "bytes_per_launch": (kv_tok + hid_tok) * 2 * d * s,
+                      "achieved": ((kv_tok + hid_tok) * 2 * d * s / (t_att / 1e3) / 1e9) if t_att > 0 else None},
+        "combine": {"ms": t_comb},
+        "descriptor_upload": {"ms": t_up},
+    }
+    dom = "recon_gemm" if t_rec >= t_att else "attention"
+    k = kernels[dom]
+    if dom == "recon_gemm":
+        peak = tf_sus
+        roof = {"bound": "tensor", "kernel": "recon_tc_kernel", "achieved": k["achieved"], "peak": peak,
+                "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get("recon"),
+                "peak_kind": "bf16 sustained, " + peak_src}
+    else:
+        peak = hbm
+        roof = {"bound": "hbm", "kernel": "attn_pipe_kernel", "achieved": k["achieved"], "peak": peak,
+                "unit": "GB/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get("attention"),
+                "peak_kind": "HBM copy, " + peak_src}
+    T_roof = max(F_alg / (tf_sus * 1e12), B_alg / (hbm * 1e9))
+    line = {
+        "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
+                   "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
+                   "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} (weak)",
+                   "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note},
+        "roofline": roof,
+        "step_roofline": {"T_roof_ms": T_roof * 1e3, "frac": T_roof * 1e3 / ms, "alg_bytes": B_alg,
+                          "alg_flops": F_alg, "alg_GBps": B_alg / (ms / 1e3) / 1e9,
+                          "alg_TFLOPs": F_alg / (ms / 1e3) / 1e12, "peaks": peak_src},
+        "kernels": kernels,
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ncu --set full per-launch DRAM traffic (bytes) of the dominant kernels, from the
+# committed profiles/ summaries; None until measured.
+TRAFFIC = {}
+_tp = os.path.join(ROOT, "profiles", "traffic.json")
+if os.path.exists(_tp):
+    try:
+        TRAFFIC = json.load(open(_tp))
+    except Exception:
+        TRAFFIC = {}
+
+if __name__ == "__main__":
+    sys.exit(main())

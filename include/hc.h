@@ -1,0 +1,161 @@
+/*
+ * hc.h — C ABI of the B200-native hybrid-cache decode-attention library (libhc.so).
+ *
+ * The method (Apt-Serve, arXiv 2504.07494; citations are /root/reference/PAPER.md line
+ * numbers "P:n" and SPEC.md lines "S:n"): every request i of a decode batch keeps,
+ * per layer, EITHER a KV cache (beta_i = 0) OR a hidden cache of the layer's input
+ * hidden states x_j (beta_i = 1; "Opportunity I", half the memory).
+ * One decode step of one attention layer computes, per request and head h,
+ *     hidden mode:  k_j = W_K x_j (+b_K),  v_j = W_V x_j (+b_V)   for all cached j  (Eq. 1)
+ *     a_j = softmax_j(scale * q_h . k_{j,h})                                           (Eq. 2)
+ *     out_{i,h} = sum_j a_j v_{j,h}         (Eq. 3 before W_o; v_i typo = v_j)
+ * over all n_i cached tokens INCLUDING the current one ("attending to ... itself").
+ * Cache storage is one unified pool of fixed-size blocks holding K, V or X vectors of
+ * B consecutive tokens of one request (§4.3; Fig. 6).
+ *
+ * Conventions
+ *  - Every call returns hc_status (HC_OK == 0) and never throws; hc_last_error() gives a
+ *    thread-local message for the last non-OK status.
+ *  - Validation errors are synchronous and leave the pool unchanged.  Launch failures
+ *    return HC_E_CUDA (device state then undefined for that call).
+ *  - One pool = one device.  Calls on a pool must be serialised by the caller (one host
+ *    thread at a time) and their device work must be ordered (pass the same stream, or
+ *    order the streams); device work is asynchronous on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream).
+ *  - The caller owns ALL device memory (pool storage, weights, q, out, lse, workspace);
+ *    the library borrows the pointers.  It owns only host metadata (free list, block
+ *    tables, a small ring of pinned staging buffers) — no hidden cudaMalloc.
+ *  - Element type of K/V/X/q/out/W is the pool dtype (bf16 or fp32); bias and lse are fp32.
+ */
+#ifndef HC_H_
+#define HC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HC_OK = 0,
+  HC_E_INVALID = 1,        /* bad argument: null pointer, n_req < 0, duplicate ids, n_i = 0 ... */
+  HC_E_OOM = 2,            /* not enough free unit blocks (append is all-or-nothing) */
+  HC_E_UNKNOWN_REQ = 3,    /* decode of an id the pool has never seen / has freed */
+  HC_E_MODE_MISMATCH = 4,  /* append with the other mode; switching = hc_free + re-append */
+  HC_E_CUDA = 5,           /* a CUDA runtime call or launch failed */
+  HC_E_UNSUPPORTED = 6,    /* shape / dtype combination not implemented */
+  HC_E_WORKSPACE = 7       /* workspace too small (see hc_workspace_size) */
+} hc_status;
+
+typedef enum { HC_MODE_KV = 0, HC_MODE_HIDDEN = 1 } hc_mode; /* beta_i = 0 / 1 */
+typedef enum { HC_BF16 = 0, HC_F32 = 1 } hc_dtype;
+
+/* hc_pool_config.flags */
+#define HC_FLAG_ACCOUNTING_ONLY 0x1 /* host allocator only: storage/w_kv may be NULL, no device
+                                       work; hc_decode_attention returns HC_E_UNSUPPORTED */
+#define HC_FLAG_FORCE_SIMT 0x2      /* rebuild K/V with the SIMT GEMM even in bf16 (cross-check) */
+#define HC_FLAG_GENERIC_ATTN 0x4    /* use the generic (unpipelined) attention kernel */
+
+typedef struct hc_pool hc_pool;
+
+typedef struct {
+  int32_t d_model;       /* d = n_heads * head_dim */
+  int32_t n_heads;       /* H; heads are contiguous head_dim-column slices of d (DESIGN R1) */
+  int32_t head_dim;      /* dh */
+  int32_t block_size;    /* B tokens per unit block (paper: fixed, unstated; default 16, R7) */
+  int64_t num_blocks;    /* unit blocks in the pool (each B*d elements) */
+  int32_t dtype;         /* hc_dtype */
+  int32_t flags;         /* HC_FLAG_* */
+  void* storage;         /* device buffer of hc_pool_storage_bytes() bytes, borrowed */
+  size_t storage_bytes;
+  const void* w_kv;      /* device [2d, d] row-major, rows = W_K (d rows) then W_V; k = W_K x.
+                            Copied once at create into head-interleaved order inside storage;
+                            may be freed after create. */
+  const float* b_kv;     /* nullable device [2d] fp32 bias (b_K then b_V); copied at create */
+  int32_t device;        /* CUDA device ordinal the storage lives on */
+  int32_t split_tokens;  /* split-K chunk in tokens (multiple of B); 0 = automatic */
+} hc_pool_config;
+
+/* Bytes of device storage a pool with this config needs: the unit blocks, the
+ * head-interleaved W_KV copy, the bias copy and the append staging area (256-B aligned).
+ * Returns 0 for an invalid config. */
+size_t hc_pool_storage_bytes(const hc_pool_config* cfg);
+
+/* Create a pool ("unified block-wise memory pool").  Zero-fills the block
+ * region (so padding rows of a partly filled block are finite), copies W_KV / b_KV into
+ * storage, and builds TMA descriptors.  Synchronous w.r.t. the device (cudaDeviceSynchronize
+ * on cfg->device).  Errors: HC_E_INVALID (null / inconsistent sizes, storage too small),
+ * HC_E_UNSUPPORTED (shape not implemented), HC_E_CUDA. */
+hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out);
+
+/* Destroy; does not free caller-owned device memory.  NULL is a no-op. */
+void hc_pool_destroy(hc_pool* pool);
+
+/* Append tokens (hidden-cache I/O; cache-map creation/extension).
+ * For each of the n_req DISTINCT requests, n_tokens[i] >= 0 new tokens are appended at
+ * the end of its cache in mode modes[i] (a new id is created with that mode).  Rows are
+ * device buffers packed in request order: `k`, `v` hold [sum over KV-mode requests of
+ * n_tokens, d]; `x` holds [sum over hidden-mode requests of n_tokens, d] (token-major,
+ * row-major).  Either of k/v or x may be NULL if no request of that mode is present.
+ * Block allocation: SPEC memory-pool contract — unit blocks, KV takes a K and a V block
+ * per B tokens, hidden one, new blocks only when the last is full,
+ * lowest free id first, K before V per logical block, requests in call order,
+ * ALL-OR-NOTHING over the whole call.  Errors: HC_E_INVALID, HC_E_OOM,
+ * HC_E_MODE_MISMATCH (pool unchanged), HC_E_CUDA.  Asynchronous on `stream`; host
+ * buffers k/v/x are NOT accepted. */
+hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                    const int32_t* n_tokens, const void* k, const void* v, const void* x,
+                    void* stream);
+
+/* Discard a request's cache (cache-type switch = discard + recompute).
+ * Unknown ids are an idempotent no-op.  *released_units (nullable) = unit blocks freed. */
+hc_status hc_free(hc_pool* pool, int64_t req_id, int64_t* released_units);
+
+/* Workspace bytes hc_decode_attention needs for this batch (descriptor, split partials,
+ * reconstructed-K/V scratch).  Returns 0 on invalid input (see hc_last_error). */
+size_t hc_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_ids);
+
+/* One decode-step attention layer over the hybrid cache (Eq. 1-3).
+ *   req_ids  host [n_req], distinct, known, each with n_i >= 1 (current token appended).
+ *   q        device [n_req, d] pool dtype, row i = query of req_ids[i].
+ *   scale    softmax scale (Eq. 2 uses 1/sqrt(d) for one head; multi-head 1/sqrt(dh), R1).
+ *   out      device [n_req, d] pool dtype: concat_h sum_j a_j v_{j,h} (pre-W_o).
+ *   lse      nullable device [n_req, H] fp32: log sum_j exp(scale q_h.k_j) (natural log).
+ *   workspace device, >= hc_workspace_size() bytes, 256-B aligned.
+ * Hidden-mode K/V are rebuilt by a tcgen05 GEMM (bf16 in, fp32 accumulate, bf16 out),
+ * then one split-K flash-decoding pass covers KV- and hidden-mode requests, then a
+ * split combine.  n_req = 0 is HC_OK and launches nothing.  Errors: HC_E_INVALID,
+ * HC_E_UNKNOWN_REQ, HC_E_WORKSPACE, HC_E_UNSUPPORTED, HC_E_CUDA. */
+hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
+                              const void* q, float scale, void* out, float* lse,
+                              void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- introspection (host-side, no device work) ------------------------------------ */
+int64_t hc_pool_num_free(const hc_pool* pool);
+/* mode (hc_mode), cached tokens and unit blocks of a request; HC_E_UNKNOWN_REQ if absent */
+hc_status hc_request_info(const hc_pool* pool, int64_t req_id, int32_t* mode, int64_t* n_tokens,
+                          int64_t* n_units);
+/* block ids of a request's cache map: kind 0 = K (or X for hidden), 1 = V.
+ * Writes min(count, cap) ids to out; *count = list length. */
+hc_status hc_request_blocks(const hc_pool* pool, int64_t req_id, int32_t kind, int32_t* out,
+                            int64_t cap, int64_t* count);
+
+/* ---- measurement hooks --------------------------------------------------------------- */
+/* Kernels launched by the last hc_decode_attention / hc_append call on this pool. */
+int32_t hc_last_launch_count(const hc_pool* pool);
+/* When enabled, hc_decode_attention records CUDA events around each of its kernels on
+ * the stream it launches them on.  hc_kernel_times() synchronises on all events recorded
+ * since the previous read and returns, summed over those calls, the milliseconds of
+ * [0] reconstruction GEMM, [1] attention, [2] combine, [3] descriptor upload, plus the
+ * number of calls in *n_calls; then it clears the record. */
+hc_status hc_set_profiling(hc_pool* pool, int32_t enable);
+hc_status hc_kernel_times(hc_pool* pool, float* ms4, int32_t* n_calls);
+
+const char* hc_last_error(void);
+const char* hc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HC_H_ */

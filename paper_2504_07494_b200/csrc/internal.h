@@ -1,0 +1,97 @@
+// Internal types shared by the host runtime (runtime.cu) and the kernels.
+// Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace hc {
+
+// Per-request entry of the decode-call descriptor (uploaded once per call).
+struct ReqDesc {
+  int32_t mode;          // 0 KV, 1 hidden (beta_i)
+  int32_t n;             // cached tokens incl. the current one
+  int32_t tab_off;       // KV: offset of (K,V) block-id pairs in the flat table
+  int32_t scratch_blk0;  // hidden: first scratch block of the rebuilt K/V
+  int32_t split_begin;   // first split of this request
+  int32_t split_count;
+  int32_t pad0, pad1;
+};
+
+// A split-K unit: tokens [lb0*B, lb0*B + ntok) of request `req`.
+struct SplitDesc {
+  int32_t req;
+  int32_t lb0;   // first logical block
+  int32_t ntok;  // tokens in this split (>= 1)
+  int32_t pad;
+};
+
+struct AttnParams {
+  const ReqDesc* reqs;
+  const SplitDesc* splits;
+  const int32_t* tables;  // KV (K id, V id) pairs per logical block
+  const void* pool;       // unit blocks; KV block layout [H][B][dh]
+  const void* scr_k;      // rebuilt K of hidden requests, [hblock][H][B][dh]
+  const void* scr_v;
+  const void* q;          // [n_req, d]
+  float* part_ml;         // [n_tasks][2]: running max (log2 domain), sum
+  float* part_acc;        // [n_tasks][dh]: unnormalised sum_j p_j v_j
+  int32_t* task_counter;  // zero on entry (part of the uploaded descriptor)
+  int32_t n_tasks;        // n_splits * H; task = split * H + head
+  int32_t H, dh, B, d;
+  float scale_log2;       // scale * log2(e)
+};
+
+struct CombineParams {
+  const ReqDesc* reqs;
+  const float* part_ml;
+  const float* part_acc;
+  void* out;   // [n_req, d]
+  float* lse;  // nullable [n_req, H]
+  int32_t n_req, H, dh, d;
+};
+
+struct ReconParams {
+  const int32_t* gather;  // pool block id of each hidden block (in scratch order)
+  int32_t n_hblocks;      // hidden blocks; GEMM rows M = n_hblocks * B
+  const void* pool;
+  const void* w_int;      // head-interleaved W_KV copy, [2d, d]: row h*2dh + kv*dh + c
+  const float* b_int;     // nullable, same interleaving
+  void* scr_k;
+  void* scr_v;
+  int32_t d, H, dh, B;
+};
+
+struct AppendReq {
+  int32_t mode;
+  int32_t start;    // tokens already cached
+  int32_t n_tok;    // rows appended
+  int32_t row_off;  // first source row in k/v (KV) or x (hidden)
+  int32_t tab_off;  // block ids covering logical blocks [start/B, (start+n_tok-1)/B];
+                    // KV: (K,V) pairs, hidden: single ids
+  int32_t pad0, pad1, pad2;
+};
+
+struct AppendParams {
+  const AppendReq* reqs;
+  const int32_t* tabs;
+  const void* k;
+  const void* v;
+  const void* x;
+  void* pool;
+  int32_t n_req, d, H, dh, B;
+};
+
+// dtype: 0 bf16, 1 fp32
+cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaStream_t s);
+cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d,
+                              int H, int dh, int dtype, cudaStream_t s);
+cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
+cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
+                            int num_sms, cudaStream_t s);
+bool recon_tc_supported(int d, int H, int dh, int B);
+cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s);
+bool attn_pipe_supported(int dtype, int dh, int B);
+cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
+
+}  // namespace hc

@@ -1,0 +1,143 @@
+// Cache append, weight re-layout, split combine (row a6).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace hc {
+
+namespace {
+
+// Block-wise cache write, "fusing reshaping with read/write": each appended row
+// goes to (table[pos / B], pos % B).  KV rows are scattered head-major ([H][B][dh] per
+// unit block, so a head's rows of a block are contiguous for the attention reads);
+// hidden rows are stored row-major ([B][d], the GEMM's gathered A operand).
+// 16-byte vectors; grid.y = request of the call, grid.x strides over its rows.
+template <typename T>
+__global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
+  const AppendReq rq = p.reqs[blockIdx.y];
+  constexpr int VE = 16 / sizeof(T);   // elements per vector
+  const int d = p.d, B = p.B, dh = p.dh;
+  const int nvec = d / VE;
+  T* pool = static_cast<T*>(p.pool);
+  const int lb_first = rq.start / B;
+  for (int r = blockIdx.x; r < rq.n_tok; r += gridDim.x) {
+    const int pos = rq.start + r;
+    const int lb = pos / B - lb_first, row = pos % B;
+    const size_t src_row = (size_t)(rq.row_off + r) * d;
+    if (rq.mode == 0) {
+      const int kb = p.tabs[rq.tab_off + 2 * lb], vb = p.tabs[rq.tab_off + 2 * lb + 1];
+      const uint4* ks = reinterpret_cast<const uint4*>(static_cast<const T*>(p.k) + src_row);
+      const uint4* vs = reinterpret_cast<const uint4*>(static_cast<const T*>(p.v) + src_row);
+      for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
+        const int col = e * VE, h = col / dh, c = col - h * dh;
+        const size_t off = (size_t)h * B * dh + (size_t)row * dh + c;
+        *reinterpret_cast<uint4*>(pool + (size_t)kb * B * d + off) = ks[e];
+        *reinterpret_cast<uint4*>(pool + (size_t)vb * B * d + off) = vs[e];
+      }
+    } else {
+      const int xb = p.tabs[rq.tab_off + lb];
+      const uint4* xs = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + src_row);
+      uint4* dst = reinterpret_cast<uint4*>(pool + (size_t)xb * B * d + (size_t)row * d);
+      for (int e = threadIdx.x; e < nvec; e += blockDim.x) dst[e] = xs[e];
+    }
+  }
+}
+
+// W_int[h*2dh + kv*dh + c, :] = W_KV[kv*d + h*dh + c, :]  (and the bias likewise): one
+// N=256 GEMM tile of the head-interleaved weight then yields K_h || V_h directly.
+template <typename T>
+__global__ void __launch_bounds__(256) relayout_kernel(const T* __restrict__ w, T* __restrict__ wi,
+                                                       const float* __restrict__ b, float* __restrict__ bi,
+                                                       int d, int dh) {
+  const int dst = blockIdx.x;   // 0 .. 2d-1
+  const int h = dst / (2 * dh), rem = dst - h * 2 * dh, kv = rem / dh, c = rem - kv * dh;
+  const int src = kv * d + h * dh + c;
+  constexpr int VE = 16 / sizeof(T);
+  const uint4* s = reinterpret_cast<const uint4*>(w + (size_t)src * d);
+  uint4* o = reinterpret_cast<uint4*>(wi + (size_t)dst * d);
+  for (int e = threadIdx.x; e < d / VE; e += blockDim.x) o[e] = s[e];
+  if (threadIdx.x == 0 && bi != nullptr) bi[dst] = b ? b[src] : 0.f;
+}
+
+template <typename T>
+__device__ __forceinline__ void st_out(T* p, float v);
+template <>
+__device__ __forceinline__ void st_out<float>(float* p, float v) {
+  *p = v;
+}
+template <>
+__device__ __forceinline__ void st_out<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+  *p = __float2bfloat16_rn(v);
+}
+
+// Split combine: M = max_s m_s, L = sum_s 2^(m_s-M) l_s, out = sum_s 2^(m_s-M) acc_s / L,
+// lse = (M + log2 L) ln 2 (scores were kept in log2 units).  One warp per (request, head).
+template <typename T>
+__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= p.n_req * p.H) return;
+  const int r = w / p.H, h = w - r * p.H;
+  const ReqDesc rq = p.reqs[r];
+  const int H = p.H, dh = p.dh;
+  float M = -INFINITY;
+  for (int s = lane; s < rq.split_count; s += 32)
+    M = fmaxf(M, p.part_ml[2 * ((size_t)(rq.split_begin + s) * H + h)]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f;
+  for (int s = lane; s < rq.split_count; s += 32) {
+    const size_t t = (size_t)(rq.split_begin + s) * H + h;
+    L += exp2f(p.part_ml[2 * t] - M) * p.part_ml[2 * t + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  const float inv = 1.f / L;
+  T* out = static_cast<T*>(p.out) + (size_t)r * p.d + h * dh;
+  for (int c = lane; c < dh; c += 32) {
+    float o = 0.f;
+    for (int s = 0; s < rq.split_count; ++s) {
+      const size_t t = (size_t)(rq.split_begin + s) * H + h;
+      o += exp2f(p.part_ml[2 * t] - M) * p.part_acc[t * dh + c];
+    }
+    st_out<T>(out + c, o * inv);
+  }
+  if (lane == 0 && p.lse) p.lse[(size_t)r * H + h] = (M + log2f(L)) * 0.69314718055994531f;
+}
+
+}  // namespace
+
+cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaStream_t s) {
+  if (p.n_req <= 0 || max_rows <= 0) return cudaSuccess;
+  dim3 grid(max_rows < 1024 ? max_rows : 1024, p.n_req);
+  if (dtype == 1)
+    append_kernel<float><<<grid, 256, 0, s>>>(p);
+  else
+    append_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d, int H,
+                              int dh, int dtype, cudaStream_t s) {
+  (void)H;
+  if (dtype == 1)
+    relayout_kernel<float><<<2 * d, 256, 0, s>>>(static_cast<const float*>(w), static_cast<float*>(w_int),
+                                                 b, b_int, d, dh);
+  else
+    relayout_kernel<__nv_bfloat16><<<2 * d, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(w),
+                                                         static_cast<__nv_bfloat16*>(w_int), b, b_int, d, dh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s) {
+  const int warps = p.n_req * p.H;
+  if (warps <= 0) return cudaSuccess;
+  const int blocks = (warps + 3) / 4;
+  if (dtype == 1)
+    combine_kernel<float><<<blocks, 128, 0, s>>>(p);
+  else
+    combine_kernel<__nv_bfloat16><<<blocks, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace hc

@@ -1,0 +1,259 @@
+// tcgen05 / TMEM / TMA K/V reconstruction GEMM for sm_100a.
+//
+//   [K || V] = X W_KV^T (+ b)                       Eq. 1 on every cached x_j
+//
+// M = rows of the gathered hidden blocks (sum over hidden requests of ceil(n_i/B)*B),
+// N = 2d, K = d.  The hidden cache's "extra linear transformation cost" (t = rho m,
+// P:308-311) is exactly this contraction: 4 d^2 FLOPs per cached hidden token, so it
+// runs on the 5th-generation tensor cores.
+//
+// Design (one CTA per SM, persistent, warp-specialised, 192 threads):
+//   warp 0      TMA producer.  A tile = 128 gathered rows x 64 k: 128/min(B,128) boxes of
+//               [min(B,128) rows x 64] bf16, one per hidden block (the block-wise hidden
+//               cache is the A operand — no gather copy), SWIZZLE_128B.  B tile = 256 rows
+//               of the head-interleaved W_KV (K_h || V_h for 128-wide heads) x 64 k.
+//               4-stage smem ring (48 KiB/stage), full/empty mbarriers.
+//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.mma.cta_group::1
+//               kind::f16, M=128 N=256 K=16, fp32 accumulators in TMEM, two accumulator
+//               buffers (2 x 256 columns) so the epilogue of tile i overlaps tile i+1.
+//               tcgen05.commit releases smem stages / signals the epilogue.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (thread = one output row), + bias,
+//               RNE to bf16, store K_h and V_h rows into scratch blocks [hblock][H][B][dh].
+// Tile order: grouped rasterisation (GROUP_M m-tiles sweep all n-tiles) so a wave of 148
+// tiles shares A and W_KV tiles in L2 (W_KV is 340 MB at OPT-66B, larger than L2).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace hc {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;      // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;      // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int GROUP_M = 16;
+constexpr int TMEM_COLS = 512;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+struct TcArgs {
+  const int32_t* gather;
+  int32_t n_hblocks, M, B, rows_per_box;
+  int32_t m_tiles, n_tiles, k_iters;
+  int32_t H, dh, d;
+  __nv_bfloat16* scr_k;
+  __nv_bfloat16* scr_v;
+  const float* bias;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& mt, int& nt) {
+  const int per_group = GROUP_M * n_tiles;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gsize = min(GROUP_M, m_tiles - first_m);
+  const int r = t - g * per_group;
+  mt = first_m + r % gsize;
+  nt = r / gsize;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    recon_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                    const TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+  uint8_t* sA = smem;                              // STAGES x 16 KiB
+  uint8_t* sB = smem + STAGES * A_BYTES;           // STAGES x 32 KiB
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles_total = a.m_tiles * a.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_x);
+    ptx::prefetch_tmap(&tmap_w);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol_w = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      const int nbox = BM / a.rows_per_box;
+      const int box_bytes = a.rows_per_box * BK * 2;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        int mt, nt;
+        tile_coords(t, a.m_tiles, a.n_tiles, mt, nt);
+        // physical pool rows of this m-tile's boxes (gathered hidden blocks)
+        int prow[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          prow[i] = 0;
+          if (i < nbox) {
+            const int grow = mt * BM + i * a.rows_per_box;
+            const int g = grow / a.B;
+            if (g < a.n_hblocks) prow[i] = a.gather[g] * a.B + (grow - g * a.B);
+          }
+        }
+        for (int kb = 0; kb < a.k_iters; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* dA = sA + stage * A_BYTES;
+          for (int i = 0; i < nbox; ++i)
+            ptx::tma_load_2d(dA + i * box_bytes, &tmap_x, kb * BK, prow[i], &full[stage]);
+          ptx::tma_load_2d_hint(sB + stage * B_BYTES, &tmap_w, kb * BK, nt * BN, &full[stage], pol_w);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc_bf16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < a.k_iters; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = ptx::umma_desc_k_sw128(a_addr + k * 32);
+            const uint64_t bd = ptx::umma_desc_k_sw128(b_addr + k * 32);
+            ptx::umma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int row_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+      int mt, nt;
+      tile_coords(t, a.m_tiles, a.n_tiles, mt, nt);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int grow = mt * BM + row_in_tile;
+      const bool valid = grow < a.M;
+      const int g = grow / a.B, r = grow - g * a.B;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        ptx::tmem_ld_wait();
+        const int n = nt * BN + c * 32;            // interleaved output column
+        const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        if (a.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += __ldg(a.bias + n + j);
+        }
+        if (valid) {
+          __nv_bfloat16* dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            d4[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+                               pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+}  // namespace
+
+bool recon_tc_supported(int d, int H, int dh, int B) {
+  if (d % BK != 0 || d != H * dh) return false;
+  if ((2 * dh) > BN || BN % (2 * dh) != 0 || dh % 32 != 0) return false;
+  if ((2 * d) % BN != 0) return false;
+  if (B < 8 || (B & (B - 1)) != 0) return false;  // power of two >= 8: boxes are whole swizzle atoms
+  if (B > BM && B % BM != 0) return false;
+  return true;
+}
+
+cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w, int num_sms,
+                            cudaStream_t s) {
+  if (p.n_hblocks <= 0) return cudaSuccess;
+  TcArgs a;
+  a.gather = p.gather;
+  a.n_hblocks = p.n_hblocks;
+  a.B = p.B;
+  a.M = p.n_hblocks * p.B;
+  a.rows_per_box = p.B < BM ? p.B : BM;
+  a.m_tiles = (a.M + BM - 1) / BM;
+  a.n_tiles = 2 * p.d / BN;
+  a.k_iters = p.d / BK;
+  a.H = p.H;
+  a.dh = p.dh;
+  a.d = p.d;
+  a.scr_k = static_cast<__nv_bfloat16*>(p.scr_k);
+  a.scr_v = static_cast<__nv_bfloat16*>(p.scr_v);
+  a.bias = p.b_int;
+  cudaError_t e = cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  recon_tc_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
+                                                      *static_cast<const CUtensorMap*>(tmap_w), a);
+  return cudaGetLastError();
+}
+
+}  // namespace hc

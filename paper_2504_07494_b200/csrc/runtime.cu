@@ -1,0 +1,664 @@
+// Host runtime behind the C ABI (include/hc.h): unit-block pool allocator and block
+// tables, append (a2), decode-call descriptor / split-K work list
+// (a3) and launch sequencing of the reconstruction GEMM (a4), attention (a5) and
+// combine (a6).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <queue>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/hc.h"
+#include "internal.h"
+
+using namespace hc;
+
+namespace {
+
+thread_local std::string g_err;
+
+hc_status fail(hc_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+hc_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(HC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr size_t kStagingBytes = 4u << 20;  // append descriptor staging inside storage
+constexpr int kRing = 4;                      // pinned host staging buffers
+
+struct Req {
+  int32_t mode = 0;
+  int64_t n = 0;
+  std::vector<int32_t> a;  // K blocks (KV) or X blocks (hidden)
+  std::vector<int32_t> b;  // V blocks (KV)
+};
+
+struct Layout {  // storage layout
+  size_t blocks_off, blocks_bytes, w_off, w_bytes, b_off, b_bytes, stage_off, total;
+};
+
+bool layout_for(const hc_pool_config* c, Layout* L) {
+  if (!c || c->d_model <= 0 || c->n_heads <= 0 || c->head_dim <= 0 || c->block_size <= 0 ||
+      c->num_blocks <= 0 || (c->dtype != HC_BF16 && c->dtype != HC_F32))
+    return false;
+  if ((int64_t)c->n_heads * c->head_dim != c->d_model) return false;
+  const size_t e = c->dtype == HC_BF16 ? 2 : 4;
+  const size_t d = (size_t)c->d_model;
+  L->blocks_off = 0;
+  L->blocks_bytes = (size_t)c->num_blocks * c->block_size * d * e;
+  L->w_off = align_up(L->blocks_off + L->blocks_bytes, 1024);
+  L->w_bytes = 2 * d * d * e;
+  L->b_off = align_up(L->w_off + L->w_bytes, kAlign);
+  L->b_bytes = 2 * d * sizeof(float);
+  L->stage_off = align_up(L->b_off + L->b_bytes, kAlign);
+  L->total = align_up(L->stage_off + kStagingBytes, kAlign);
+  return true;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_tmap_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                  uint32_t box_outer) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+struct Pinned {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+
+// Decode-call plan: sizes and offsets inside the caller's workspace.
+struct Plan {
+  int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1;
+  int64_t n_tab = 0;
+  size_t off_reqs, off_splits, off_tabs, off_gather, desc_bytes;
+  size_t off_ml, off_acc, off_sk, off_sv, total;
+};
+
+}  // namespace
+
+struct hc_pool {
+  hc_pool_config cfg{};
+  Layout L{};
+  size_t elem = 2;
+  bool accounting = false;
+  bool has_bias = false;
+  char* storage = nullptr;
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_ids;
+  std::unordered_map<int64_t, Req> reqs;
+  CUtensorMap tmap_x{}, tmap_w{};
+  bool tc_ok = false;
+  int num_sms = 148;
+  std::array<Pinned, kRing> ring{};
+  int ring_next = 0;
+  int32_t last_launches = 0;
+  bool profiling = false;
+  std::vector<std::array<cudaEvent_t, 5>> prof_pending;
+  std::vector<cudaEvent_t> ev_free;
+
+  ~hc_pool() {
+    for (auto& p : ring) {
+      if (p.ev) {
+        cudaEventSynchronize(p.ev);
+        cudaEventDestroy(p.ev);
+      }
+      if (p.ptr) cudaFreeHost(p.ptr);
+    }
+    for (auto& a : prof_pending)
+      for (auto e : a) cudaEventDestroy(e);
+    for (auto e : ev_free) cudaEventDestroy(e);
+  }
+
+  // pinned staging buffer of >= bytes; waits only if its previous copy is still queued
+  Pinned* pinned(size_t bytes) {
+    Pinned* p = &ring[ring_next];
+    ring_next = (ring_next + 1) % kRing;
+    if (p->pending) {
+      cudaEventSynchronize(p->ev);
+      p->pending = false;
+    }
+    if (!p->ev && cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (p->cap < bytes) {
+      if (p->ptr) cudaFreeHost(p->ptr);
+      p->ptr = nullptr;
+      size_t cap = std::max<size_t>(bytes, 1 << 16);
+      cap = align_up(cap + cap / 2, 4096);
+      if (cudaMallocHost(&p->ptr, cap) != cudaSuccess) {
+        p->cap = 0;
+        return nullptr;
+      }
+      p->cap = cap;
+    }
+    return p;
+  }
+
+  cudaEvent_t get_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+
+  int32_t split_tokens_auto(const std::vector<const Req*>& rs) const {
+    const int B = cfg.block_size, H = cfg.n_heads;
+    int spb = std::max(1, 256 / B);
+    const int64_t target = 4LL * num_sms * 6;  // ~4 tasks per resident warp
+    while (spb > 1) {
+      int64_t ns = 0;
+      for (auto* r : rs) ns += cdiv(cdiv(r->n, B), spb);
+      if (ns * H >= target) break;
+      spb /= 2;
+    }
+    return spb;
+  }
+
+  Plan plan(const std::vector<const Req*>& rs) const {
+    Plan P;
+    const int B = cfg.block_size, H = cfg.n_heads, dh = cfg.head_dim;
+    P.n_req = (int32_t)rs.size();
+    P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
+    for (auto* r : rs) {
+      const int64_t nb = cdiv(r->n, B);
+      P.n_splits += (int32_t)cdiv(nb, P.split_blocks);
+      if (r->mode == HC_MODE_KV) P.n_tab += 2 * nb;
+      else P.n_hb += (int32_t)nb;
+    }
+    size_t o = 16;  // header: task counter + pad
+    P.off_reqs = o = align_up(o, 64);
+    o += sizeof(ReqDesc) * P.n_req;
+    P.off_splits = o = align_up(o, 64);
+    o += sizeof(SplitDesc) * P.n_splits;
+    P.off_tabs = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_tab;
+    P.off_gather = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_hb;
+    P.desc_bytes = align_up(o, kAlign);
+    const size_t n_tasks = (size_t)P.n_splits * H;
+    P.off_ml = P.desc_bytes;
+    P.off_acc = align_up(P.off_ml + n_tasks * 2 * sizeof(float), kAlign);
+    const size_t scr = (size_t)P.n_hb * H * B * dh * elem;
+    P.off_sk = align_up(P.off_acc + n_tasks * dh * sizeof(float), 1024);
+    P.off_sv = align_up(P.off_sk + scr, 1024);
+    P.total = align_up(P.off_sv + scr, kAlign);
+    return P;
+  }
+};
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* hc_last_error(void) { return g_err.c_str(); }
+const char* hc_version(void) { return "hc 0.1 (sm_100a)"; }
+
+size_t hc_pool_storage_bytes(const hc_pool_config* cfg) {
+  Layout L;
+  if (!layout_for(cfg, &L)) {
+    g_err = "invalid pool config";
+    return 0;
+  }
+  return L.total;
+}
+
+hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
+  if (!out) return fail(HC_E_INVALID, "out is null");
+  *out = nullptr;
+  Layout L;
+  if (!layout_for(cfg, &L)) return fail(HC_E_INVALID, "invalid pool config (d = H*dh, positive sizes, dtype)");
+  const size_t e = cfg->dtype == HC_BF16 ? 2 : 4;
+  if ((cfg->head_dim * e) % 16 != 0)
+    return fail(HC_E_UNSUPPORTED, "head_dim * element size must be a multiple of 16 bytes");
+  if (cfg->num_blocks > INT32_MAX || (int64_t)cfg->num_blocks * cfg->block_size > INT32_MAX)
+    return fail(HC_E_UNSUPPORTED, "num_blocks * block_size must fit in int32");
+  const bool accounting = (cfg->flags & HC_FLAG_ACCOUNTING_ONLY) != 0;
+  if (!accounting) {
+    if (!cfg->storage || cfg->storage_bytes < L.total)
+      return fail(HC_E_INVALID, "storage null or smaller than hc_pool_storage_bytes()");
+    if (reinterpret_cast<uintptr_t>(cfg->storage) % 1024 != 0)
+      return fail(HC_E_INVALID, "storage must be 1024-byte aligned");
+    if (!cfg->w_kv) return fail(HC_E_INVALID, "w_kv is null");
+  }
+  hc_pool* p = new hc_pool();
+  p->cfg = *cfg;
+  p->L = L;
+  p->elem = e;
+  p->accounting = accounting;
+  p->has_bias = cfg->b_kv != nullptr;
+  for (int32_t i = 0; i < (int32_t)cfg->num_blocks; ++i) p->free_ids.push(i);
+  if (!accounting) {
+    DeviceGuard g(cfg->device);
+    p->storage = static_cast<char*>(cfg->storage);
+    cudaDeviceProp prop;
+    cudaError_t err = cudaGetDeviceProperties(&prop, cfg->device);
+    if (err != cudaSuccess) {
+      delete p;
+      return cuda_fail(err, "cudaGetDeviceProperties");
+    }
+    p->num_sms = prop.multiProcessorCount;
+    err = cudaMemset(p->storage + L.blocks_off, 0, L.blocks_bytes);
+    if (err == cudaSuccess)
+      err = launch_relayout_w(cfg->w_kv, p->storage + L.w_off, cfg->b_kv, reinterpret_cast<float*>(p->storage + L.b_off),
+                              cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->dtype, 0);
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) {
+      delete p;
+      return cuda_fail(err, "pool init");
+    }
+    if (cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) &&
+        recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)) {
+      const uint32_t rpb = (uint32_t)std::min(cfg->block_size, 128);
+      const bool ok1 = make_tmap_2d(&p->tmap_x, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
+                                    (uint64_t)cfg->num_blocks * cfg->block_size, 64, rpb);
+      const bool ok2 = make_tmap_2d(&p->tmap_w, p->storage + L.w_off, (uint64_t)cfg->d_model,
+                                    2 * (uint64_t)cfg->d_model, 64, 256);
+      if (!ok1 || !ok2) {
+        delete p;
+        return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed");
+      }
+      p->tc_ok = true;
+    }
+  }
+  *out = p;
+  return HC_OK;
+}
+
+void hc_pool_destroy(hc_pool* pool) {
+  if (!pool) return;
+  DeviceGuard g(pool->cfg.device);
+  delete pool;
+}
+
+int64_t hc_pool_num_free(const hc_pool* pool) { return pool ? (int64_t)pool->free_ids.size() : -1; }
+
+hc_status hc_request_info(const hc_pool* pool, int64_t id, int32_t* mode, int64_t* n_tokens, int64_t* n_units) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  auto it = pool->reqs.find(id);
+  if (it == pool->reqs.end()) return fail(HC_E_UNKNOWN_REQ, "unknown request id");
+  if (mode) *mode = it->second.mode;
+  if (n_tokens) *n_tokens = it->second.n;
+  if (n_units) *n_units = (int64_t)(it->second.a.size() + it->second.b.size());
+  return HC_OK;
+}
+
+hc_status hc_request_blocks(const hc_pool* pool, int64_t id, int32_t kind, int32_t* out, int64_t cap,
+                            int64_t* count) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  auto it = pool->reqs.find(id);
+  if (it == pool->reqs.end()) return fail(HC_E_UNKNOWN_REQ, "unknown request id");
+  const std::vector<int32_t>& v = kind == 0 ? it->second.a : it->second.b;
+  if (count) *count = (int64_t)v.size();
+  if (out)
+    for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); ++i) out[i] = v[i];
+  return HC_OK;
+}
+
+hc_status hc_free(hc_pool* pool, int64_t id, int64_t* released) {
+  if (released) *released = 0;
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  auto it = pool->reqs.find(id);
+  if (it == pool->reqs.end()) return HC_OK;  // idempotent
+  for (int32_t b : it->second.a) pool->free_ids.push(b);
+  for (int32_t b : it->second.b) pool->free_ids.push(b);
+  if (released) *released = (int64_t)(it->second.a.size() + it->second.b.size());
+  pool->reqs.erase(it);
+  return HC_OK;
+}
+
+hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                    const int32_t* n_tokens, const void* k, const void* v, const void* x, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req == 0) return HC_OK;
+  if (!req_ids || !modes || !n_tokens) return fail(HC_E_INVALID, "null id/mode/n_tokens array");
+  const int B = pool->cfg.block_size;
+  std::unordered_set<int64_t> seen;
+  int64_t need = 0, kv_rows = 0, x_rows = 0;
+  for (int32_t i = 0; i < n_req; ++i) {
+    if (!seen.insert(req_ids[i]).second) return fail(HC_E_INVALID, "duplicate request id in append");
+    if (modes[i] != HC_MODE_KV && modes[i] != HC_MODE_HIDDEN) return fail(HC_E_INVALID, "bad mode");
+    if (n_tokens[i] < 0) return fail(HC_E_INVALID, "n_tokens < 0");
+    int64_t n0 = 0;
+    auto it = pool->reqs.find(req_ids[i]);
+    if (it != pool->reqs.end()) {
+      if (it->second.mode != modes[i])
+        return fail(HC_E_MODE_MISMATCH, "request exists with the other cache mode (switch = free + re-append)");
+      n0 = it->second.n;
+    }
+    if (n0 + n_tokens[i] > INT32_MAX) return fail(HC_E_INVALID, "context too long");
+    const int64_t per = cdiv(n0 + n_tokens[i], B) - cdiv(n0, B);
+    need += modes[i] == HC_MODE_KV ? 2 * per : per;
+    (modes[i] == HC_MODE_KV ? kv_rows : x_rows) += n_tokens[i];
+  }
+  if (need > (int64_t)pool->free_ids.size()) return fail(HC_E_OOM, "not enough free blocks (all-or-nothing)");
+  if (!pool->accounting && ((kv_rows > 0 && (!k || !v)) || (x_rows > 0 && !x)))
+    return fail(HC_E_INVALID, "k/v or x is null while rows of that mode are appended");
+
+  // ---- allocate (lowest free id first; K then V per logical block; call order) ----
+  std::vector<AppendReq> ar;
+  std::vector<int32_t> tabs;
+  ar.reserve(n_req);
+  int32_t kv_off = 0, x_off = 0, max_rows = 0;
+  for (int32_t i = 0; i < n_req; ++i) {
+    Req& r = pool->reqs[req_ids[i]];
+    if (r.n == 0 && r.a.empty()) r.mode = modes[i];
+    const int64_t t = n_tokens[i];
+    const int64_t new_lb = cdiv(r.n + t, B) - cdiv(r.n, B);
+    for (int64_t j = 0; j < new_lb; ++j) {
+      r.a.push_back(pool->free_ids.top());
+      pool->free_ids.pop();
+      if (r.mode == HC_MODE_KV) {
+        r.b.push_back(pool->free_ids.top());
+        pool->free_ids.pop();
+      }
+    }
+    if (t > 0) {
+      AppendReq q{};
+      q.mode = r.mode;
+      q.start = (int32_t)r.n;
+      q.n_tok = (int32_t)t;
+      q.row_off = r.mode == HC_MODE_KV ? kv_off : x_off;
+      q.tab_off = (int32_t)tabs.size();
+      const int64_t lb0 = r.n / B, lb1 = (r.n + t - 1) / B;
+      for (int64_t lb = lb0; lb <= lb1; ++lb) {
+        tabs.push_back(r.a[lb]);
+        if (r.mode == HC_MODE_KV) tabs.push_back(r.b[lb]);
+      }
+      ar.push_back(q);
+      max_rows = std::max<int32_t>(max_rows, (int32_t)t);
+      (r.mode == HC_MODE_KV ? kv_off : x_off) += (int32_t)t;
+    }
+    r.n += t;
+  }
+  if (pool->accounting || ar.empty()) return HC_OK;
+
+  // ---- upload descriptor(s) and scatter (chunked to the staging area) ----
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* staging = pool->storage + pool->L.stage_off;
+  size_t i0 = 0;
+  while (i0 < ar.size()) {
+    // largest prefix [i0, i1) whose descriptor fits the staging area
+    size_t i1 = i0, tab_lo = ar[i0].tab_off;
+    size_t bytes_req = 0, bytes_tab = 0;
+    int32_t rows = 0;
+    while (i1 < ar.size()) {
+      const size_t tab_hi = (i1 + 1 < ar.size()) ? ar[i1 + 1].tab_off : tabs.size();
+      const size_t nb_req = align_up((i1 - i0 + 1) * sizeof(AppendReq), 64);
+      const size_t nb_tab = (tab_hi - tab_lo) * sizeof(int32_t);
+      if (i1 > i0 && nb_req + nb_tab > kStagingBytes) break;
+      bytes_req = nb_req;
+      bytes_tab = nb_tab;
+      rows = std::max(rows, ar[i1].n_tok);
+      ++i1;
+    }
+    if (bytes_req + bytes_tab > kStagingBytes) return fail(HC_E_UNSUPPORTED, "append descriptor too large");
+    Pinned* pin = pool->pinned(bytes_req + bytes_tab);
+    if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+    AppendReq* hr = static_cast<AppendReq*>(pin->ptr);
+    for (size_t i = i0; i < i1; ++i) {
+      hr[i - i0] = ar[i];
+      hr[i - i0].tab_off = (int32_t)(ar[i].tab_off - tab_lo);
+    }
+    std::memcpy(static_cast<char*>(pin->ptr) + bytes_req, tabs.data() + tab_lo, bytes_tab);
+    cudaError_t err = cudaMemcpyAsync(staging, pin->ptr, bytes_req + bytes_tab, cudaMemcpyHostToDevice, s);
+    if (err != cudaSuccess) return cuda_fail(err, "append descriptor upload");
+    cudaEventRecord(pin->ev, s);
+    pin->pending = true;
+    AppendParams ap;
+    ap.reqs = reinterpret_cast<const AppendReq*>(staging);
+    ap.tabs = reinterpret_cast<const int32_t*>(staging + bytes_req);
+    ap.k = k;
+    ap.v = v;
+    ap.x = x;
+    ap.pool = pool->storage + pool->L.blocks_off;
+    ap.n_req = (int32_t)(i1 - i0);
+    ap.d = pool->cfg.d_model;
+    ap.H = pool->cfg.n_heads;
+    ap.dh = pool->cfg.head_dim;
+    ap.B = B;
+    err = launch_append(ap, pool->cfg.dtype, rows, s);
+    if (err != cudaSuccess) return cuda_fail(err, "append kernel");
+    ++pool->last_launches;
+    i0 = i1;
+  }
+  return HC_OK;
+}
+
+static hc_status collect(const hc_pool* pool, int32_t n_req, const int64_t* ids, std::vector<const Req*>* rs) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req > 0 && !ids) return fail(HC_E_INVALID, "req_ids is null");
+  std::unordered_set<int64_t> seen;
+  rs->reserve(n_req);
+  for (int32_t i = 0; i < n_req; ++i) {
+    if (!seen.insert(ids[i]).second) return fail(HC_E_INVALID, "duplicate request id in decode batch");
+    auto it = pool->reqs.find(ids[i]);
+    if (it == pool->reqs.end()) return fail(HC_E_UNKNOWN_REQ, "unknown request id " + std::to_string(ids[i]));
+    if (it->second.n < 1) return fail(HC_E_INVALID, "request has no cached token (append the current one first, P:135)");
+    rs->push_back(&it->second);
+  }
+  return HC_OK;
+}
+
+size_t hc_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_ids) {
+  std::vector<const Req*> rs;
+  if (collect(pool, n_req, req_ids, &rs) != HC_OK) return 0;
+  if (n_req == 0) return kAlign;
+  return pool->plan(rs).total;
+}
+
+hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const void* q, float scale,
+                              void* out, float* lse, void* workspace, size_t ws_bytes, void* stream) {
+  if (pool) pool->last_launches = 0;
+  std::vector<const Req*> rs;
+  hc_status st = collect(pool, n_req, req_ids, &rs);
+  if (st != HC_OK) return st;
+  if (n_req == 0) return HC_OK;
+  if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
+  if (!q || !out || !workspace) return fail(HC_E_INVALID, "q/out/workspace is null");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return fail(HC_E_INVALID, "workspace must be 256-B aligned");
+  const Plan P = pool->plan(rs);
+  if (ws_bytes < P.total) return fail(HC_E_WORKSPACE, "workspace smaller than hc_workspace_size()");
+  const int B = pool->cfg.block_size, H = pool->cfg.n_heads;
+
+  // ---- descriptor (a3): requests, split-K work list, KV block tables, hidden gather list
+  Pinned* pin = pool->pinned(P.desc_bytes);
+  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  char* h = static_cast<char*>(pin->ptr);
+  std::memset(h, 0, 16);  // task counter = 0
+  ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + P.off_reqs);
+  SplitDesc* sd = reinterpret_cast<SplitDesc*>(h + P.off_splits);
+  int32_t* tab = reinterpret_cast<int32_t*>(h + P.off_tabs);
+  int32_t* gat = reinterpret_cast<int32_t*>(h + P.off_gather);
+  int32_t n_split = 0, n_tab = 0, n_hb = 0;
+  for (int32_t i = 0; i < n_req; ++i) {
+    const Req& r = *rs[i];
+    const int32_t nb = (int32_t)cdiv(r.n, B);
+    ReqDesc d{};
+    d.mode = r.mode;
+    d.n = (int32_t)r.n;
+    d.split_begin = n_split;
+    if (r.mode == HC_MODE_KV) {
+      d.tab_off = n_tab;
+      for (int32_t lb = 0; lb < nb; ++lb) {
+        tab[n_tab++] = r.a[lb];
+        tab[n_tab++] = r.b[lb];
+      }
+    } else {
+      d.scratch_blk0 = n_hb;
+      for (int32_t lb = 0; lb < nb; ++lb) gat[n_hb++] = r.a[lb];
+    }
+    for (int32_t lb = 0; lb < nb; lb += P.split_blocks) {
+      SplitDesc s{};
+      s.req = i;
+      s.lb0 = lb;
+      const int64_t t0 = (int64_t)lb * B;
+      s.ntok = (int32_t)std::min<int64_t>((int64_t)P.split_blocks * B, r.n - t0);
+      sd[n_split++] = s;
+    }
+    d.split_count = n_split - d.split_begin;
+    rd[i] = d;
+  }
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::array<cudaEvent_t, 5> ev{};
+  if (pool->profiling) {
+    for (auto& e : ev) e = pool->get_event();
+    cudaEventRecord(ev[0], s);
+  }
+  char* ws = static_cast<char*>(workspace);
+  cudaError_t err = cudaMemcpyAsync(ws, h, P.desc_bytes, cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) return cuda_fail(err, "descriptor upload");
+  cudaEventRecord(pin->ev, s);
+  pin->pending = true;
+  if (pool->profiling) cudaEventRecord(ev[1], s);
+
+  char* blocks = pool->storage + pool->L.blocks_off;
+  int launches = 0;
+  // ---- a4: K/V reconstruction of hidden-mode requests
+  if (P.n_hb > 0) {
+    ReconParams rp;
+    rp.gather = reinterpret_cast<const int32_t*>(ws + P.off_gather);
+    rp.n_hblocks = P.n_hb;
+    rp.pool = blocks;
+    rp.w_int = pool->storage + pool->L.w_off;
+    rp.b_int = pool->has_bias ? reinterpret_cast<const float*>(pool->storage + pool->L.b_off) : nullptr;
+    rp.scr_k = ws + P.off_sk;
+    rp.scr_v = ws + P.off_sv;
+    rp.d = pool->cfg.d_model;
+    rp.H = H;
+    rp.dh = pool->cfg.head_dim;
+    rp.B = B;
+    err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, pool->num_sms, s)
+                      : launch_recon_simt(rp, pool->cfg.dtype, s);
+    if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
+    ++launches;
+  }
+  if (pool->profiling) cudaEventRecord(ev[2], s);
+  // ---- a5: split-K attention over KV blocks and rebuilt K/V
+  AttnParams ap;
+  ap.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
+  ap.splits = reinterpret_cast<const SplitDesc*>(ws + P.off_splits);
+  ap.tables = reinterpret_cast<const int32_t*>(ws + P.off_tabs);
+  ap.pool = blocks;
+  ap.scr_k = ws + P.off_sk;
+  ap.scr_v = ws + P.off_sv;
+  ap.q = q;
+  ap.part_ml = reinterpret_cast<float*>(ws + P.off_ml);
+  ap.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
+  ap.task_counter = reinterpret_cast<int32_t*>(ws);
+  ap.n_tasks = P.n_splits * H;
+  ap.H = H;
+  ap.dh = pool->cfg.head_dim;
+  ap.B = B;
+  ap.d = pool->cfg.d_model;
+  ap.scale_log2 = scale * 1.4426950408889634f;
+  err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
+  if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
+  ++launches;
+  if (pool->profiling) cudaEventRecord(ev[3], s);
+  // ---- a6: combine splits
+  CombineParams cp;
+  cp.reqs = ap.reqs;
+  cp.part_ml = ap.part_ml;
+  cp.part_acc = ap.part_acc;
+  cp.out = out;
+  cp.lse = lse;
+  cp.n_req = n_req;
+  cp.H = H;
+  cp.dh = pool->cfg.head_dim;
+  cp.d = pool->cfg.d_model;
+  err = launch_combine(cp, pool->cfg.dtype, s);
+  if (err != cudaSuccess) return cuda_fail(err, "combine kernel");
+  ++launches;
+  if (pool->profiling) {
+    cudaEventRecord(ev[4], s);
+    pool->prof_pending.push_back(ev);
+  }
+  pool->last_launches = launches;
+  return HC_OK;
+}
+
+int32_t hc_last_launch_count(const hc_pool* pool) { return pool ? pool->last_launches : -1; }
+
+hc_status hc_set_profiling(hc_pool* pool, int32_t enable) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->profiling = enable != 0;
+  return HC_OK;
+}
+
+hc_status hc_kernel_times(hc_pool* pool, float* ms4, int32_t* n_calls) {
+  if (!pool || !ms4) return fail(HC_E_INVALID, "null argument");
+  DeviceGuard g(pool->cfg.device);
+  double acc[4] = {0, 0, 0, 0};
+  for (auto& ev : pool->prof_pending) {
+    cudaError_t err = cudaEventSynchronize(ev[4]);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaEventSynchronize");
+    float t;
+    const int pairs[4][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 1}};
+    for (int k = 0; k < 4; ++k) {
+      cudaEventElapsedTime(&t, ev[pairs[k][0]], ev[pairs[k][1]]);
+      acc[k] += t;
+    }
+    for (auto e : ev) pool->ev_free.push_back(e);
+  }
+  if (n_calls) *n_calls = (int32_t)pool->prof_pending.size();
+  pool->prof_pending.clear();
+  for (int k = 0; k < 4; ++k) ms4[k] = (float)acc[k];
+  return HC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,244 @@
+"""Thin ctypes binding of libhc.so (include/hc.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only turns
+torch tensors into pointers and status codes into exceptions.  There is no fallback: if
+libhc.so is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhc.so")
+
+HC_OK, HC_E_INVALID, HC_E_OOM, HC_E_UNKNOWN_REQ, HC_E_MODE_MISMATCH, HC_E_CUDA, HC_E_UNSUPPORTED, \
+    HC_E_WORKSPACE = range(8)
+STATUS_NAMES = {0: "HC_OK", 1: "HC_E_INVALID", 2: "HC_E_OOM", 3: "HC_E_UNKNOWN_REQ",
+                4: "HC_E_MODE_MISMATCH", 5: "HC_E_CUDA", 6: "HC_E_UNSUPPORTED", 7: "HC_E_WORKSPACE"}
+HC_MODE_KV, HC_MODE_HIDDEN = 0, 1
+HC_BF16, HC_F32 = 0, 1
+HC_FLAG_ACCOUNTING_ONLY, HC_FLAG_FORCE_SIMT, HC_FLAG_GENERIC_ATTN = 1, 2, 4
+
+
+class HcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PoolConfig(ctypes.Structure):
+    _fields_ = [
+        ("d_model", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+        ("block_size", ctypes.c_int32), ("num_blocks", ctypes.c_int64), ("dtype", ctypes.c_int32),
+        ("flags", ctypes.c_int32), ("storage", ctypes.c_void_p), ("storage_bytes", ctypes.c_size_t),
+        ("w_kv", ctypes.c_void_p), ("b_kv", ctypes.c_void_p), ("device", ctypes.c_int32),
+        ("split_tokens", ctypes.c_int32),
+    ]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built (run __graft_entry__.build() or "
+                          "python paper_2504_07494_b200/build.py); there is no fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, SZ, VP = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p
+    pI32, pI64, pF = ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_float)
+    sig = {
+        "hc_pool_storage_bytes": (SZ, [ctypes.POINTER(PoolConfig)]),
+        "hc_pool_create": (I32, [ctypes.POINTER(PoolConfig), ctypes.POINTER(P)]),
+        "hc_pool_destroy": (None, [P]),
+        "hc_append": (I32, [P, I32, pI64, pI32, pI32, VP, VP, VP, VP]),
+        "hc_free": (I32, [P, I64, pI64]),
+        "hc_workspace_size": (SZ, [P, I32, pI64]),
+        "hc_decode_attention": (I32, [P, I32, pI64, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
+        "hc_pool_num_free": (I64, [P]),
+        "hc_request_info": (I32, [P, I64, pI32, pI64, pI64]),
+        "hc_request_blocks": (I32, [P, I64, I32, pI32, I64, pI64]),
+        "hc_last_launch_count": (I32, [P]),
+        "hc_set_profiling": (I32, [P, I32]),
+        "hc_kernel_times": (I32, [P, pF, pI32]),
+        "hc_last_error": (ctypes.c_char_p, []),
+        "hc_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != HC_OK:
+        raise HcError(status, lib.hc_last_error().decode())
+
+
+def _i64(vals: Sequence[int]):
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def _i32(vals: Sequence[int]):
+    return (ctypes.c_int32 * len(vals))(*[int(v) for v in vals])
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+# ------------------------------------------------------------------ raw C-ABI mirrors
+def hc_pool_storage_bytes(cfg: PoolConfig) -> int:
+    return int(lib.hc_pool_storage_bytes(ctypes.byref(cfg)))
+
+
+def hc_pool_create(cfg: PoolConfig) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(lib.hc_pool_create(ctypes.byref(cfg), ctypes.byref(h)))
+    return h
+
+
+def hc_pool_destroy(h) -> None:
+    lib.hc_pool_destroy(h)
+
+
+def hc_append(h, req_ids, modes, n_tokens, k=None, v=None, x=None, stream=None) -> None:
+    n = len(req_ids)
+    s = _stream(stream) if (k is not None or x is not None) else ctypes.c_void_p(None)
+    _check(lib.hc_append(h, n, _i64(req_ids), _i32(modes), _i32(n_tokens), _ptr(k), _ptr(v), _ptr(x), s))
+
+
+def hc_free(h, req_id: int) -> int:
+    rel = ctypes.c_int64(0)
+    _check(lib.hc_free(h, int(req_id), ctypes.byref(rel)))
+    return rel.value
+
+
+def hc_workspace_size(h, req_ids) -> int:
+    n = int(lib.hc_workspace_size(h, len(req_ids), _i64(req_ids)))
+    if n == 0 and len(req_ids) > 0:
+        raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
+    return n
+
+
+def hc_decode_attention(h, req_ids, q, scale, out, lse, workspace, stream=None) -> None:
+    _check(lib.hc_decode_attention(h, len(req_ids), _i64(req_ids), _ptr(q), float(scale), _ptr(out), _ptr(lse),
+                                   _ptr(workspace), workspace.numel() * workspace.element_size()
+                                   if workspace is not None else 0, _stream(stream)))
+
+
+# ------------------------------------------------------------------ convenience owner
+_TORCH_DT = {HC_BF16: torch.bfloat16, HC_F32: torch.float32}
+
+
+class HybridCachePool:
+    """Owns the torch storage of one pool and marshals calls to libhc.so."""
+
+    def __init__(self, d_model: int, n_heads: int, head_dim: int, block_size: int, num_blocks: int,
+                 dtype: int, w_kv: Optional[torch.Tensor] = None, b_kv: Optional[torch.Tensor] = None,
+                 device: int = 0, flags: int = 0, split_tokens: int = 0):
+        self.cfg = PoolConfig(d_model, n_heads, head_dim, block_size, num_blocks, dtype, flags, None, 0,
+                              None, None, device, split_tokens)
+        self.dtype = dtype
+        self.tdtype = _TORCH_DT[dtype]
+        self.d, self.H, self.dh, self.B = d_model, n_heads, head_dim, block_size
+        self.device = device
+        self.storage = None
+        if not flags & HC_FLAG_ACCOUNTING_ONLY:
+            nbytes = hc_pool_storage_bytes(self.cfg)
+            if nbytes == 0:
+                raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
+            dev = torch.device("cuda", device)
+            self.storage = torch.empty(nbytes + 1024, dtype=torch.uint8, device=dev)
+            base = self.storage.data_ptr()
+            off = (-base) % 1024
+            self.cfg.storage = base + off
+            self.cfg.storage_bytes = nbytes
+            assert w_kv is not None and w_kv.is_cuda and w_kv.dtype == self.tdtype and w_kv.is_contiguous()
+            assert tuple(w_kv.shape) == (2 * d_model, d_model)
+            self.cfg.w_kv = w_kv.data_ptr()
+            if b_kv is not None:
+                assert b_kv.is_cuda and b_kv.dtype == torch.float32 and b_kv.numel() == 2 * d_model
+                self._b_keep = b_kv.contiguous()
+                self.cfg.b_kv = self._b_keep.data_ptr()
+        self.handle = hc_pool_create(self.cfg)
+        self._ws = None
+
+    def close(self):
+        if getattr(self, "handle", None):
+            hc_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    # -- cache management
+    def append(self, req_ids, modes, n_tokens, k=None, v=None, x=None, stream=None):
+        for t in (k, v, x):
+            if t is not None:
+                assert t.is_cuda and t.dtype == self.tdtype and t.is_contiguous(), "rows must be contiguous device tensors"
+        hc_append(self.handle, req_ids, modes, n_tokens, k, v, x, stream)
+
+    def free(self, req_id) -> int:
+        return hc_free(self.handle, req_id)
+
+    def num_free(self) -> int:
+        return int(lib.hc_pool_num_free(self.handle))
+
+    def request_info(self, req_id):
+        m, n, u = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.hc_request_info(self.handle, int(req_id), ctypes.byref(m), ctypes.byref(n), ctypes.byref(u)))
+        return m.value, n.value, u.value
+
+    def request_blocks(self, req_id, kind=0):
+        cnt = ctypes.c_int64()
+        _check(lib.hc_request_blocks(self.handle, int(req_id), kind, None, 0, ctypes.byref(cnt)))
+        buf = (ctypes.c_int32 * max(1, cnt.value))()
+        _check(lib.hc_request_blocks(self.handle, int(req_id), kind, buf, cnt.value, ctypes.byref(cnt)))
+        return list(buf[:cnt.value])
+
+    # -- decode
+    def workspace_size(self, req_ids) -> int:
+        return hc_workspace_size(self.handle, req_ids)
+
+    def workspace(self, req_ids) -> torch.Tensor:
+        n = self.workspace_size(req_ids)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return self._ws
+
+    def decode(self, req_ids, q, scale, out=None, lse=None, want_lse=True, workspace=None, stream=None):
+        n = len(req_ids)
+        assert q.is_cuda and q.dtype == self.tdtype and q.is_contiguous() and tuple(q.shape) == (n, self.d)
+        if out is None:
+            out = torch.empty((n, self.d), dtype=self.tdtype, device=q.device)
+        if lse is None and want_lse:
+            lse = torch.empty((n, self.H), dtype=torch.float32, device=q.device)
+        ws = workspace if workspace is not None else self.workspace(req_ids)
+        hc_decode_attention(self.handle, req_ids, q, scale, out, lse, ws, stream)
+        return out, lse
+
+    # -- measurement hooks
+    def last_launch_count(self) -> int:
+        return int(lib.hc_last_launch_count(self.handle))
+
+    def set_profiling(self, on: bool):
+        _check(lib.hc_set_profiling(self.handle, 1 if on else 0))
+
+    def kernel_times(self):
+        ms = (ctypes.c_float * 4)()
+        n = ctypes.c_int32()
+        _check(lib.hc_kernel_times(self.handle, ms, ctypes.byref(n)))
+        return {"recon_ms": ms[0], "attn_ms": ms[1], "combine_ms": ms[2], "upload_ms": ms[3], "calls": n.value}

@@ -1,0 +1,120 @@
+"""C-ABI library: loads, exports every symbol include/hc.h declares, and its host-side
+allocator matches the reference pool semantics (accounting-only pools: no device work,
+so this runs on the CPU box)."""
+import ctypes
+import os
+import random
+import re
+
+import pytest
+
+from oracle.pool_oracle import PoolOracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hc():
+    from paper_2504_07494_b200 import build
+    build.build()
+    from paper_2504_07494_b200 import hc as m
+    return m
+
+
+def test_exports_every_declared_symbol(hc):
+    hdr = open(os.path.join(ROOT, "include", "hc.h")).read()
+    declared = set(re.findall(r"^(?:const\s+)?[a-z_0-9]+\s*\*?\s+(hc_[a-z_0-9]+)\(", hdr, re.M))
+    assert {"hc_pool_create", "hc_append", "hc_decode_attention"} <= declared
+    lib = ctypes.CDLL(hc.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in hc.h but not exported"
+    assert b"sm_100a" in hc.lib.hc_version()
+
+
+def _acct_pool(hc, num_blocks, B, d=32, H=2):
+    return hc.HybridCachePool(d, H, d // H, B, num_blocks, hc.HC_F32, flags=hc.HC_FLAG_ACCOUNTING_ONLY)
+
+
+def _tables_equal(pool, orc, rid):
+    mode, n, units = pool.request_info(rid)
+    t = orc.table(rid)
+    if mode == 0:
+        return pool.request_blocks(rid, 0) == t[0] and pool.request_blocks(rid, 1) == t[1] and n == orc.req[rid]["n"]
+    return pool.request_blocks(rid, 0) == t[0] and pool.request_blocks(rid, 1) == [] and n == orc.req[rid]["n"]
+
+
+def test_fig6_through_the_abi(hc):
+    """Fig. 6: 16 blocks, B=4: A (KV, 11 tok) -> 6 units, B (hidden, 14) -> 4."""
+    p = _acct_pool(hc, 16, 4)
+    o = PoolOracle(16, 4)
+    p.append([0], [0], [11])
+    o.append([0], [0], [11])
+    p.append([1], [1], [14])
+    o.append([1], [1], [14])
+    assert p.request_info(0)[2] == 6 and p.request_info(1)[2] == 4 and p.num_free() == 6
+    assert _tables_equal(p, o, 0) and _tables_equal(p, o, 1)
+    assert p.free(0) == 6 and p.free(0) == 0 and p.num_free() == 12
+
+
+def test_error_codes(hc):
+    p = _acct_pool(hc, 5, 4)
+    p.append([1], [1], [16])
+    with pytest.raises(hc.HcError) as e:
+        p.append([2], [0], [1])                     # KV needs 2 blocks, 1 free
+    assert e.value.status == hc.HC_E_OOM and p.num_free() == 1
+    with pytest.raises(hc.HcError) as e:
+        p.append([1], [0], [1])
+    assert e.value.status == hc.HC_E_MODE_MISMATCH
+    with pytest.raises(hc.HcError) as e:
+        p.append([3, 3], [1, 1], [1, 1])
+    assert e.value.status == hc.HC_E_INVALID
+    with pytest.raises(hc.HcError) as e:
+        p.request_info(99)
+    assert e.value.status == hc.HC_E_UNKNOWN_REQ
+    with pytest.raises(hc.HcError) as e:
+        p.append([4, 5], [1, 1], [4, 4])            # batch OOM is all-or-nothing
+    assert e.value.status == hc.HC_E_OOM and p.num_free() == 1
+    with pytest.raises(hc.HcError):
+        hc.HybridCachePool(30, 4, 8, 4, 8, hc.HC_F32, flags=hc.HC_FLAG_ACCOUNTING_ONLY)  # d != H*dh
+    with pytest.raises(hc.HcError) as e:
+        hc.hc_decode_attention(p.handle, [1], None, 1.0, None, None, None, stream=0)
+    assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+def test_fuzz_against_pool_oracle(hc):
+    """10^3 random append/free sequences: block ids, lengths and free counts bit-exact."""
+    rs = random.Random(1)
+    p = _acct_pool(hc, 61, 4)
+    o = PoolOracle(61, 4)
+    for _ in range(1000):
+        if rs.random() < 0.65:
+            ids = rs.sample(range(20), rs.randint(1, 3))
+            modes = [o.req[i]["mode"] if i in o.req else rs.randint(0, 1) for i in ids]
+            toks = [rs.randint(0, 9) for _ in ids]
+            want = o.append(ids, modes, toks)
+            try:
+                p.append(ids, modes, toks)
+                got = "ok"
+            except hc.HcError as e:
+                got = {hc.HC_E_OOM: "oom"}.get(e.status, "err")
+            assert got == want
+        else:
+            r = rs.randrange(20)
+            assert p.free(r) == o.free_req(r)
+        assert p.num_free() == o.num_free()
+        for rid in o.req:
+            assert _tables_equal(p, o, rid)
+
+
+def test_storage_bytes_and_workspace_queries(hc):
+    cfg = hc.PoolConfig(9216, 72, 128, 16, 1000, hc.HC_BF16, 0, None, 0, None, None, 0, 0)
+    n = hc.hc_pool_storage_bytes(cfg)
+    blocks = 1000 * 16 * 9216 * 2
+    assert n >= blocks + 2 * 9216 * 9216 * 2 and n < blocks + 2 * 9216 * 9216 * 2 + (8 << 20)
+    bad = hc.PoolConfig(100, 3, 33, 16, 10, hc.HC_BF16, 0, None, 0, None, None, 0, 0)
+    assert hc.hc_pool_storage_bytes(bad) == 0
+    p = _acct_pool(hc, 64, 4)
+    p.append([5, 6], [0, 1], [9, 3])
+    assert p.workspace_size([5, 6]) > 0
+    with pytest.raises(hc.HcError):
+        p.workspace_size([5, 5])

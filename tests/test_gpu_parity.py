@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded inputs.  Tolerances (BASELINE.json north_star): max normwise relative error
+<= 1e-5 in fp32 mode, <= 1e-2 in bf16 (reading R12)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from synth import configs as C
+from synth.configs import MODE_HIDDEN, MODE_KV, LayerShape, Workload
+from tests import hc_testlib as T
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+TOL_BF16 = 1e-2
+
+
+@pytest.fixture(scope="module")
+def hc():
+    from paper_2504_07494_b200 import build
+    build.build()
+    from paper_2504_07494_b200 import hc as m
+    return m
+
+
+def _run(w, flags=0, split_tokens=0, order="rr", idx=None):
+    pool = T.make_pool(w, flags=flags, split_tokens=split_tokens)
+    T.fill(pool, w, order=order)
+    q = T.queries(w)
+    out, lse = T.decode(pool, w, q, idx)
+    return pool, out, lse
+
+
+# ------------------------------------------------------------------ tiny fp32 (full)
+@pytest.mark.parametrize("B", [16, 4])
+@pytest.mark.parametrize("bias", [False, True])
+def test_tiny_fp32_full(hc, B, bias):
+    w = C.tiny(block_size=B, bias=bias)
+    pool, out, lse = _run(w)
+    err, lerr = T.compare(w, out, lse, range(4))
+    assert err <= TOL_F32, err
+    assert lerr <= 1e-5, lerr
+    assert pool.last_launch_count() == 3  # reconstruction, attention, combine
+
+
+def test_tiny_fp32_generic_attention_kernel(hc):
+    w = C.tiny()
+    _, out, lse = _run(w, flags=hc.HC_FLAG_GENERIC_ATTN)
+    assert T.compare(w, out, lse, range(4))[0] <= TOL_F32
+
+
+# ------------------------------------------------------------------ bf16, several tiles + ragged tails
+SHAPES = [
+    # (d, H, dh, B)
+    (256, 2, 128, 16),
+    (512, 8, 64, 32),
+    (384, 3, 128, 8),     # B=8: generic attention, 16 TMA boxes per A tile
+    (256, 2, 128, 64),
+    (256, 2, 128, 256),   # block larger than an M tile
+]
+N_MIX = [1, 15, 16, 17, 129, 300, 513, 1000, 33, 2]
+
+
+def _bf16_workload(d, H, dh, B, n=N_MIX, bias=False, seed=11, modes=None):
+    shape = LayerShape(f"test-{d}", d, H, dh)
+    if modes is None:
+        modes = [MODE_KV if i % 2 == 0 else MODE_HIDDEN for i in range(len(n))]
+    return Workload(f"bf16-{d}-{B}", shape, B, "bf16", seed, list(n), list(modes), list(range(len(n))), bias)
+
+
+@pytest.mark.parametrize("d,H,dh,B", SHAPES)
+def test_bf16_mixed_batch_vs_oracle(hc, d, H, dh, B):
+    w = _bf16_workload(d, H, dh, B, bias=True)
+    _, out, lse = _run(w)
+    err, lerr = T.compare(w, out, lse, range(len(w.n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= 5e-2, lerr
+
+
+@pytest.mark.parametrize("flags", ["simt", "generic"])
+def test_bf16_alternative_kernels_agree(hc, flags):
+    """The SIMT reconstruction and the generic attention kernel meet the same bar."""
+    f = hc.HC_FLAG_FORCE_SIMT if flags == "simt" else hc.HC_FLAG_GENERIC_ATTN
+    w = _bf16_workload(256, 2, 128, 16)
+    _, out, lse = _run(w, flags=f)
+    assert T.compare(w, out, lse, range(len(w.n)))[0] <= TOL_BF16
+
+
+def test_bf16_all_hidden_many_tiles(hc):
+    """M spans many 128-row tiles of the tcgen05 GEMM with a ragged last tile."""
+    n = [700, 1, 333, 1025, 64, 65]
+    w = _bf16_workload(512, 4, 128, 16, n=n, modes=[MODE_HIDDEN] * len(n), bias=True)
+    _, out, lse = _run(w)
+    assert T.compare(w, out, lse, range(len(n)))[0] <= TOL_BF16
+
+
+# ------------------------------------------------------------------ invariants (north_star)
+def test_constant_values_give_ones(hc):
+    """V = 1 => out = 1 (softmax rows sum to 1).  Hidden: W_V = 0, b_V = 1 => V = 1."""
+    d, H, dh, B = 256, 2, 128, 16
+    w = _bf16_workload(d, H, dh, B, n=[5, 300, 17, 1000])
+    dev = torch.device("cuda", 0)
+    W = w.w_kv(device=dev)
+    W[d:] = 0
+    b = torch.zeros(2 * d, dtype=torch.float32, device=dev)
+    b[d:] = 1.0
+    pool = T.make_pool(w, w_kv=W, b_kv=b)
+    data = {}
+    for i in range(len(w.n)):
+        if w.modes[i] == MODE_KV:
+            K, _ = w.kv(i, device=dev)
+            data[i] = (K, torch.ones_like(K))
+        else:
+            data[i] = w.x(i, device=dev)
+    T.fill(pool, w, data=data)
+    out, _ = T.decode(pool, w, T.queries(w))
+    assert np.all(out == 1.0)
+
+
+def test_single_token_returns_v1(hc):
+    """n = 1 => out = v_1 exactly (KV); hidden => bf16(W_V x_1) up to reconstruction rounding."""
+    w = _bf16_workload(256, 2, 128, 16, n=[1, 1])
+    pool, out, lse = _run(w)
+    K, V = w.kv(0)
+    assert np.array_equal(out[0], V[0].float().numpy())
+    assert T.compare(w, out, lse, [1])[0] <= TOL_BF16
+
+
+def test_block_placement_is_bitwise_irrelevant(hc):
+    """Same logical content, different physical blocks => bitwise-identical output."""
+    w = _bf16_workload(256, 2, 128, 16)
+    _, a, la = _run(w, split_tokens=64, order="rr")
+    _, b, lb = _run(w, split_tokens=64, order="seq")
+    _, c, lc = _run(w, split_tokens=64, order="shuffle")
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert np.array_equal(la, lb) and np.array_equal(la, lc)
+
+
+@pytest.mark.parametrize("S", [16, 64, 512, 4096])
+def test_split_size_invariance(hc, S):
+    w = _bf16_workload(256, 2, 128, 16)
+    _, out, lse = _run(w, split_tokens=S)
+    assert T.compare(w, out, lse, range(len(w.n)))[0] <= TOL_BF16
+
+
+def test_batch_invariance_and_determinism(hc):
+    w = _bf16_workload(256, 2, 128, 16)
+    pool = T.make_pool(w, split_tokens=64)
+    T.fill(pool, w)
+    q = T.queries(w)
+    full, lf = T.decode(pool, w, q)
+    again, la = T.decode(pool, w, q)
+    assert np.array_equal(full, again) and np.array_equal(lf, la)
+    for i in (0, 3, 6):
+        alone, l1 = T.decode(pool, w, q, [i])
+        assert np.array_equal(alone[0], full[i]) and np.array_equal(l1[0], lf[i])
+    sub = [7, 2, 5]
+    part, lp = T.decode(pool, w, q, sub)
+    assert np.array_equal(part, full[sub])
+
+
+def test_hidden_equals_kv_twin(hc):
+    """hidden(X) == KV(K = bf16(X W_K^T + b_K), V = ...) (north_star invariant).
+    The twin's K/V are the oracle's fp64 projections rounded to bf16 on the host."""
+    from oracle import hc_oracle as O
+    d, H, dh, B = 256, 2, 128, 16
+    n = [40, 300, 7]
+    w = _bf16_workload(d, H, dh, B, n=n, modes=[MODE_HIDDEN] * 3, bias=True)
+    W, b = w.w_kv(), w.b_kv()
+    twin = Workload("twin", w.shape, B, "bf16", w.seed, n, [MODE_KV] * 3, [100, 101, 102], True)
+    dev = torch.device("cuda", 0)
+    pool = T.make_pool(w, num_blocks=200)
+    data_h, data_k = {}, {}
+    for i in range(3):
+        X = w.x(i)
+        K, V = O.hidden_request_kv(X, W, b)
+        data_h[i] = X.to(dev)
+        data_k[i] = (torch.tensor(K).to(torch.bfloat16).to(dev), torch.tensor(V).to(torch.bfloat16).to(dev))
+    T.fill(pool, w, data=data_h)
+    T.fill(pool, twin, data=data_k)
+    q = T.queries(w)
+    oh, lh = pool.decode(w.req_ids, q, w.scale)
+    ok, lk = pool.decode(twin.req_ids, q, w.scale)
+    oh, ok = oh.float().cpu().numpy(), ok.float().cpu().numpy()
+    assert O.max_rel_err(oh, ok, H) <= TOL_BF16
+    assert np.abs(lh.cpu().numpy() - lk.cpu().numpy()).max() <= 2e-2
+
+
+def test_switch_mode_by_free_and_reappend(hc):
+    """Cache-type switch = discard + recompute: free, re-append in the other mode."""
+    d, H, dh, B = 256, 2, 128, 16
+    w = _bf16_workload(d, H, dh, B, n=[90, 31], modes=[MODE_KV, MODE_HIDDEN])
+    pool = T.make_pool(w, num_blocks=64)
+    T.fill(pool, w)
+    with pytest.raises(hc.HcError) as e:
+        pool.append([w.req_ids[0]], [MODE_HIDDEN], [1], x=w.x(0, device="cuda")[:1].contiguous())
+    assert e.value.status == hc.HC_E_MODE_MISMATCH
+    assert pool.free(w.req_ids[0]) == 2 * math.ceil(90 / B)
+    w2 = _bf16_workload(d, H, dh, B, n=[90, 31], modes=[MODE_HIDDEN, MODE_HIDDEN])
+    pool.append([w2.req_ids[0]], [MODE_HIDDEN], [90], x=w2.x(0, device="cuda"))
+    out, lse = T.decode(pool, w2, T.queries(w2))
+    assert T.compare(w2, out, lse, [0, 1])[0] <= TOL_BF16
+
+
+def test_error_paths_on_device(hc):
+    w = _bf16_workload(256, 2, 128, 16, n=[20, 20])
+    pool = T.make_pool(w, num_blocks=16)
+    T.fill(pool, w)
+    q = T.queries(w)
+    out, lse = pool.decode([], q[:0].contiguous(), 1.0)
+    assert pool.last_launch_count() == 0
+    for bad, code in (([0, 0], hc.HC_E_INVALID), ([0, 77], hc.HC_E_UNKNOWN_REQ)):
+        with pytest.raises(hc.HcError) as e:
+            hc.hc_decode_attention(pool.handle, bad, q, 1.0, torch.empty_like(q), None, pool.workspace([0]))
+        assert e.value.status == code
+    small = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(hc.HcError) as e:
+        hc.hc_decode_attention(pool.handle, [0, 1], q, 1.0, torch.empty_like(q), None, small)
+    assert e.value.status == hc.HC_E_WORKSPACE
+    pool.append([5], [MODE_KV], [0])                # created with 0 tokens
+    with pytest.raises(hc.HcError) as e:
+        pool.decode([5], q[:1].contiguous(), 1.0)
+    assert e.value.status == hc.HC_E_INVALID
+
+
+# ------------------------------------------------------------------ OPT-shaped configs, sampled
+def _sample(w, n_kv=4, n_hid=2):
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
+    rs = np.random.default_rng(0)
+    pick = list(rs.choice(kv, size=min(n_kv, len(kv)), replace=False)) if kv else []
+    if hid:
+        longest = max(hid, key=lambda i: w.n[i])
+        others = [i for i in hid if i != longest]
+        pick += [longest] + (list(rs.choice(others, size=min(n_hid - 1, len(others)), replace=False)) if others else [])
+    return [int(i) for i in pick]
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4"])
+def test_opt_shaped_sampled_parity(hc, cfg):
+    """Full batch on the GPU in the bench's launch configuration (auto split, tcgen05
+    GEMM, pipelined attention); the oracle checks a seeded sample of requests (KV: all
+    heads; hidden: 3 heads incl. the first and last) including the longest hidden one."""
+    w = C.by_name(cfg)
+    pool = T.make_pool(w)
+    T.fill(pool, w)
+    q = T.queries(w)
+    out, lse = T.decode(pool, w, q)
+    assert np.isfinite(out).all()
+    idx = _sample(w)
+    H = w.shape.H
+    heads = {i: [0, H // 2, H - 1] for i in idx if w.modes[i] == MODE_HIDDEN}
+    err, lerr = T.compare(w, out[idx], lse[idx], idx, heads)
+    assert err <= TOL_BF16, err
+    assert lerr <= 5e-2, lerr
