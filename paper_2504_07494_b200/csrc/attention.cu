@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -78,35 +79,43 @@ struct Bfly {
   }
 };
 
-struct TaskInfo {
-  const void* kbase;  // row 0 of (block, head) for logical block lb0 is computed per chunk
-  int32_t nchunks;
-};
-
 template <int DH, int NW, int NST>
 struct PipeCfg {
   static constexpr int TOK = 16;                      // tokens per chunk
   static constexpr int CHUNK = TOK * DH * 2;          // bytes of one K (or V) chunk
   static constexpr int QB = DH * 2;                   // bytes of q_h
-  static constexpr int STAGE = 2 * CHUNK + QB;
-  static constexpr int WARP_BYTES = NST * STAGE + NST * 8 + NST * 16 + TOK * 4;
+  static constexpr int STAGE = 2 * CHUNK + QB;        // multiple of 16 bytes
+  static_assert(STAGE % 16 == 0, "stage alignment");
+  static constexpr int WARP_BYTES = (NST * STAGE + NST * 8 + NST * 16 + TOK * 4 + 127) / 128 * 128;
   static constexpr int SMEM = NW * WARP_BYTES;
 };
+
+__device__ __forceinline__ void bf16x8_to_f32(uint4 u, float (&f)[8]) {
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16);
+  f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16);
+  f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
 
 template <int DH, int NW, int NST>
 __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams p) {
   using C = PipeCfg<DH, NW, NST>;
   constexpr int TOK = C::TOK;
-  constexpr int LPR = DH / 4;      // lanes per row (each lane: 4 dims = 8 bytes)
-  constexpr int RPI = 32 / LPR;    // rows per load instruction
-  constexpr int NV = TOK / RPI;    // partial dot products per lane per chunk
+  constexpr int LPR = DH / 8;      // lanes per row (each lane: 8 dims = 16 bytes)
+  constexpr int RPI = 32 / LPR;    // rows per 128-bit load instruction
+  constexpr int NV = TOK / RPI;    // rows (partial dot products) per lane per chunk
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* wb = smem + warp * C::WARP_BYTES;
   uint8_t* stage_base = wb;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wb + NST * C::STAGE);
-  int4* meta = reinterpret_cast<int4*>(wb + NST * C::STAGE + NST * 8);
-  float* pbuf = reinterpret_cast<float*>(wb + NST * C::STAGE + NST * 8 + NST * 16);
+  // per-warp layout: NST stages (16-B multiples) | meta[NST] int4 | bars[NST] | pbuf[16]
+  int4* meta = reinterpret_cast<int4*>(wb + NST * C::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wb + NST * C::STAGE + NST * 16);
+  float* pbuf = reinterpret_cast<float*>(wb + NST * C::STAGE + NST * 16 + NST * 8);
 
   if (lane == 0) {
     for (int s = 0; s < NST; ++s) ptx::mbar_init(&bars[s], 1);
@@ -150,21 +159,21 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams 
     if (ptask >= p.n_tasks) return false;
     const int tok = psp.lb0 * B + pchunk * TOK;   // token index within the request
     const int lb = tok / B, row = tok - lb * B;
-    const __nv_bfloat16 *ksrc, *vsrc;
-    if (prq.mode == 0) {
-      const int kb = p.tables[prq.tab_off + 2 * lb];
-      const int vb = p.tables[prq.tab_off + 2 * lb + 1];
-      ksrc = pool + (size_t)kb * blk_elems + phead * head_elems + (size_t)row * DH;
-      vsrc = pool + (size_t)vb * blk_elems + phead * head_elems + (size_t)row * DH;
-    } else {
-      const size_t off = ((size_t)(prq.scratch_blk0 + lb) * H + phead) * head_elems + (size_t)row * DH;
-      ksrc = scr_k + off;
-      vsrc = scr_v + off;
-    }
     const int rem = psp.ntok - pchunk * TOK;
     const int nvalid = rem < TOK ? rem : TOK;
     const bool first = pchunk == 0, last = pchunk == pnch - 1;
     if (lane == 0) {
+      const __nv_bfloat16 *ksrc, *vsrc;
+      if (prq.mode == 0) {
+        const int kb = p.tables[prq.tab_off + 2 * lb];
+        const int vb = p.tables[prq.tab_off + 2 * lb + 1];
+        ksrc = pool + (size_t)kb * blk_elems + phead * head_elems + (size_t)row * DH;
+        vsrc = pool + (size_t)vb * blk_elems + phead * head_elems + (size_t)row * DH;
+      } else {
+        const size_t off = ((size_t)(prq.scratch_blk0 + lb) * H + phead) * head_elems + (size_t)row * DH;
+        ksrc = scr_k + off;
+        vsrc = scr_v + off;
+      }
       meta[stage] = make_int4(ptask, pchunk, nvalid, (first ? 1 : 0) | (last ? 2 : 0));
       uint8_t* sb = stage_base + stage * C::STAGE;
       ptx::fence_proxy_async_smem();
@@ -188,11 +197,12 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams 
     if (produce(s)) ++in_flight;
   __syncwarp();
 
-  const int lr = lane % LPR;   // this lane's 8-byte column slot
+  const int lr = lane % LPR;   // this lane's 16-byte column slot (dims 8*lr .. 8*lr+7)
   const int lg = lane / LPR;   // this lane's row group
-  float qf[4] = {0, 0, 0, 0};
-  float acc[4] = {0, 0, 0, 0};
-  float m_run = -INFINITY, l_run = 0.f;
+  float qf[8], acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) qf[i] = acc[i] = 0.f;
+  float m_run = -INFINITY, l_lane = 0.f;   // l kept per lane (rows this lane owns), reduced per task
   int cstage = 0;
   uint32_t cphase = 0;
 
@@ -201,25 +211,31 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams 
     const int4 mt = meta[cstage];
     ptx::mbar_wait(&bars[cstage], cphase);
     const uint8_t* sb = stage_base + cstage * C::STAGE;
-    if (mt.w & 1) {  // first chunk of a task: fresh state, load q_h
-      const uint2 qq = reinterpret_cast<const uint2*>(sb + 2 * C::CHUNK)[lr];
-      bf16x4_to_f32(qq, qf);
+    if (mt.w & 1) {  // first chunk of a task: fresh state, load q_h (pre-scaled by scale*log2 e)
+      bf16x8_to_f32(reinterpret_cast<const uint4*>(sb + 2 * C::CHUNK)[lr], qf);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 8; ++i) {
         qf[i] *= p.scale_log2;
         acc[i] = 0.f;
       }
       m_run = -INFINITY;
-      l_run = 0.f;
+      l_lane = 0.f;
     }
-    // ---- scores ----
-    const uint2* ks = reinterpret_cast<const uint2*>(sb);
+    // ---- scores: lane dots 8 dims of NV rows, butterfly leaves one full score per lane pair
+    const uint4* ks = reinterpret_cast<const uint4*>(sb);
     float part[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      float kf[4];
-      bf16x4_to_f32(ks[(i * RPI + lg) * LPR + lr], kf);
-      part[i] = qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3];
+      float kf[8];
+      bf16x8_to_f32(ks[(i * RPI + lg) * LPR + lr], kf);
+      float a0 = qf[0] * kf[0], a1 = qf[1] * kf[1];
+      a0 = fmaf(qf[2], kf[2], a0);
+      a1 = fmaf(qf[3], kf[3], a1);
+      a0 = fmaf(qf[4], kf[4], a0);
+      a1 = fmaf(qf[5], kf[5], a1);
+      a0 = fmaf(qf[6], kf[6], a0);
+      a1 = fmaf(qf[7], kf[7], a1);
+      part[i] = a0 + a1;
     }
     int idx = 0;
     Bfly<NV, LPR / 2>::run(part, lane, idx);
@@ -229,39 +245,45 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams 
     const float m_new = fmaxf(m_run, warp_max(s));
     const float pj = valid ? fast_exp2(s - m_new) : 0.f;
     const float alpha = fast_exp2(m_run - m_new);   // 0 when m_run = -inf
-    if ((lane & 1) == 0) pbuf[row] = pj;
-    const float lsum = warp_sum((lane & 1) ? 0.f : pj);
-    l_run = l_run * alpha + lsum;
+    if ((lane & 1) == 0) {
+      pbuf[row] = pj;
+      l_lane = l_lane * alpha + pj;
+    } else {
+      l_lane *= alpha;
+    }
     m_run = m_new;
     __syncwarp();
-    // ---- acc = alpha * acc + sum_j p_j v_j ----
-    const uint2* vs = reinterpret_cast<const uint2*>(sb + C::CHUNK);
+    // ---- acc = alpha * acc + sum_j p_j v_j (padding rows have p_j = 0 and finite v_j)
+    const uint4* vs = reinterpret_cast<const uint4*>(sb + C::CHUNK);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] *= alpha;
+    for (int i = 0; i < 8; ++i) acc[i] *= alpha;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int r = i * RPI + lg;
-      float vf[4];
-      bf16x4_to_f32(vs[r * LPR + lr], vf);
+      float vf[8];
+      bf16x8_to_f32(vs[r * LPR + lr], vf);
       const float pr = pbuf[r];
-      const bool ok = r < mt.z;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] += ok ? pr * vf[c] : 0.f;
+      for (int c = 0; c < 8; ++c) acc[c] = fmaf(pr, vf[c], acc[c]);
     }
-    if (mt.w & 2) {  // last chunk of the task: emit the partial
-      float a[4] = {acc[0], acc[1], acc[2], acc[3]};
-      if constexpr (RPI > 1) {
+    if (mt.w & 2) {  // last chunk of the task: emit the partial (m, l, acc)
+      float a[8];
 #pragma unroll
-        for (int o = LPR; o < 32; o <<= 1)
+      for (int c = 0; c < 8; ++c) a[c] = acc[c];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) a[c] += __shfl_xor_sync(FULL, a[c], o);
-      }
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[c] += __shfl_xor_sync(FULL, a[c], o);
+      const float l_tot = warp_sum(l_lane);
       const int task = mt.x;
-      if (lane < LPR)
-        reinterpret_cast<float4*>(p.part_acc + (size_t)task * DH)[lane] = make_float4(a[0], a[1], a[2], a[3]);
+      if (lane < LPR) {
+        float4* dst = reinterpret_cast<float4*>(p.part_acc + (size_t)task * DH) + 2 * lane;
+        dst[0] = make_float4(a[0], a[1], a[2], a[3]);
+        dst[1] = make_float4(a[4], a[5], a[6], a[7]);
+      }
       if (lane == 0) {
         p.part_ml[2 * (size_t)task] = m_run;
-        p.part_ml[2 * (size_t)task + 1] = l_run;
+        p.part_ml[2 * (size_t)task + 1] = l_tot;
       }
     }
     __syncwarp();
@@ -379,8 +401,13 @@ bool attn_pipe_supported(int dtype, int dh, int B) {
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s) {
   if (p.n_tasks <= 0) return cudaSuccess;
   if (!generic && attn_pipe_supported(dtype, p.dh, p.B)) {
-    if (p.dh == 128) return launch_pipe<128, 6, 4>(p, num_sms, s);
-    return launch_pipe<64, 6, 6>(p, num_sms, s);
+    static const int cfg = [] { const char* v = std::getenv("HC_ATTN_CFG"); return v ? std::atoi(v) : 0; }();
+    if (p.dh == 128) {
+      if (cfg == 1) return launch_pipe<128, 6, 4>(p, num_sms, s);
+      if (cfg == 2) return launch_pipe<128, 4, 6>(p, num_sms, s);
+      return launch_pipe<128, 8, 3>(p, num_sms, s);
+    }
+    return launch_pipe<64, 8, 5>(p, num_sms, s);
   }
   if (p.dh > 256) return cudaErrorInvalidValue;
   const int threads = 128;

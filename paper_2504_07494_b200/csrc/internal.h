@@ -60,6 +60,7 @@ struct ReconParams {
   void* scr_k;
   void* scr_v;
   int32_t d, H, dh, B;
+  int32_t* sync_counter;  // >= 32*num_sms zeroed ints (pair progress words)
 };
 
 struct AppendReq {
@@ -87,8 +88,9 @@ cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaSt
 cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d,
                               int H, int dh, int dtype, cudaStream_t s);
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
+// tmap_w: W_int with 256-row boxes (1-SM kernel); tmap_w_half: 128-row boxes (CTA-pair kernel)
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
-                            int num_sms, cudaStream_t s);
+                            const void* tmap_w_half, int num_sms, cudaStream_t s);
 bool recon_tc_supported(int d, int H, int dh, int B);
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s);
 bool attn_pipe_supported(int dtype, int dh, int B);

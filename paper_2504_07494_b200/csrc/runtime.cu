@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <queue>
@@ -39,6 +40,7 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr size_t kStagingBytes = 4u << 20;  // append descriptor staging inside storage
 constexpr int kRing = 4;                      // pinned host staging buffers
+constexpr size_t kHeaderBytes = 128 + 128 * 80;  // zeroed each call: counter + 80 progress lines
 
 struct Req {
   int32_t mode = 0;
@@ -93,9 +95,14 @@ bool make_tmap_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t outer, ui
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
+  const char* pe = std::getenv("HC_PROMO");
+  const int promo = pe ? std::atoi(pe) : 3;
+  const CUtensorMapL2promotion pr = promo == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 struct DeviceGuard {
@@ -135,7 +142,7 @@ struct hc_pool {
   char* storage = nullptr;
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_ids;
   std::unordered_map<int64_t, Req> reqs;
-  CUtensorMap tmap_x{}, tmap_w{};
+  CUtensorMap tmap_x{}, tmap_w{}, tmap_w_half{};
   bool tc_ok = false;
   int num_sms = 148;
   std::array<Pinned, kRing> ring{};
@@ -216,7 +223,7 @@ struct hc_pool {
       if (r->mode == HC_MODE_KV) P.n_tab += 2 * nb;
       else P.n_hb += (int32_t)nb;
     }
-    size_t o = 16;  // header: task counter + pad
+    size_t o = kHeaderBytes;  // header: attention task counter, then GEMM pair-progress words
     P.off_reqs = o = align_up(o, 64);
     o += sizeof(ReqDesc) * P.n_req;
     P.off_splits = o = align_up(o, 64);
@@ -303,7 +310,9 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
                                     (uint64_t)cfg->num_blocks * cfg->block_size, 64, rpb);
       const bool ok2 = make_tmap_2d(&p->tmap_w, p->storage + L.w_off, (uint64_t)cfg->d_model,
                                     2 * (uint64_t)cfg->d_model, 64, 256);
-      if (!ok1 || !ok2) {
+      const bool ok3 = make_tmap_2d(&p->tmap_w_half, p->storage + L.w_off, (uint64_t)cfg->d_model,
+                                    2 * (uint64_t)cfg->d_model, 64, 128);
+      if (!ok1 || !ok2 || !ok3) {
         delete p;
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed");
       }
@@ -518,7 +527,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   Pinned* pin = pool->pinned(P.desc_bytes);
   if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
   char* h = static_cast<char*>(pin->ptr);
-  std::memset(h, 0, 16);  // task counter = 0
+  std::memset(h, 0, kHeaderBytes);  // attention task counter and GEMM progress words = 0
   ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + P.off_reqs);
   SplitDesc* sd = reinterpret_cast<SplitDesc*>(h + P.off_splits);
   int32_t* tab = reinterpret_cast<int32_t*>(h + P.off_tabs);
@@ -582,7 +591,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     rp.H = H;
     rp.dh = pool->cfg.head_dim;
     rp.B = B;
-    err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, pool->num_sms, s)
+    rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
+    err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, s)
                       : launch_recon_simt(rp, pool->cfg.dtype, s);
     if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
     ++launches;

@@ -125,7 +125,7 @@ def test_single_token_returns_v1(hc):
     pool, out, lse = _run(w)
     K, V = w.kv(0)
     assert np.array_equal(out[0], V[0].float().numpy())
-    assert T.compare(w, out, lse, [1])[0] <= TOL_BF16
+    assert T.compare(w, out[[1]], lse[[1]], [1])[0] <= TOL_BF16
 
 
 def test_block_placement_is_bitwise_irrelevant(hc):
