@@ -130,7 +130,7 @@ def run_reference(args, rank: int, world: int):
     W = None
     if hid:
         dev = "cuda" if torch.cuda.is_available() else "cpu"
-        W = w.w_kv(device=dev).cpu()   # synth is bit-identical on any device (tests/test_synth_device)
+        W = w.w_kv(device=dev).cpu()   # synth is bit-identical on any device (tests/test_gpu_parity.py::test_synth_bit_identical_on_device)
     picks = []
     for s in range(args.warmup + args.steps):
         step = []
@@ -234,6 +234,8 @@ def main():
     ap.add_argument("--impl", default="hc", choices=["hc", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--split-tokens", type=int, default=0)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: one batch split across ranks by LPT (default: weak)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -260,7 +262,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w0 = workload_from(args.config)
-    w = C.shard_for_rank(w0, rank, world)
+    if args.strong:
+        from synth.partition import strong_shard
+        w = strong_shard(w0, rank, world)
+    else:
+        w = C.shard_for_rank(w0, rank, world)
     pool = T.make_pool(w, device=local, split_tokens=args.split_tokens)
     T.fill(pool, w, device=local)
     q = T.queries(w, device=local)
@@ -308,7 +314,8 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * n_req / (ms / 1e3)
+    n_total = len(w0.n) if args.strong else world * n_req
+    value = n_total / (ms / 1e3)
 
     # ---- end to end through the public API: pinned host q -> device, decode, out -> host
     e2e = None
@@ -339,7 +346,7 @@ def main():
             t = torch.tensor([ms_e2e], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        e2e = {"value": world * n_req / (ms_e2e / 1e3), "unit": "req-layers/s",
+        e2e = {"value": n_total / (ms_e2e / 1e3), "unit": "req-layers/s",
                "h2d_bytes_per_step": q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size(),
                "ms_per_step": ms_e2e}
@@ -383,11 +390,12 @@ def main():
     T_roof = max(F_alg / (tf_sus * 1e12), B_alg / (hbm * 1e9))
     line = {
         "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
-                   "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} (weak)",
+                   "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note},
         "roofline": roof,
         "step_roofline": {"T_roof_ms": T_roof * 1e3, "frac": T_roof * 1e3 / ms, "alg_bytes": B_alg,

@@ -255,3 +255,15 @@ def test_opt_shaped_sampled_parity(hc, cfg):
     err, lerr = T.compare(w, out[idx], lse[idx], idx, heads)
     assert err <= TOL_BF16, err
     assert lerr <= 5e-2, lerr
+
+
+def test_synth_bit_identical_on_device():
+    """The counter-based generator gives the same bits on CUDA and CPU, so the oracle can
+    regenerate inputs on the host (no oracle input is read back from the GPU path)."""
+    from synth import rng
+    for dt in (torch.bfloat16, torch.float32):
+        a = rng.normal_tensor(3, rng.STREAM_X, 17, [333, 96], 0.7, dt, "cpu", offset=12345)
+        b = rng.normal_tensor(3, rng.STREAM_X, 17, [333, 96], 0.7, dt, "cuda", offset=12345).cpu()
+        assert torch.equal(a, b)
+    w = C.cfg4()
+    assert torch.equal(w.w_kv(rows=(100, 140)), w.w_kv(device="cuda", rows=(100, 140)).cpu())

@@ -1,0 +1,77 @@
+"""N>1 host logic on CPU with torch.distributed gloo, world_size 2: weak-scaling shards,
+LPT strong sharding, and the bench's max-over-ranks timing reduction."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from synth import configs as C
+from synth import partition as P
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = C.shard_for_rank(C.cfg4(), rank, world)
+    # every rank sees the same recipe sizes but its own request ids
+    ids = torch.tensor(w.req_ids[:4], dtype=torch.int64)
+    gathered = [torch.zeros_like(ids) for _ in range(world)]
+    dist.all_gather(gathered, ids)
+    # bench.py's timing rule: the step time is the MAX over ranks
+    ms = torch.tensor([10.0 + 5.0 * rank])
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # strong scaling: every rank derives the same LPT assignment independently
+    parts = P.lpt([P.request_cost(n, m, 9216) for n, m in zip(w.n, w.modes)], world)
+    mine = torch.tensor([len(parts[rank]), sum(w.n[i] for i in parts[rank])], dtype=torch.int64)
+    all_parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(all_parts, mine)
+    out[rank] = {"ids": [g.tolist() for g in gathered], "ms": float(ms.item()),
+                 "n_tok": w.n_tokens(), "parts": [p.tolist() for p in all_parts]}
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharding_and_max_timing():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    r0, r1 = out[0], out[1]
+    assert r0["ms"] == r1["ms"] == 15.0
+    assert r0["n_tok"] == r1["n_tok"]
+    a, b = r0["ids"]
+    assert set(a).isdisjoint(b)                      # distinct requests per rank
+    assert r0["parts"] == r1["parts"]               # identical LPT on every rank
+    assert sum(p[0] for p in r0["parts"]) == 256
+
+
+def test_lpt_balance_and_coverage():
+    w = C.cfg4()
+    costs = [P.request_cost(n, m, w.shape.d) for n, m in zip(w.n, w.modes)]
+    for G in (2, 4, 8):
+        parts = P.lpt(costs, G)
+        flat = sorted(i for p in parts for i in p)
+        assert flat == list(range(len(costs)))
+        loads = [sum(costs[i] for i in p) for p in parts]
+        assert max(loads) / (sum(loads) / G) < 1.05     # near-linear strong scaling possible
+    # LPT bound (4/3 - 1/(3G)) on a classic instance
+    parts = P.lpt([3, 3, 2, 2, 2], 2)
+    assert sorted(sum([3, 3, 2, 2, 2][i] for i in p) for p in parts) == [5, 7]
+
+
+def test_strong_shard_subsets_partition_the_batch():
+    w = C.cfg2()
+    subs = [P.strong_shard(w, r, 4) for r in range(4)]
+    ids = sorted(i for s in subs for i in s.req_ids)
+    assert ids == sorted(w.req_ids)
