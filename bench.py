@@ -379,13 +379,13 @@ def main():
     k = kernels[dom]
     if dom == "recon_gemm":
         peak = tf_sus
-        roof = {"bound": "tensor", "kernel": "recon_tc_kernel", "achieved": k["achieved"], "peak": peak,
-                "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get("recon"),
+        roof = {"bound": "tensor", "kernel": "recon_tc2_kernel<2>", "achieved": k["achieved"], "peak": peak,
+                "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get("recon"),
                 "peak_kind": "bf16 sustained, " + peak_src}
     else:
         peak = hbm
-        roof = {"bound": "hbm", "kernel": "attn_pipe_kernel", "achieved": k["achieved"], "peak": peak,
-                "unit": "GB/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get("attention"),
+        roof = {"bound": "hbm", "kernel": "attn_pipe_kernel<128,8,3>", "achieved": k["achieved"], "peak": peak,
+                "unit": "GB/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get("attention"),
                 "peak_kind": "HBM copy, " + peak_src}
     T_roof = max(F_alg / (tf_sus * 1e12), B_alg / (hbm * 1e9))
     line = {

@@ -292,6 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + STAGES_;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* prow = reinterpret_cast<int32_t*>(tempty + 4);   // 16 gathered pool rows of the current tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -332,15 +333,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = pair; t < n_tiles_total; t += n_pairs) {
         int mt, nt;
         tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
-        int prow[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          prow[i] = 0;
-          if (i < nbox) {
-            const int grow = mt * P_BM + (int)rank * 128 + i * a.rows_per_box;
-            const int g = grow / a.B;
-            if (g < a.n_hblocks) prow[i] = a.gather[g] * a.B + (grow - g * a.B);
-          }
+        for (int i = 0; i < nbox; ++i) {
+          const int grow = mt * P_BM + (int)rank * 128 + i * a.rows_per_box;
+          const int g = grow / a.B;
+          prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
         }
         const int wrow = nt * PC::TILE_N + (int)rank * 128;
         for (int kb = 0; kb < a.k_iters; ++kb) {
