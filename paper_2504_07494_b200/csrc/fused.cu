@@ -1,0 +1,170 @@
+// Fused decode step (SURVEY §3.2 "[s1] reconstruction concurrent with [s2] KV attention",
+// hard part 4): one persistent kernel per SM running
+//   warps 0-5   the CTA-pair tcgen05 reconstruction GEMM (pair_gemm.cuh, 3-stage ring), and
+//   warps 6..   NA split-K attention warps (attn_pipe.cuh) on a shared task counter.
+// Attention tasks are ordered KV-mode first (their K/V are in the pool: they stream from HBM
+// while the tensor cores rebuild hidden K/V), then hidden-mode tasks in the GEMM's n-tile
+// order.  Before reading a hidden task's K/V a warp waits until every GEMM tile covering its
+// rows and head has been written: each of the 8 epilogue warps of a pair tile fences its
+// stores and adds 1 to the tile's counter (release); the attention warp acquires 8, then
+// fences the async proxy before its bulk copies.  The two workloads use different units —
+// tensor pipes + L2 for the GEMM, HBM + LSU for the KV stream — so near the KV/hidden
+// crossover the step approaches max(T_gemm, T_attn) instead of their sum.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+
+#include "attn_pipe.cuh"
+#include "internal.h"
+#include "pair_gemm.cuh"
+#include "ptx.cuh"
+
+namespace hc {
+namespace {
+
+constexpr int kNsub = 2;
+constexpr bool kLateJoin = true;
+using PC = pg::PairCfg<kNsub, 3>;   // default GEMM ring (3 x 48 KiB); tile geometry is stage-independent
+
+struct FusedTaskMap {
+  const AttnParams* p;
+  __device__ __forceinline__ void map(int t, int& split, int& head) const {
+    const int H = p->H;
+    if (t < p->n_kv_tasks) {
+      const int ks = t / H;
+      split = p->kv_split_ids[ks];
+      head = t - ks * H;
+      return;
+    }
+    const int hpt = p->gemm_tile_n / (2 * p->dh);     // heads per GEMM n-tile
+    const int u = t - p->n_kv_tasks;
+    const int per_nt = p->n_hid_splits * hpt;
+    const int nt = u / per_nt;
+    const int r = u - nt * per_nt;
+    split = p->hid_split_ids[r / hpt];
+    head = nt * hpt + r % hpt;
+  }
+  __device__ __forceinline__ void wait_ready(int /*split*/, int head, const SplitDesc& sp, const ReqDesc& rq,
+                                             int lane) const {
+    if (rq.mode != 1) return;
+    if (lane == 0) {
+      const int B = p->B;
+      const int g0 = rq.scratch_blk0 + sp.lb0;
+      const int nblk = (sp.ntok + B - 1) / B;
+      const int mt0 = (g0 * B) / p->gemm_tile_m, mt1 = ((g0 + nblk) * B - 1) / p->gemm_tile_m;
+      const int nt = head * 2 * p->dh / p->gemm_tile_n;
+      const long long t0 = clock64();
+      for (int mt = mt0; mt <= mt1; ++mt) {
+        const int32_t* f = p->tile_done + mt * p->gemm_n_tiles + nt;
+        while (pg::ld_acquire(f) < 8) {
+          __nanosleep(256);
+          if (clock64() - t0 > (1ll << 35)) __trap();
+        }
+      }
+      // K/V were written by generic stores; the bulk copies read through the async proxy.
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+  }
+};
+
+template <int GS, int NA, int NSTA>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * NA, 1)
+    fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                      const pg::TcArgs a, const AttnParams p) {
+  constexpr int kGemmStages = GS;
+  using PC = pg::PairCfg<kNsub, GS>;
+  // late-joining GEMM warps: as many 2-stage attention rings as fit in the GEMM stage buffers
+  constexpr int kJoin = (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2>::WARP_BYTES) < 6
+                            ? (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2>::WARP_BYTES) : 6;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+  const pg::PairSmem ps = pg::pair_carve<kNsub, kGemmStages>(smem);
+  uint8_t* attn_base = smem + PC::REGION_BYTES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pg::pair_setup<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *ps.tmem_slot;
+  if (warp < pg::GEMM_THREADS / 32) {
+    pg::pair_roles<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+    if (p.n_tasks > 0 && kLateJoin) {
+      // This CTA's GEMM has drained (the epilogue consumed the last tile, so the leader's
+      // UMMAs no longer read these stages): its 6 warps join the attention pool, each with a
+      // 2-stage ring carved from the freed GEMM stage buffers.
+      asm volatile("bar.sync 1, %0;" ::"n"(pg::GEMM_THREADS) : "memory");
+      ptx::fence_proxy_async_smem();
+      if (warp < kJoin) {
+        const FusedTaskMap tm{&p};
+        ap::attn_warp_run<128, 2>(p, ps.stages + warp * ap::PipeCfg<128, 2>::WARP_BYTES, lane, tm);
+      }
+    }
+  } else {
+    const FusedTaskMap tm{&p};
+    ap::attn_warp_run<128, NSTA>(p, attn_base + (warp - pg::GEMM_THREADS / 32) * ap::PipeCfg<128, NSTA>::WARP_BYTES,
+                                 lane, tm);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  pg::pair_teardown<kNsub, kGemmStages>(warp, tmem_base);
+}
+
+template <int GS, int NA, int NSTA>
+cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, int num_sms,
+                       cudaStream_t s) {
+  constexpr int smem = 1024 + pg::PairCfg<kNsub, GS>::REGION_BYTES + NA * ap::PipeCfg<128, NSTA>::WARP_BYTES;
+  static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
+  auto k = fused_step_kernel<GS, NA, NSTA>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int pairs = num_sms / 2;
+  k<<<2 * pairs, pg::GEMM_THREADS + 32 * NA, smem, s>>>(*static_cast<const CUtensorMap*>(tmx),
+                                                        *static_cast<const CUtensorMap*>(tmw), a, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool fused_supported(int d, int H, int dh, int B) {
+  return dh == 128 && d == H * dh && d % 64 == 0 && (2 * d) % (256 * kNsub) == 0 && B % 16 == 0 &&
+         B >= 16 && (B <= 128 || B % 256 == 0) && (B & (B - 1)) == 0;
+}
+int fused_tile_m() { return pg::P_BM; }
+int fused_tile_n() { return PC::TILE_N; }
+
+cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
+                         int32_t* tile_done, int num_sms, cudaStream_t s) {
+  pg::TcArgs a{};
+  a.gather = rp.gather;
+  a.n_hblocks = rp.n_hblocks;
+  a.B = rp.B;
+  a.M = rp.n_hblocks * rp.B;
+  a.rows_per_box = rp.B < 128 ? rp.B : 128;
+  a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
+  a.n_tiles = 2 * rp.d / PC::TILE_N;
+  a.k_iters = rp.d / pg::BK;
+  a.H = rp.H;
+  a.dh = rp.dh;
+  a.d = rp.d;
+  a.scr_k = static_cast<__nv_bfloat16*>(rp.scr_k);
+  a.scr_v = static_cast<__nv_bfloat16*>(rp.scr_v);
+  a.bias = rp.b_int;
+  a.group_m = -2;
+  a.l2_hint = 0;
+  a.sync_w = 8;
+  a.sync = (num_sms / 2 <= pg::kMaxSyncPairs) ? rp.sync_counter : nullptr;
+  a.tile_done = tile_done;
+  ap_.tile_done = tile_done;
+  ap_.gemm_n_tiles = a.n_tiles;
+  ap_.gemm_tile_m = pg::P_BM;
+  ap_.gemm_tile_n = PC::TILE_N;
+  // 3-stage GEMM ring + 4 attention warps x 2 stages (measured best of {3,4,2}, {3,3,3},
+  // {2,6,2}, {2,4,3}: two GEMM stages starve the tensor cores).
+  return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+}
+
+}  // namespace hc

@@ -40,6 +40,13 @@ struct AttnParams {
   int32_t n_tasks;        // n_splits * H; task = split * H + head
   int32_t H, dh, B, d;
   float scale_log2;       // scale * log2(e)
+  // ---- fused step kernel only: KV tasks first, then hidden tasks in GEMM n-tile order
+  const int32_t* kv_split_ids;   // splits of KV-mode requests
+  const int32_t* hid_split_ids;  // splits of hidden-mode requests, in scratch (GEMM row) order
+  int32_t n_kv_tasks;            // (#KV splits) * H
+  int32_t n_hid_splits;
+  const int32_t* tile_done;      // [gemm_m_tiles][gemm_n_tiles] finished epilogue warps (8 = ready)
+  int32_t gemm_n_tiles, gemm_tile_m, gemm_tile_n;
 };
 
 struct CombineParams {
@@ -94,6 +101,13 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
 bool recon_tc_supported(int d, int H, int dh, int B);
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s);
 bool attn_pipe_supported(int dtype, int dh, int B);
+// Fused step: reconstruction GEMM (CTA pairs, 256x512 tiles) and split-K attention warps in
+// one persistent kernel; hidden tasks wait on per-tile completion counters.
+bool fused_supported(int d, int H, int dh, int B);
+int fused_tile_m();
+int fused_tile_n();
+cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
+                         int32_t* tile_done, int num_sms, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 
 }  // namespace hc

@@ -1,0 +1,307 @@
+// CTA-pair (cta_group::2) tcgen05 reconstruction GEMM roles, shared by the stand-alone
+// reconstruction kernel (recon_tc.cu) and the fused step kernel (fused.cu).
+//
+//   [K || V] = X W_KV^T (+ b)        Eq. 1 applied to every cached x_j
+//
+// A CTA pair computes a 256 x (256*NSUB) tile.  CTA rank r loads A rows [r*128, r*128+128)
+// of the 256-row M tile (one TMA box per hidden block: the block-wise hidden cache IS the
+// A operand) and, for each 256-wide N sub-tile j, W_int rows [j*256 + r*128, +128); the
+// leader issues M=256 N=256 K=16 UMMAs that read both CTAs' smem; each CTA's TMEM holds its
+// own 128 rows x 256*NSUB fp32 columns.  Warp roles (192 threads):
+//   warp 0  TMA producer (both CTAs; bytes counted on the leader's full barrier)
+//   warp 1  TMEM allocator (both CTAs) and single-thread MMA issuer (leader only)
+//   warps 2-5  epilogue: tcgen05.ld -> (+bias) -> bf16 RNE -> scratch [hblock][H][B][dh]
+// Schedule: n-major raster (2 n-tiles per group) — pairs p and p^1 of a wave share an A
+// panel, every wave shares the group's W panels — plus a partner k-progress lockstep that
+// keeps p and p^1 within `sync_w` k-steps so the second reader of A hits in L2.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace hc {
+namespace pg {
+
+constexpr int BK = 64, BN = 256, P_BM = 256;
+constexpr int P_A_BYTES = 128 * BK * 2;   // this CTA's half of A: 16 KiB
+constexpr int P_B_BYTES = 128 * BK * 2;   // this CTA's half of one 256-wide B sub-tile: 16 KiB
+constexpr int TMEM_COLS = 512;
+constexpr int GEMM_THREADS = 192;
+constexpr int kMaxSyncPairs = 80;         // progress words reserved in the workspace header
+
+struct TcArgs {
+  const int32_t* gather;
+  int32_t n_hblocks, M, B, rows_per_box;
+  int32_t m_tiles, n_tiles, k_iters;
+  int32_t H, dh, d;
+  __nv_bfloat16* scr_k;
+  __nv_bfloat16* scr_v;
+  const float* bias;
+  int32_t group_m;      // raster group (m-tiles sweeping all n-tiles); < 0: n-major, -group_m n-tiles
+  int32_t l2_hint;      // 0 none, 1 A evict_last + W evict_first, 2 the reverse
+  int32_t* sync;        // zeroed per-pair progress words (stride 32 ints), nullptr = off
+  int32_t sync_w;       // partner lockstep window in k-steps
+  int32_t* tile_done;   // nullable: per (m-tile, n-tile) count of finished epilogue warps (8 = ready)
+};
+
+template <int NSUB, int NSTAGE>
+struct PairCfg {
+  static constexpr int STAGE_BYTES = P_A_BYTES + NSUB * P_B_BYTES;
+  static constexpr int STAGES = NSTAGE;
+  static constexpr int NACC = 2 / NSUB;   // accumulator buffers in the 512 TMEM columns
+  static constexpr int TILE_N = 256 * NSUB;
+  static constexpr int REGION_BYTES = STAGES * STAGE_BYTES + 512;   // stages + barriers (1024-aligned base)
+};
+
+__device__ __forceinline__ void tile_coords_p(int t, int m_tiles, int n_tiles, int group_m, int& mt, int& nt) {
+  if (group_m < 0) {  // n-major raster: -group_m n-tiles sweep all m-tiles
+    const int gn = -group_m;
+    const int per_group = gn * m_tiles;
+    const int g = t / per_group;
+    const int first_n = g * gn;
+    const int gsize = min(gn, n_tiles - first_n);
+    const int r = t - g * per_group;
+    nt = first_n + r % gsize;
+    mt = r / gsize;
+    return;
+  }
+  const int per_group = group_m * n_tiles;
+  const int g = t / per_group;
+  const int first_m = g * group_m;
+  const int gsize = min(group_m, m_tiles - first_m);
+  const int r = t - g * per_group;
+  mt = first_m + r % gsize;
+  nt = r / gsize;
+}
+
+__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct PairSmem {
+  uint8_t* stages;
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* tfull;
+  uint64_t* tempty;
+  uint32_t* tmem_slot;
+  int32_t* prow;   // 16 gathered pool rows of the producer's current tile
+};
+
+template <int NSUB, int NSTAGE>
+__device__ __forceinline__ PairSmem pair_carve(uint8_t* base /*1024-aligned*/) {
+  using PC = PairCfg<NSUB, NSTAGE>;
+  PairSmem s;
+  s.stages = base;
+  s.full = reinterpret_cast<uint64_t*>(base + PC::STAGES * PC::STAGE_BYTES);
+  s.empty = s.full + PC::STAGES;
+  s.tfull = s.empty + PC::STAGES;
+  s.tempty = s.tfull + 2;
+  s.tmem_slot = reinterpret_cast<uint32_t*>(s.tempty + 2);
+  s.prow = reinterpret_cast<int32_t*>(s.tempty + 4);
+  return s;
+}
+
+// Barrier init (warp 0) and pair TMEM allocation (warp 1, both CTAs).  The caller must then
+// run tc_fence_before; cluster_sync; tc_fence_after before reading *tmem_slot.
+template <int NSUB, int NSTAGE>
+__device__ __forceinline__ void pair_setup(const PairSmem& s, int warp, int lane, const CUtensorMap* tmx,
+                                           const CUtensorMap* tmw) {
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(tmx);
+    ptx::prefetch_tmap(tmw);
+    for (int i = 0; i < NSTAGE; ++i) {
+      ptx::mbar_init(&s.full[i], 1);
+      ptx::mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s.tfull[i], 1);
+      ptx::mbar_init(&s.tempty[i], 8);   // 4 epilogue warps x 2 CTAs (used on the leader)
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_cg2<TMEM_COLS>(s.tmem_slot);
+}
+
+// Roles of warps 0..5.  Call with warp < 6 only.
+template <int NSUB, int NSTAGE>
+__device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane, const CUtensorMap* tmap_x,
+                                           const CUtensorMap* tmap_w, const TcArgs& a, uint32_t tmem_base) {
+  using PC = PairCfg<NSUB, NSTAGE>;
+  constexpr int STAGES_ = PC::STAGES, NACC = PC::NACC;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_tiles_total = a.m_tiles * a.n_tiles;
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs) =================
+    if (lane == 0) {
+      const uint64_t pol_a = a.l2_hint == 2 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+      const uint64_t pol_b = a.l2_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      int my_step = 0;
+      const bool sync_on = a.sync != nullptr && leader && (pair ^ 1) < n_pairs;
+      const int nbox = 128 / a.rows_per_box;
+      const int box_bytes = a.rows_per_box * BK * 2;
+      for (int t = pair; t < n_tiles_total; t += n_pairs) {
+        int mt, nt;
+        tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
+        for (int i = 0; i < nbox; ++i) {
+          const int grow = mt * P_BM + (int)rank * 128 + i * a.rows_per_box;
+          const int g = grow / a.B;
+          s.prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
+        }
+        const int wrow = nt * PC::TILE_N + (int)rank * 128;
+        for (int kb = 0; kb < a.k_iters; ++kb) {
+          if (sync_on && (my_step & 7) == 0) {
+            // partner lockstep: pairs p and p^1 share the A panel; keep them within sync_w
+            // k-steps so the second reader hits in L2.
+            st_relaxed(a.sync + 32 * pair, my_step);
+            if (my_step > a.sync_w) {
+              const long long t0 = clock64();
+              while (ld_relaxed(a.sync + 32 * (pair ^ 1)) < my_step - a.sync_w) {
+                if (clock64() - t0 > (1ll << 34)) __trap();
+              }
+            }
+          }
+          ptx::mbar_wait(&s.empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&s.full[stage], 2 * PC::STAGE_BYTES);
+          uint8_t* dA = s.stages + stage * PC::STAGE_BYTES;
+          uint8_t* dB = dA + P_A_BYTES;
+          if (a.l2_hint == 0) {
+            for (int i = 0; i < nbox; ++i)
+              ptx::tma_load_2d_cg2(dA + i * box_bytes, tmap_x, kb * BK, s.prow[i], &s.full[stage]);
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j)
+              ptx::tma_load_2d_cg2(dB + j * P_B_BYTES, tmap_w, kb * BK, wrow + j * 256, &s.full[stage]);
+          } else {
+            for (int i = 0; i < nbox; ++i)
+              ptx::tma_load_2d_cg2_hint(dA + i * box_bytes, tmap_x, kb * BK, s.prow[i], &s.full[stage], pol_a);
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j)
+              ptx::tma_load_2d_cg2_hint(dB + j * P_B_BYTES, tmap_w, kb * BK, wrow + j * 256, &s.full[stage], pol_b);
+          }
+          ++my_step;
+          if (++stage == STAGES_) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (sync_on) st_relaxed(a.sync + 32 * pair, 0x7fffffff);  // done: never hold the partner
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA only) =================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc_bf16_f32(P_BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
+        const int acc = it % NACC;
+        const uint32_t acc_phase = (it / NACC) & 1;
+        ptx::mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * PC::TILE_N;
+        for (int kb = 0; kb < a.k_iters; ++kb) {
+          ptx::mbar_wait(&s.full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(s.stages + stage * PC::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + P_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = ptx::umma_desc_k_sw128(a_addr + k * 32);
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+              const uint64_t bd = ptx::umma_desc_k_sw128(b_addr + j * P_B_BYTES + k * 32);
+              ptx::umma_f16_ss_cg2(d_tmem + j * 256, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+          }
+          ptx::umma_commit_cg2_mc(&s.empty[stage], 0x3);
+          if (++stage == STAGES_) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit_cg2_mc(&s.tfull[acc], 0x3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue (warps 2..5 of both CTAs) =================
+    const int q = warp & 3;
+    const int row_in_tile = (int)rank * 128 + q * 32 + lane;
+    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&s.tempty[0]), 0);
+    int it = 0;
+    for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
+      int mt, nt;
+      tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
+      const int acc = it % NACC;
+      const uint32_t acc_phase = (it / NACC) & 1;
+      ptx::mbar_wait(&s.tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int grow = mt * P_BM + row_in_tile;
+      const bool valid = grow < a.M;
+      const int g = grow / a.B, r = grow - g * a.B;
+#pragma unroll 1
+      for (int c = 0; c < PC::TILE_N / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, v);
+        ptx::tmem_ld_wait();
+        const int n = nt * PC::TILE_N + c * 32;
+        const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        if (a.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += __ldg(a.bias + n + j);
+        }
+        if (valid) {
+          __nv_bfloat16* dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            d4[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+                               pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
+        }
+      }
+      ptx::tc_fence_before();
+      if (a.tile_done) __threadfence();   // this warp's rows are globally visible before the count
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        if (a.tile_done) red_release_add(a.tile_done + mt * a.n_tiles + nt, 1);
+      }
+    }
+  }
+}
+
+template <int NSUB, int NSTAGE>
+__device__ __forceinline__ void pair_teardown(int warp, uint32_t tmem_base) {
+  if (warp == 1) ptx::tmem_dealloc_cg2<TMEM_COLS>(tmem_base);
+}
+
+}  // namespace pg
+}  // namespace hc

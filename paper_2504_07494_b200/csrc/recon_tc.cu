@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "pair_gemm.cuh"
 #include "ptx.cuh"
 
 namespace hc {
@@ -41,20 +42,6 @@ constexpr int GROUP_M = 16;
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 
-struct TcArgs {
-  const int32_t* gather;
-  int32_t n_hblocks, M, B, rows_per_box;
-  int32_t m_tiles, n_tiles, k_iters;
-  int32_t H, dh, d;
-  __nv_bfloat16* scr_k;
-  __nv_bfloat16* scr_v;
-  const float* bias;
-  int32_t group_m;   // raster group (m-tiles sweeping all n-tiles); < 0: n-major
-  int32_t* sync;     // zeroed per-pair progress words (stride 32 ints), nullptr = off
-  int32_t sync_w;    // partner lockstep window in k-steps
-  int32_t l2_hint;   // 0 none, 1 A evict_last + W evict_first, 2 A evict_first + W evict_last
-};
-
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& mt, int& nt) {
   const int per_group = GROUP_M * n_tiles;
   const int g = t / per_group;
@@ -65,23 +52,9 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
   nt = r / gsize;
 }
 
-__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
-  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     recon_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                    const TcArgs a) {
+                    const pg::TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
@@ -218,8 +191,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            d4[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
+            d4[j] = make_uint4(pg::pack_bf16(f[8 * j], f[8 * j + 1]), pg::pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+                               pg::pack_bf16(f[8 * j + 4], f[8 * j + 5]), pg::pack_bf16(f[8 * j + 6], f[8 * j + 7]));
         }
       }
       ptx::tc_fence_before();
@@ -234,248 +207,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 
 // ------------------------------------------------------------------------------------
-// 2-SM version (cta_group::2): a CTA pair computes a 256 x (256*NSUB) tile.  CTA rank r
-// loads A rows [r*128, r*128+128) of the 256-row M tile and, for each 256-wide N sub-tile
-// j, W_KV rows [j*256 + r*128, +128); the leader issues M=256 N=256 UMMAs that read both
-// CTAs' smem, and each CTA's TMEM receives its own 128 rows x 256*NSUB columns.
-//   NSUB = 1: 32 KiB/stage/CTA, 6 stages, two TMEM accumulator buffers (epilogue overlaps).
-//   NSUB = 2: 48 KiB/stage/CTA, 4 stages, one 512-column accumulator; 25% fewer operand
-//             bytes per FLOP (A is reused across both N sub-tiles), which is what binds
-//             when the L2 -> SM operand stream is the bottleneck.
-constexpr int P_BM = 256;
-constexpr int P_A_BYTES = 128 * BK * 2;   // this CTA's half of A: 16 KiB
-constexpr int P_B_BYTES = 128 * BK * 2;   // this CTA's half of one 256-wide B sub-tile: 16 KiB
-constexpr int P_GROUP_M = 8;
-
-template <int NSUB>
-struct PairCfg {
-  static constexpr int STAGE_BYTES = P_A_BYTES + NSUB * P_B_BYTES;
-  static constexpr int STAGES = NSUB == 1 ? 6 : 4;
-  static constexpr int NACC = 2 / NSUB;   // accumulator buffers in the 512 TMEM columns
-  static constexpr int TILE_N = 256 * NSUB;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 512;
-};
-
-__device__ __forceinline__ void tile_coords_p(int t, int m_tiles, int n_tiles, int group_m, int& mt, int& nt) {
-  if (group_m < 0) {  // n-major raster: -group_m n-tiles sweep all m-tiles
-    const int gn = -group_m;
-    const int per_group = gn * m_tiles;
-    const int g = t / per_group;
-    const int first_n = g * gn;
-    const int gsize = min(gn, n_tiles - first_n);
-    const int r = t - g * per_group;
-    nt = first_n + r % gsize;
-    mt = r / gsize;
-    return;
-  }
-  const int per_group = group_m * n_tiles;
-  const int g = t / per_group;
-  const int first_m = g * group_m;
-  const int gsize = min(group_m, m_tiles - first_m);
-  const int r = t - g * per_group;
-  mt = first_m + r % gsize;
-  nt = r / gsize;
-}
-
-template <int NSUB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+// CTA-pair kernel: the roles live in pair_gemm.cuh (shared with the fused step kernel).
+template <int NSUB, int NSTAGE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS, 1)
     recon_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                     const TcArgs a) {
-  using PC = PairCfg<NSUB>;
-  constexpr int STAGES_ = PC::STAGES, NACC = PC::NACC;
+                     const pg::TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-  // stage s: A half at s*STAGE_BYTES, then NSUB B halves
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES_ * PC::STAGE_BYTES);
-  uint64_t* empty = full + STAGES_;
-  uint64_t* tfull = empty + STAGES_;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int32_t* prow = reinterpret_cast<int32_t*>(tempty + 4);   // 16 gathered pool rows of the current tile
-
+  const pg::PairSmem ps = pg::pair_carve<NSUB, NSTAGE>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int n_tiles_total = a.m_tiles * a.n_tiles;
-
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmap_x);
-    ptx::prefetch_tmap(&tmap_w);
-    for (int s = 0; s < STAGES_; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 8);   // 4 epilogue warps x 2 CTAs (used on the leader)
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) ptx::tmem_alloc_cg2<TMEM_COLS>(tmem_slot);
+  pg::pair_setup<NSUB, NSTAGE>(ps, warp, lane, &tmap_x, &tmap_w);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ================= TMA producer (both CTAs) =================
-    if (lane == 0) {
-      const uint64_t pol_a = a.l2_hint == 2 ? ptx::policy_evict_first() : ptx::policy_evict_last();
-      const uint64_t pol_b = a.l2_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      int my_step = 0;
-      const bool sync_on = a.sync != nullptr && leader && (pair ^ 1) < n_pairs;
-      const int nbox = 128 / a.rows_per_box;
-      const int box_bytes = a.rows_per_box * BK * 2;
-      for (int t = pair; t < n_tiles_total; t += n_pairs) {
-        int mt, nt;
-        tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
-        for (int i = 0; i < nbox; ++i) {
-          const int grow = mt * P_BM + (int)rank * 128 + i * a.rows_per_box;
-          const int g = grow / a.B;
-          prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
-        }
-        const int wrow = nt * PC::TILE_N + (int)rank * 128;
-        for (int kb = 0; kb < a.k_iters; ++kb) {
-          if (sync_on && (my_step & 7) == 0) {
-            // partner lockstep: pairs p and p^1 share the A panel (n-major raster, 2 n-tiles
-            // per group); keep them within sync_w k-steps so the second reader hits in L2.
-            st_relaxed(a.sync + 32 * pair, my_step);
-            if (my_step > a.sync_w) {
-              const long long t0 = clock64();
-              while (ld_relaxed(a.sync + 32 * (pair ^ 1)) < my_step - a.sync_w) {
-                if (clock64() - t0 > (1ll << 34)) __trap();
-              }
-            }
-          }
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * PC::STAGE_BYTES);
-          uint8_t* dA = smem + stage * PC::STAGE_BYTES;
-          uint8_t* dB = dA + P_A_BYTES;
-          if (a.l2_hint == 0) {
-            for (int i = 0; i < nbox; ++i)
-              ptx::tma_load_2d_cg2(dA + i * box_bytes, &tmap_x, kb * BK, prow[i], &full[stage]);
-#pragma unroll
-            for (int j = 0; j < NSUB; ++j)
-              ptx::tma_load_2d_cg2(dB + j * P_B_BYTES, &tmap_w, kb * BK, wrow + j * 256, &full[stage]);
-          } else {
-            for (int i = 0; i < nbox; ++i)
-              ptx::tma_load_2d_cg2_hint(dA + i * box_bytes, &tmap_x, kb * BK, prow[i], &full[stage], pol_a);
-#pragma unroll
-            for (int j = 0; j < NSUB; ++j)
-              ptx::tma_load_2d_cg2_hint(dB + j * P_B_BYTES, &tmap_w, kb * BK, wrow + j * 256, &full[stage], pol_b);
-          }
-          ++my_step;
-          if (++stage == STAGES_) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-      if (sync_on) st_relaxed(a.sync + 32 * pair, 0x7fffffff);  // done: never hold the partner
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer (leader CTA only) =================
-    if (leader && lane == 0) {
-      constexpr uint32_t idesc = ptx::umma_idesc_bf16_f32(P_BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
-        const int acc = it % NACC;
-        const uint32_t acc_phase = (it / NACC) & 1;
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * PC::TILE_N;
-        for (int kb = 0; kb < a.k_iters; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem + stage * PC::STAGE_BYTES);
-          const uint32_t b_addr = a_addr + P_A_BYTES;
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = ptx::umma_desc_k_sw128(a_addr + k * 32);
-#pragma unroll
-            for (int j = 0; j < NSUB; ++j) {
-              const uint64_t bd = ptx::umma_desc_k_sw128(b_addr + j * P_B_BYTES + k * 32);
-              ptx::umma_f16_ss_cg2(d_tmem + j * 256, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-            }
-          }
-          ptx::umma_commit_cg2_mc(&empty[stage], 0x3);
-          if (++stage == STAGES_) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        ptx::umma_commit_cg2_mc(&tfull[acc], 0x3);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ================= epilogue (warps 2..5 of both CTAs) =================
-    const int q = warp & 3;
-    const int row_in_tile = (int)rank * 128 + q * 32 + lane;
-    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
-    int it = 0;
-    for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
-      int mt, nt;
-      tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
-      const int acc = it % NACC;
-      const uint32_t acc_phase = (it / NACC) & 1;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      const int grow = mt * P_BM + row_in_tile;
-      const bool valid = grow < a.M;
-      const int g = grow / a.B, r = grow - g * a.B;
-#pragma unroll 1
-      for (int c = 0; c < PC::TILE_N / 32; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, v);
-        ptx::tmem_ld_wait();
-        const int n = nt * PC::TILE_N + c * 32;
-        const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        if (a.bias) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] += __ldg(a.bias + n + j);
-        }
-        if (valid) {
-          __nv_bfloat16* dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            d4[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
-        }
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
-    }
-  }
+  const uint32_t tmem_base = *ps.tmem_slot;
+  pg::pair_roles<NSUB, NSTAGE>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  if (warp == 1) ptx::tmem_dealloc_cg2<TMEM_COLS>(tmem_base);
+  pg::pair_teardown<NSUB, NSTAGE>(warp, tmem_base);
 }
 
-template <int NSUB>
-cudaError_t launch_pair(TcArgs a, const void* tmap_x, const void* tmap_w_half, int num_sms, cudaStream_t s) {
-  using PC = PairCfg<NSUB>;
-  a.m_tiles = (a.M + P_BM - 1) / P_BM;
+template <int NSUB, int NSTAGE>
+cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_half, int num_sms, cudaStream_t s) {
+  using PC = pg::PairCfg<NSUB, NSTAGE>;
+  constexpr int smem = 1024 + PC::REGION_BYTES;
+  a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
   a.n_tiles = 2 * a.d / PC::TILE_N;
-  cudaError_t e = cudaFuncSetAttribute(recon_tc2_kernel<NSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PC::SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(recon_tc2_kernel<NSUB, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int tiles = a.m_tiles * a.n_tiles;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  if (pairs > 80) a.sync = nullptr;  // progress words reserved for <= 80 pairs
-  recon_tc2_kernel<NSUB><<<2 * pairs, NUM_THREADS, PC::SMEM_BYTES, s>>>(
+  if (pairs > pg::kMaxSyncPairs) a.sync = nullptr;
+  recon_tc2_kernel<NSUB, NSTAGE><<<2 * pairs, pg::GEMM_THREADS, smem, s>>>(
       *static_cast<const CUtensorMap*>(tmap_x), *static_cast<const CUtensorMap*>(tmap_w_half), a);
   return cudaGetLastError();
 }
@@ -499,7 +264,7 @@ bool recon_tc_supported(int d, int H, int dh, int B) {
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
                             const void* tmap_w_half, int num_sms, cudaStream_t s) {
   if (p.n_hblocks <= 0) return cudaSuccess;
-  TcArgs a;
+  pg::TcArgs a{};
   a.gather = p.gather;
   a.n_hblocks = p.n_hblocks;
   a.B = p.B;
@@ -526,8 +291,11 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   if (pair_mode) {
     const int nsub_env = getenv_int("HC_TC_NSUB");
     const bool can2 = (2 * p.d) % 512 == 0;
-    if (can2 && nsub_env != 1) return launch_pair<2>(a, tmap_x, tmap_w_half, num_sms, s);
-    return launch_pair<1>(a, tmap_x, tmap_w_half, num_sms, s);
+    if (can2 && nsub_env != 1) {
+      if (getenv_int("HC_TC_STAGES") == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s);
+      return launch_pair<2, 4>(a, tmap_x, tmap_w_half, num_sms, s);
+    }
+    return launch_pair<1, 6>(a, tmap_x, tmap_w_half, num_sms, s);
   }
   cudaError_t e = cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;

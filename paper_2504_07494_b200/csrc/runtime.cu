@@ -126,8 +126,11 @@ struct Pinned {
 // Decode-call plan: sizes and offsets inside the caller's workspace.
 struct Plan {
   int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1;
+  int32_t n_kv_splits = 0, n_hid_splits = 0;
+  bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
+  int32_t gemm_m_tiles = 0, gemm_n_tiles = 0;
   int64_t n_tab = 0;
-  size_t off_reqs, off_splits, off_tabs, off_gather, desc_bytes;
+  size_t off_reqs, off_splits, off_tabs, off_gather, off_kvsplit, off_hidsplit, off_tiledone, desc_bytes;
   size_t off_ml, off_acc, off_sk, off_sv, total;
 };
 
@@ -219,9 +222,23 @@ struct hc_pool {
     P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
     for (auto* r : rs) {
       const int64_t nb = cdiv(r->n, B);
-      P.n_splits += (int32_t)cdiv(nb, P.split_blocks);
-      if (r->mode == HC_MODE_KV) P.n_tab += 2 * nb;
-      else P.n_hb += (int32_t)nb;
+      const int32_t ns = (int32_t)cdiv(nb, P.split_blocks);
+      P.n_splits += ns;
+      if (r->mode == HC_MODE_KV) {
+        P.n_tab += 2 * nb;
+        P.n_kv_splits += ns;
+      } else {
+        P.n_hb += (int32_t)nb;
+        P.n_hid_splits += ns;
+      }
+    }
+    const char* fe = std::getenv("HC_FUSED");
+    const int fused_env = fe ? std::atoi(fe) : -1;
+    P.fused = tc_ok && P.n_hb > 0 && fused_env != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
+              fused_supported(cfg.d_model, cfg.n_heads, cfg.head_dim, B);
+    if (P.fused) {
+      P.gemm_m_tiles = (int32_t)cdiv((int64_t)P.n_hb * B, fused_tile_m());
+      P.gemm_n_tiles = 2 * cfg.d_model / fused_tile_n();
     }
     size_t o = kHeaderBytes;  // header: attention task counter, then GEMM pair-progress words
     P.off_reqs = o = align_up(o, 64);
@@ -232,6 +249,12 @@ struct hc_pool {
     o += sizeof(int32_t) * P.n_tab;
     P.off_gather = o = align_up(o, 64);
     o += sizeof(int32_t) * P.n_hb;
+    P.off_kvsplit = o = align_up(o, 64);
+    o += P.fused ? sizeof(int32_t) * P.n_kv_splits : 0;
+    P.off_hidsplit = o = align_up(o, 64);
+    o += P.fused ? sizeof(int32_t) * P.n_hid_splits : 0;
+    P.off_tiledone = o = align_up(o, 64);
+    o += P.fused ? sizeof(int32_t) * (size_t)P.gemm_m_tiles * P.gemm_n_tiles : 0;
     P.desc_bytes = align_up(o, kAlign);
     const size_t n_tasks = (size_t)P.n_splits * H;
     P.off_ml = P.desc_bytes;
@@ -532,7 +555,10 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   SplitDesc* sd = reinterpret_cast<SplitDesc*>(h + P.off_splits);
   int32_t* tab = reinterpret_cast<int32_t*>(h + P.off_tabs);
   int32_t* gat = reinterpret_cast<int32_t*>(h + P.off_gather);
-  int32_t n_split = 0, n_tab = 0, n_hb = 0;
+  int32_t* kvs = reinterpret_cast<int32_t*>(h + P.off_kvsplit);
+  int32_t* hds = reinterpret_cast<int32_t*>(h + P.off_hidsplit);
+  int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0;
+  if (P.fused) std::memset(h + P.off_tiledone, 0, P.desc_bytes - P.off_tiledone);
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = *rs[i];
     const int32_t nb = (int32_t)cdiv(r.n, B);
@@ -556,6 +582,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       s.lb0 = lb;
       const int64_t t0 = (int64_t)lb * B;
       s.ntok = (int32_t)std::min<int64_t>((int64_t)P.split_blocks * B, r.n - t0);
+      if (P.fused) (r.mode == HC_MODE_KV ? kvs[n_kvs++] : hds[n_hds++]) = n_split;
       sd[n_split++] = s;
     }
     d.split_count = n_split - d.split_begin;
@@ -577,29 +604,21 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
 
   char* blocks = pool->storage + pool->L.blocks_off;
   int launches = 0;
-  // ---- a4: K/V reconstruction of hidden-mode requests
-  if (P.n_hb > 0) {
-    ReconParams rp;
-    rp.gather = reinterpret_cast<const int32_t*>(ws + P.off_gather);
-    rp.n_hblocks = P.n_hb;
-    rp.pool = blocks;
-    rp.w_int = pool->storage + pool->L.w_off;
-    rp.b_int = pool->has_bias ? reinterpret_cast<const float*>(pool->storage + pool->L.b_off) : nullptr;
-    rp.scr_k = ws + P.off_sk;
-    rp.scr_v = ws + P.off_sv;
-    rp.d = pool->cfg.d_model;
-    rp.H = H;
-    rp.dh = pool->cfg.head_dim;
-    rp.B = B;
-    rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
-    err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, s)
-                      : launch_recon_simt(rp, pool->cfg.dtype, s);
-    if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
-    ++launches;
-  }
-  if (pool->profiling) cudaEventRecord(ev[2], s);
-  // ---- a5: split-K attention over KV blocks and rebuilt K/V
-  AttnParams ap;
+  // ---- a4 + a5: K/V reconstruction of hidden-mode requests, split-K attention
+  ReconParams rp{};
+  rp.gather = reinterpret_cast<const int32_t*>(ws + P.off_gather);
+  rp.n_hblocks = P.n_hb;
+  rp.pool = blocks;
+  rp.w_int = pool->storage + pool->L.w_off;
+  rp.b_int = pool->has_bias ? reinterpret_cast<const float*>(pool->storage + pool->L.b_off) : nullptr;
+  rp.scr_k = ws + P.off_sk;
+  rp.scr_v = ws + P.off_sv;
+  rp.d = pool->cfg.d_model;
+  rp.H = H;
+  rp.dh = pool->cfg.head_dim;
+  rp.B = B;
+  rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
+  AttnParams ap{};
   ap.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
   ap.splits = reinterpret_cast<const SplitDesc*>(ws + P.off_splits);
   ap.tables = reinterpret_cast<const int32_t*>(ws + P.off_tabs);
@@ -616,10 +635,32 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.B = B;
   ap.d = pool->cfg.d_model;
   ap.scale_log2 = scale * 1.4426950408889634f;
-  err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
-  if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
-  ++launches;
-  if (pool->profiling) cudaEventRecord(ev[3], s);
+  if (P.fused) {
+    ap.kv_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_kvsplit);
+    ap.hid_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_hidsplit);
+    ap.n_kv_tasks = P.n_kv_splits * H;
+    ap.n_hid_splits = P.n_hid_splits;
+    err = launch_fused(rp, ap, &pool->tmap_x, &pool->tmap_w_half, reinterpret_cast<int32_t*>(ws + P.off_tiledone),
+                       pool->num_sms, s);
+    if (err != cudaSuccess) return cuda_fail(err, "fused step kernel");
+    ++launches;
+    if (pool->profiling) {
+      cudaEventRecord(ev[2], s);   // fused time is reported as the reconstruction slot
+      cudaEventRecord(ev[3], s);
+    }
+  } else {
+    if (P.n_hb > 0) {
+      err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, s)
+                        : launch_recon_simt(rp, pool->cfg.dtype, s);
+      if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
+      ++launches;
+    }
+    if (pool->profiling) cudaEventRecord(ev[2], s);
+    err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
+    if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
+    ++launches;
+    if (pool->profiling) cudaEventRecord(ev[3], s);
+  }
   // ---- a6: combine splits
   CombineParams cp;
   cp.reqs = ap.reqs;

@@ -7,7 +7,7 @@ for envs in "$@"; do
 import json,sys
 try:
   d=json.loads(sys.stdin.read()); k=d["kernels"]
-  print("ms/step=%.3f recon=%.3fms (%.0f TF/s) attn=%.3fms (%.0f GB/s) comb=%.3f frac_step=%.3f clk=%s" % (d["ms_per_step"], k["recon_gemm"]["ms"], k["recon_gemm"]["achieved"] or 0, k["attention"]["ms"], k["attention"]["achieved"] or 0, k["combine"]["ms"], d["step_roofline"]["frac"], d["clocks"]))
+  print("ms/step=%.3f recon=%.3fms (%.0f TF/s) attn=%.3fms (%.0f GB/s) comb=%.3f frac_step=%.3f clk=%s" % (d["ms_per_step"], (k.get("recon_gemm") or k.get("fused_step"))["ms"], (k.get("recon_gemm") or k.get("fused_step"))["achieved"] or 0, k["attention"]["ms"], k["attention"]["achieved"] or 0, k["combine"]["ms"], d["step_roofline"]["frac"], d["clocks"]))
 except Exception as e: print("ERR", e)
 ')"
   tail -3 /tmp/err.txt

@@ -267,3 +267,25 @@ def test_synth_bit_identical_on_device():
         assert torch.equal(a, b)
     w = C.cfg4()
     assert torch.equal(w.w_kv(rows=(100, 140)), w.w_kv(device="cuda", rows=(100, 140)).cpu())
+
+
+@pytest.mark.parametrize("env", [{"HC_FUSED": "0"}, {"HC_FUSED": "0", "HC_TC_1SM": "1"},
+                                 {"HC_FUSED": "0", "HC_TC_NSUB": "1"}])
+def test_bf16_alternative_gemm_schedules(hc, monkeypatch, env):
+    """Non-default GEMM paths (stand-alone CTA-pair GEMM + attention kernel, the 1-SM
+    tcgen05 kernel, 256-wide pair tiles) meet the same bar as the fused default."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = _bf16_workload(512, 4, 128, 16, bias=True)
+    _, out, lse = _run(w)
+    assert T.compare(w, out, lse, range(len(w.n)))[0] <= TOL_BF16
+
+
+def test_fused_and_unfused_agree_bitwise(hc, monkeypatch):
+    """The fused step kernel and the two-kernel path compute the same thing in the same
+    order (same GEMM tiles, same split-K tasks) => identical bits."""
+    w = _bf16_workload(512, 4, 128, 16, bias=True)
+    _, a, la = _run(w, split_tokens=64)
+    monkeypatch.setenv("HC_FUSED", "0")
+    _, b, lb = _run(w, split_tokens=64)
+    assert np.array_equal(a, b) and np.array_equal(la, lb)
