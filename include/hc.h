@@ -75,6 +75,13 @@ typedef struct {
   const float* b_kv;     /* nullable device [2d] fp32 bias (b_K then b_V); copied at create */
   int32_t device;        /* CUDA device ordinal the storage lives on */
   int32_t split_tokens;  /* split-K chunk in tokens (multiple of B); 0 = automatic */
+  /* Optional rest of the attention module (NEXT row f1; all nullable, copied at create):
+   * w_q [d, d] (q = W_Q x, Eq. 1), b_q [d] fp32; w_o [d, d] (the output map of Eq. 3),
+   * b_o [d] fp32.  Required by hc_project_append / hc_output_projection / hc_decode_layer. */
+  const void* w_q;
+  const float* b_q;
+  const void* w_o;
+  const float* b_o;
 } hc_pool_config;
 
 /* Bytes of device storage a pool with this config needs: the unit blocks, the
@@ -130,6 +137,29 @@ size_t hc_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_
 hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
                               const void* q, float scale, void* out, float* lse,
                               void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- the rest of the attention module (NEXT row f1) --------------------------------- */
+/* Current-token projections and cache append for one decode step: Eq. 1 for the new token
+ * fused with the block-wise cache write (the paper's I/O kernel).
+ *   x      device [n_req, d]: layer input of each request's current token.
+ *   q_out  device [n_req, d]: q = W_Q x (+ b_Q), for every request.
+ * KV-mode requests: k = W_K x (+b_K), v = W_V x (+b_V) are written by the GEMM epilogue
+ * straight into the request's cache slot (one [H][B][dh] row per head).  Hidden-mode
+ * requests: x itself is appended (their K/V are rebuilt at attention time).  Each
+ * request gains one token; allocation, modes and errors as hc_append (new ids allowed).
+ * Needs the pool's w_q.  Asynchronous on `stream`. */
+hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                            const void* x, void* q_out, void* stream);
+/* y = W_O o (+ b_O): the output map of Eq. 3.  o, y device [n_req, d]. */
+hc_status hc_output_projection(hc_pool* pool, int32_t n_req, const void* o, void* y, void* stream);
+/* One attention layer for one decode step: hc_project_append, hc_decode_attention,
+ * hc_output_projection in sequence.  `workspace` >= hc_layer_workspace_size() bytes,
+ * sized for the batch AFTER the current token is appended (unknown ids count as n = 1).
+ * lse (nullable) as hc_decode_attention. */
+size_t hc_layer_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes);
+hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                          const void* x, float scale, void* y, float* lse, void* workspace, size_t ws_bytes,
+                          void* stream);
 
 /* ---- introspection (host-side, no device work) ------------------------------------ */
 int64_t hc_pool_num_free(const hc_pool* pool);

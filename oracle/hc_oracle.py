@@ -117,6 +117,33 @@ def head_output(q_h, X, W_K_h, W_V_h, scale: float, b_K_h=None, b_V_h=None):
     return o, l[0]
 
 
+def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float,
+                    b_Q=None, b_KV=None, b_O=None):
+    """One attention layer for one decode step of one request (NEXT row f1):
+    q = W_Q x_t (+b_Q) and, for the current token, k, v = W_K x_t, W_V x_t (+b)  (Eq. 1,
+    P:121-125); the current token joins the context: KV mode appends (k, v) to
+    the cached K, V; hidden mode appends x_t to the cached X and rebuilds K, V from all of X
+    (P:269); then Eq. 2-3 with the output map y = W_O o (+b_O) (Eq. 3).
+    cache = {'mode': 0, 'K': [n-1, d], 'V': [n-1, d]} or {'mode': 1, 'X': [n-1, d]}.
+    Returns y [d], q [d], lse [H], and the context the attention saw (dict)."""
+    x_t, W_Q, W_O = _f64(x_t), _f64(W_Q), _f64(W_O)
+    W_KV = _f64(W_KV)
+    d = x_t.shape[0]
+    q = W_Q @ x_t + (0.0 if b_Q is None else _f64(b_Q))
+    if cache["mode"] == 1:
+        X = np.concatenate([_f64(cache["X"]).reshape(-1, d), x_t[None, :]])
+        K, V = hidden_request_kv(X, W_KV, b_KV)
+        ctx = {"mode": 1, "X": X}
+    else:
+        kv = W_KV @ x_t + (0.0 if b_KV is None else _f64(b_KV))
+        K = np.concatenate([_f64(cache["K"]).reshape(-1, d), kv[None, :d]])
+        V = np.concatenate([_f64(cache["V"]).reshape(-1, d), kv[None, d:]])
+        ctx = {"mode": 0, "K": K, "V": V}
+    o, lse = attend(q, K, V, n_heads, scale)
+    y = W_O @ o + (0.0 if b_O is None else _f64(b_O))
+    return y, q, lse, ctx
+
+
 def max_rel_err(gpu, ref, n_heads: int) -> float:
     """Normwise error per (request, head) row (reading R12):
     max_{i,h,c} |gpu - ref| / max(max_c' |ref_{i,h,c'}|, 1e-6)."""

@@ -90,6 +90,20 @@ struct AppendParams {
   int32_t n_req, d, H, dh, B;
 };
 
+// Dense projection GEMM for the current-token q/k/v map and the output map (NEXT row f1):
+// C = A W^T (+ bias), A [M, K] row-major, W [N, K] row-major.
+struct DenseParams {
+  const void* a;           // [M, K], pool dtype
+  const void* w;           // [N, K] (SIMT path; the tcgen05 path reads it through a tensor map)
+  const float* bias;       // nullable [N]
+  int32_t M, N, K;
+  int32_t epi;             // 1: project (q | head-interleaved K||V -> cache slot), 2: dense C
+  void* out;               // epi 1: q [M, d]; epi 2: C [M, N]
+  void* pool;              // epi 1: unit blocks
+  const int32_t* row_dst;  // epi 1: per row {K block, V block, slot, 0}; K block < 0 = hidden row
+  int32_t d, H, dh, B;
+};
+
 // dtype: 0 bf16, 1 fp32
 cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaStream_t s);
 cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d,
@@ -99,6 +113,10 @@ cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
                             const void* tmap_w_half, int num_sms, cudaStream_t s);
 bool recon_tc_supported(int d, int H, int dh, int B);
+bool dense_tc_supported(int d);
+// tmap_a: A with {64 x 128} boxes; tmap_w: W with {64 x 128} boxes
+cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s);
+cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s);
 bool attn_pipe_supported(int dtype, int dh, int B);
 // Fused step: reconstruction GEMM (CTA pairs, 256x512 tiles) and split-K attention warps in

@@ -44,7 +44,18 @@ struct TcArgs {
   int32_t* sync;        // zeroed per-pair progress words (stride 32 ints), nullptr = off
   int32_t sync_w;       // partner lockstep window in k-steps
   int32_t* tile_done;   // nullable: per (m-tile, n-tile) count of finished epilogue warps (8 = ready)
+  // ---- epilogue routing (EPI_* below) and dense-A mode
+  int32_t epi;          // EPI_SCRATCH (reconstruction), EPI_PROJECT (q + KV-cache write), EPI_DENSE
+  int32_t n_total;      // output columns (EPI_DENSE / EPI_PROJECT), = n_tiles * TILE_N
+  __nv_bfloat16* out;   // EPI_DENSE: [M, n_total];  EPI_PROJECT: q [M, d]
+  __nv_bfloat16* pool;  // EPI_PROJECT: unit blocks
+  const int32_t* row_dst;  // EPI_PROJECT: per row {K block, V block, slot} (K block < 0: hidden row)
 };
+
+// Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
+constexpr int EPI_SCRATCH = 0;   // [K||V] rows -> scratch blocks [hblock][H][B][dh]
+constexpr int EPI_PROJECT = 1;   // cols [0,d): q row; cols [d,3d) (head-interleaved K||V) -> cache slot
+constexpr int EPI_DENSE = 2;     // plain row-major C
 
 template <int NSUB, int NSTAGE>
 struct PairCfg {
@@ -169,8 +180,12 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
         tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
         for (int i = 0; i < nbox; ++i) {
           const int grow = mt * P_BM + (int)rank * 128 + i * a.rows_per_box;
-          const int g = grow / a.B;
-          s.prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
+          if (a.gather == nullptr) {
+            s.prow[i] = grow;   // dense A (rows past M are zero-filled by TMA and discarded)
+          } else {
+            const int g = grow / a.B;
+            s.prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
+          }
         }
         const int wrow = nt * PC::TILE_N + (int)rank * 128;
         for (int kb = 0; kb < a.k_iters; ++kb) {
@@ -264,13 +279,14 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       const int grow = mt * P_BM + row_in_tile;
       const bool valid = grow < a.M;
       const int g = grow / a.B, r = grow - g * a.B;
+      int4 dst_info = make_int4(-1, -1, 0, 0);
+      if (a.epi == EPI_PROJECT && valid) dst_info = *reinterpret_cast<const int4*>(a.row_dst + 4 * grow);
 #pragma unroll 1
       for (int c = 0; c < PC::TILE_N / 32; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, v);
         ptx::tmem_ld_wait();
         const int n = nt * PC::TILE_N + c * 32;
-        const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
         float f[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
@@ -278,8 +294,24 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] += __ldg(a.bias + n + j);
         }
-        if (valid) {
-          __nv_bfloat16* dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
+        if (!valid) continue;
+        __nv_bfloat16* dst = nullptr;
+        if (a.epi == EPI_SCRATCH) {
+          const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+          dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
+        } else if (a.epi == EPI_DENSE) {
+          dst = a.out + (size_t)grow * a.n_total + n;
+        } else {  // EPI_PROJECT
+          if (n < a.d) {
+            dst = a.out + (size_t)grow * a.d + n;
+          } else if (dst_info.x >= 0) {
+            const int m = n - a.d;
+            const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+            const int blk = kv ? dst_info.y : dst_info.x;
+            dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
+          }
+        }
+        if (dst != nullptr) {
           uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
           for (int j = 0; j < 4; ++j)

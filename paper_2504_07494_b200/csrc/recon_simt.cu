@@ -98,7 +98,83 @@ __global__ void __launch_bounds__(256) recon_simt_kernel(const ReconParams p) {
   }
 }
 
+// Dense C = A W^T (+ bias) with the projection epilogues (see DenseParams).
+template <typename T>
+__global__ void __launch_bounds__(256) dense_simt_kernel(const DenseParams p) {
+  constexpr int TM = 64, TN = 64, TK = 16;
+  __shared__ float As[TK][TM + 1];
+  __shared__ float Bs[TK][TN + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+  const int K = p.K, M = p.M, N = p.N;
+  const T* A = static_cast<const T*>(p.a);
+  const T* W = static_cast<const T*>(p.w);
+  float acc[4][4] = {};
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  const T* arow = (m0 + lr) < M ? A + (size_t)(m0 + lr) * K : nullptr;
+  const T* brow = (n0 + lr) < N ? W + (size_t)(n0 + lr) * K : nullptr;
+  for (int k0 = 0; k0 < K; k0 += TK) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = k0 + lk + j;
+      As[lk + j][lr] = (arow && k < K) ? to_f(arow[k]) : 0.f;
+      Bs[lk + j][lr] = (brow && k < K) ? to_f(brow[k]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[kk][ty * 4 + i];
+        b[i] = Bs[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  T* out = static_cast<T*>(p.out);
+  T* pool = static_cast<T*>(p.pool);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + ty * 4 + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (p.bias) v += p.bias[n];
+      if (p.epi == 2) {
+        out[(size_t)row * N + n] = from_f<T>(v);
+      } else if (n < p.d) {
+        out[(size_t)row * p.d + n] = from_f<T>(v);
+      } else {
+        const int4 di = reinterpret_cast<const int4*>(p.row_dst)[row];
+        if (di.x < 0) continue;
+        const int m = n - p.d;
+        const int h = m / (2 * p.dh), rem = m - h * 2 * p.dh, kv = rem / p.dh, c = rem - kv * p.dh;
+        const int blk = kv ? di.y : di.x;
+        pool[(size_t)blk * p.B * p.d + (size_t)h * p.B * p.dh + (size_t)di.z * p.dh + c] = from_f<T>(v);
+      }
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s) {
+  if (p.M <= 0) return cudaSuccess;
+  dim3 grid((p.M + 63) / 64, (p.N + 63) / 64);
+  if (dtype == 1)
+    dense_simt_kernel<float><<<grid, 256, 0, s>>>(p);
+  else
+    dense_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s) {
   if (p.n_hblocks <= 0) return cudaSuccess;

@@ -234,7 +234,7 @@ cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_hal
   using PC = pg::PairCfg<NSUB, NSTAGE>;
   constexpr int smem = 1024 + PC::REGION_BYTES;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
-  a.n_tiles = 2 * a.d / PC::TILE_N;
+  a.n_tiles = (a.n_total > 0 ? a.n_total : 2 * a.d) / PC::TILE_N;
   cudaError_t e = cudaFuncSetAttribute(recon_tc2_kernel<NSUB, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int tiles = a.m_tiles * a.n_tiles;
@@ -250,6 +250,30 @@ cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_hal
 static int getenv_int(const char* k) {
   const char* v = std::getenv(k);
   return v ? std::atoi(v) : 0;
+}
+
+bool dense_tc_supported(int d) { return d % 256 == 0; }
+
+cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s) {
+  if (p.M <= 0) return cudaSuccess;
+  pg::TcArgs a{};
+  a.gather = nullptr;   // dense A rows
+  a.M = p.M;
+  a.B = p.B;
+  a.rows_per_box = 128;
+  a.k_iters = p.K / BK;
+  a.H = p.H;
+  a.dh = p.dh;
+  a.d = p.d;
+  a.bias = p.bias;
+  a.group_m = -2;
+  a.epi = p.epi;
+  a.n_total = p.N;
+  a.out = static_cast<__nv_bfloat16*>(p.out);
+  a.pool = static_cast<__nv_bfloat16*>(p.pool);
+  a.row_dst = p.row_dst;
+  if (p.N % 512 == 0) return launch_pair<2, 4>(a, tmap_a, tmap_w, num_sms, s);
+  return launch_pair<1, 6>(a, tmap_a, tmap_w, num_sms, s);
 }
 
 bool recon_tc_supported(int d, int H, int dh, int B) {

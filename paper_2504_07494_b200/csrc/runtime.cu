@@ -50,7 +50,14 @@ struct Req {
 };
 
 struct Layout {  // storage layout
-  size_t blocks_off, blocks_bytes, w_off, w_bytes, b_off, b_bytes, stage_off, total;
+  size_t blocks_off, blocks_bytes;
+  size_t wq_off;          // W_Q [d,d] directly in front of W_int, so [W_Q; W_int] is one [3d,d] operand
+  size_t w_off, w_bytes;  // head-interleaved W_KV [2d,d]
+  size_t bq_off;          // b_Q [d] fp32 directly in front of b_int
+  size_t b_off, b_bytes;  // head-interleaved b_KV [2d] fp32
+  size_t wo_off, bo_off;  // W_O [d,d], b_O [d] (when configured)
+  size_t stage_off, total;
+  bool has_q, has_o;
 };
 
 bool layout_for(const hc_pool_config* c, Layout* L) {
@@ -60,13 +67,24 @@ bool layout_for(const hc_pool_config* c, Layout* L) {
   if ((int64_t)c->n_heads * c->head_dim != c->d_model) return false;
   const size_t e = c->dtype == HC_BF16 ? 2 : 4;
   const size_t d = (size_t)c->d_model;
+  L->has_q = c->w_q != nullptr;
+  L->has_o = c->w_o != nullptr;
   L->blocks_off = 0;
   L->blocks_bytes = (size_t)c->num_blocks * c->block_size * d * e;
-  L->w_off = align_up(L->blocks_off + L->blocks_bytes, 1024);
+  L->wq_off = align_up(L->blocks_off + L->blocks_bytes, 1024);
+  L->w_off = L->wq_off + (L->has_q ? d * d * e : 0);
   L->w_bytes = 2 * d * d * e;
-  L->b_off = align_up(L->w_off + L->w_bytes, kAlign);
+  L->bq_off = align_up(L->w_off + L->w_bytes, kAlign);
+  L->b_off = L->bq_off + d * sizeof(float);
   L->b_bytes = 2 * d * sizeof(float);
-  L->stage_off = align_up(L->b_off + L->b_bytes, kAlign);
+  size_t o = align_up(L->b_off + L->b_bytes, 1024);
+  L->wo_off = L->bo_off = 0;
+  if (L->has_o) {
+    L->wo_off = o;
+    L->bo_off = align_up(L->wo_off + d * d * e, kAlign);
+    o = align_up(L->bo_off + d * sizeof(float), kAlign);
+  }
+  L->stage_off = align_up(o, kAlign);
   L->total = align_up(L->stage_off + kStagingBytes, kAlign);
   return true;
 }
@@ -146,7 +164,9 @@ struct hc_pool {
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_ids;
   std::unordered_map<int64_t, Req> reqs;
   CUtensorMap tmap_x{}, tmap_w{}, tmap_w_half{};
+  CUtensorMap tmap_wqkv{}, tmap_wo{};   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
   bool tc_ok = false;
+  bool dense_tc_ok = false;             // bf16 tcgen05 path for the current-token / output GEMMs
   int num_sms = 148;
   std::array<Pinned, kRing> ring{};
   int ring_next = 0;
@@ -321,10 +341,33 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     if (err == cudaSuccess)
       err = launch_relayout_w(cfg->w_kv, p->storage + L.w_off, cfg->b_kv, reinterpret_cast<float*>(p->storage + L.b_off),
                               cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->dtype, 0);
+    const size_t dd = (size_t)cfg->d_model * cfg->d_model * e;
+    const size_t dbytes = (size_t)cfg->d_model * sizeof(float);
+    if (err == cudaSuccess && L.has_q) err = cudaMemcpy(p->storage + L.wq_off, cfg->w_q, dd, cudaMemcpyDeviceToDevice);
+    if (err == cudaSuccess)
+      err = cfg->b_q ? cudaMemcpy(p->storage + L.bq_off, cfg->b_q, dbytes, cudaMemcpyDeviceToDevice)
+                     : cudaMemset(p->storage + L.bq_off, 0, dbytes);
+    if (err == cudaSuccess && L.has_o) err = cudaMemcpy(p->storage + L.wo_off, cfg->w_o, dd, cudaMemcpyDeviceToDevice);
+    if (err == cudaSuccess && L.has_o)
+      err = cfg->b_o ? cudaMemcpy(p->storage + L.bo_off, cfg->b_o, dbytes, cudaMemcpyDeviceToDevice)
+                     : cudaMemset(p->storage + L.bo_off, 0, dbytes);
     if (err == cudaSuccess) err = cudaDeviceSynchronize();
     if (err != cudaSuccess) {
       delete p;
       return cuda_fail(err, "pool init");
+    }
+    p->dense_tc_ok = cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) && dense_tc_supported(cfg->d_model);
+    if (p->dense_tc_ok) {
+      bool ok = true;
+      if (L.has_q)
+        ok &= make_tmap_2d(&p->tmap_wqkv, p->storage + L.wq_off, (uint64_t)cfg->d_model, 3 * (uint64_t)cfg->d_model,
+                           64, 128);
+      if (L.has_o)
+        ok &= make_tmap_2d(&p->tmap_wo, p->storage + L.wo_off, (uint64_t)cfg->d_model, (uint64_t)cfg->d_model, 64, 128);
+      if (!ok) {
+        delete p;
+        return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (projection weights)");
+      }
     }
     if (cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) &&
         recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)) {
@@ -388,12 +431,68 @@ hc_status hc_free(hc_pool* pool, int64_t id, int64_t* released) {
   return HC_OK;
 }
 
-hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
-                    const int32_t* n_tokens, const void* k, const void* v, const void* x, void* stream) {
-  if (!pool) return fail(HC_E_INVALID, "pool is null");
-  pool->last_launches = 0;
-  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
-  if (n_req == 0) return HC_OK;
+// Upload the append descriptor(s) (chunked to the staging area) and launch the scatter.
+static hc_status scatter_rows(hc_pool* pool, const std::vector<AppendReq>& ar, const std::vector<int32_t>& tabs,
+                              const void* k, const void* v, const void* x, void* stream) {
+  // ---- upload descriptor(s) and scatter (chunked to the staging area) ----
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* staging = pool->storage + pool->L.stage_off;
+  size_t i0 = 0;
+  while (i0 < ar.size()) {
+    // largest prefix [i0, i1) whose descriptor fits the staging area
+    size_t i1 = i0, tab_lo = ar[i0].tab_off;
+    size_t bytes_req = 0, bytes_tab = 0;
+    int32_t rows = 0;
+    while (i1 < ar.size()) {
+      const size_t tab_hi = (i1 + 1 < ar.size()) ? ar[i1 + 1].tab_off : tabs.size();
+      const size_t nb_req = align_up((i1 - i0 + 1) * sizeof(AppendReq), 64);
+      const size_t nb_tab = (tab_hi - tab_lo) * sizeof(int32_t);
+      if (i1 > i0 && nb_req + nb_tab > kStagingBytes / 2) break;
+      bytes_req = nb_req;
+      bytes_tab = nb_tab;
+      rows = std::max(rows, ar[i1].n_tok);
+      ++i1;
+    }
+    if (bytes_req + bytes_tab > kStagingBytes / 2) return fail(HC_E_UNSUPPORTED, "append descriptor too large");
+    Pinned* pin = pool->pinned(bytes_req + bytes_tab);
+    if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+    AppendReq* hr = static_cast<AppendReq*>(pin->ptr);
+    for (size_t i = i0; i < i1; ++i) {
+      hr[i - i0] = ar[i];
+      hr[i - i0].tab_off = (int32_t)(ar[i].tab_off - tab_lo);
+    }
+    std::memcpy(static_cast<char*>(pin->ptr) + bytes_req, tabs.data() + tab_lo, bytes_tab);
+    cudaError_t err = cudaMemcpyAsync(staging, pin->ptr, bytes_req + bytes_tab, cudaMemcpyHostToDevice, s);
+    if (err != cudaSuccess) return cuda_fail(err, "append descriptor upload");
+    cudaEventRecord(pin->ev, s);
+    pin->pending = true;
+    AppendParams ap;
+    ap.reqs = reinterpret_cast<const AppendReq*>(staging);
+    ap.tabs = reinterpret_cast<const int32_t*>(staging + bytes_req);
+    ap.k = k;
+    ap.v = v;
+    ap.x = x;
+    ap.pool = pool->storage + pool->L.blocks_off;
+    ap.n_req = (int32_t)(i1 - i0);
+    ap.d = pool->cfg.d_model;
+    ap.H = pool->cfg.n_heads;
+    ap.dh = pool->cfg.head_dim;
+    ap.B = pool->cfg.block_size;
+    err = launch_append(ap, pool->cfg.dtype, rows, s);
+    if (err != cudaSuccess) return cuda_fail(err, "append kernel");
+    ++pool->last_launches;
+    i0 = i1;
+  }
+  return HC_OK;
+}
+
+// Validation + all-or-nothing allocation shared by hc_append and hc_project_append.
+// On success the requests' tables/lengths are extended and `ar`/`tabs` describe the new rows
+// (row_off = running row index per mode, in call order; one entry per request with t > 0).
+static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                                       const int32_t* n_tokens, const void* k, const void* v, const void* x,
+                                       std::vector<AppendReq>* ar, std::vector<int32_t>* tabs, int32_t* max_rows) {
   if (!req_ids || !modes || !n_tokens) return fail(HC_E_INVALID, "null id/mode/n_tokens array");
   const int B = pool->cfg.block_size;
   std::unordered_set<int64_t> seen;
@@ -419,10 +518,9 @@ hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const 
     return fail(HC_E_INVALID, "k/v or x is null while rows of that mode are appended");
 
   // ---- allocate (lowest free id first; K then V per logical block; call order) ----
-  std::vector<AppendReq> ar;
-  std::vector<int32_t> tabs;
-  ar.reserve(n_req);
-  int32_t kv_off = 0, x_off = 0, max_rows = 0;
+  ar->reserve(n_req);
+  int32_t kv_off = 0, x_off = 0;
+  *max_rows = 0;
   for (int32_t i = 0; i < n_req; ++i) {
     Req& r = pool->reqs[req_ids[i]];
     if (r.n == 0 && r.a.empty()) r.mode = modes[i];
@@ -442,71 +540,34 @@ hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const 
       q.start = (int32_t)r.n;
       q.n_tok = (int32_t)t;
       q.row_off = r.mode == HC_MODE_KV ? kv_off : x_off;
-      q.tab_off = (int32_t)tabs.size();
+      q.tab_off = (int32_t)tabs->size();
       const int64_t lb0 = r.n / B, lb1 = (r.n + t - 1) / B;
       for (int64_t lb = lb0; lb <= lb1; ++lb) {
-        tabs.push_back(r.a[lb]);
-        if (r.mode == HC_MODE_KV) tabs.push_back(r.b[lb]);
+        tabs->push_back(r.a[lb]);
+        if (r.mode == HC_MODE_KV) tabs->push_back(r.b[lb]);
       }
-      ar.push_back(q);
-      max_rows = std::max<int32_t>(max_rows, (int32_t)t);
+      ar->push_back(q);
+      *max_rows = std::max<int32_t>(*max_rows, (int32_t)t);
       (r.mode == HC_MODE_KV ? kv_off : x_off) += (int32_t)t;
     }
     r.n += t;
   }
-  if (pool->accounting || ar.empty()) return HC_OK;
-
-  // ---- upload descriptor(s) and scatter (chunked to the staging area) ----
-  DeviceGuard g(pool->cfg.device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  char* staging = pool->storage + pool->L.stage_off;
-  size_t i0 = 0;
-  while (i0 < ar.size()) {
-    // largest prefix [i0, i1) whose descriptor fits the staging area
-    size_t i1 = i0, tab_lo = ar[i0].tab_off;
-    size_t bytes_req = 0, bytes_tab = 0;
-    int32_t rows = 0;
-    while (i1 < ar.size()) {
-      const size_t tab_hi = (i1 + 1 < ar.size()) ? ar[i1 + 1].tab_off : tabs.size();
-      const size_t nb_req = align_up((i1 - i0 + 1) * sizeof(AppendReq), 64);
-      const size_t nb_tab = (tab_hi - tab_lo) * sizeof(int32_t);
-      if (i1 > i0 && nb_req + nb_tab > kStagingBytes) break;
-      bytes_req = nb_req;
-      bytes_tab = nb_tab;
-      rows = std::max(rows, ar[i1].n_tok);
-      ++i1;
-    }
-    if (bytes_req + bytes_tab > kStagingBytes) return fail(HC_E_UNSUPPORTED, "append descriptor too large");
-    Pinned* pin = pool->pinned(bytes_req + bytes_tab);
-    if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
-    AppendReq* hr = static_cast<AppendReq*>(pin->ptr);
-    for (size_t i = i0; i < i1; ++i) {
-      hr[i - i0] = ar[i];
-      hr[i - i0].tab_off = (int32_t)(ar[i].tab_off - tab_lo);
-    }
-    std::memcpy(static_cast<char*>(pin->ptr) + bytes_req, tabs.data() + tab_lo, bytes_tab);
-    cudaError_t err = cudaMemcpyAsync(staging, pin->ptr, bytes_req + bytes_tab, cudaMemcpyHostToDevice, s);
-    if (err != cudaSuccess) return cuda_fail(err, "append descriptor upload");
-    cudaEventRecord(pin->ev, s);
-    pin->pending = true;
-    AppendParams ap;
-    ap.reqs = reinterpret_cast<const AppendReq*>(staging);
-    ap.tabs = reinterpret_cast<const int32_t*>(staging + bytes_req);
-    ap.k = k;
-    ap.v = v;
-    ap.x = x;
-    ap.pool = pool->storage + pool->L.blocks_off;
-    ap.n_req = (int32_t)(i1 - i0);
-    ap.d = pool->cfg.d_model;
-    ap.H = pool->cfg.n_heads;
-    ap.dh = pool->cfg.head_dim;
-    ap.B = B;
-    err = launch_append(ap, pool->cfg.dtype, rows, s);
-    if (err != cudaSuccess) return cuda_fail(err, "append kernel");
-    ++pool->last_launches;
-    i0 = i1;
-  }
   return HC_OK;
+}
+
+hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                    const int32_t* n_tokens, const void* k, const void* v, const void* x, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req == 0) return HC_OK;
+  std::vector<AppendReq> ar;
+  std::vector<int32_t> tabs;
+  int32_t max_rows = 0;
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, n_tokens, k, v, x, &ar, &tabs, &max_rows);
+  if (st != HC_OK) return st;
+  if (pool->accounting || ar.empty()) return HC_OK;
+  return scatter_rows(pool, ar, tabs, k, v, x, stream);
 }
 
 static hc_status collect(const hc_pool* pool, int32_t n_req, const int64_t* ids, std::vector<const Req*>* rs) {
@@ -680,6 +741,171 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     pool->prof_pending.push_back(ev);
   }
   pool->last_launches = launches;
+  return HC_OK;
+}
+
+// ============================================================ attention-module steps (f1)
+static bool make_tmap_rows(CUtensorMap* m, const void* base, int rows, int d) {
+  return make_tmap_2d(m, const_cast<void*>(base), (uint64_t)d, (uint64_t)rows, 64, 128);
+}
+
+hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                            const void* x, void* q_out, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req == 0) return HC_OK;
+  if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
+  if (!pool->L.has_q) return fail(HC_E_UNSUPPORTED, "pool was created without w_q");
+  if (!x || !q_out) return fail(HC_E_INVALID, "x / q_out is null");
+  const int B = pool->cfg.block_size, d = pool->cfg.d_model;
+  std::vector<int32_t> ones(n_req, 1);
+  std::vector<AppendReq> ar;
+  std::vector<int32_t> tabs;
+  int32_t max_rows = 0;
+  // k/v rows come from the projection GEMM itself: pass x to satisfy the row-source check
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, ones.data(), x, x, x, &ar, &tabs, &max_rows);
+  if (st != HC_OK) return st;
+  // cache slot of each request's new token: KV rows are written by the GEMM epilogue,
+  // hidden rows (x itself) by the append scatter
+  std::vector<AppendReq> har;
+  std::vector<int32_t> row_dst(4 * (size_t)n_req, 0);
+  for (int32_t i = 0; i < n_req; ++i) {
+    const Req& r = pool->reqs[req_ids[i]];
+    const int64_t pos = r.n - 1, lb = pos / B;
+    if (r.mode == HC_MODE_KV) {
+      row_dst[4 * i] = r.a[lb];
+      row_dst[4 * i + 1] = r.b[lb];
+      row_dst[4 * i + 2] = (int32_t)(pos - lb * B);
+    } else {
+      row_dst[4 * i] = row_dst[4 * i + 1] = -1;
+      AppendReq q = ar[i];   // one token per request: ar[i] is request i
+      q.row_off = i;         // x row of request i
+      har.push_back(q);
+    }
+  }
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!har.empty()) {
+    st = scatter_rows(pool, har, tabs, nullptr, nullptr, x, stream);
+    if (st != HC_OK) return st;
+  }
+  const int launches = pool->last_launches;
+  const size_t rd_bytes = row_dst.size() * sizeof(int32_t);
+  if (rd_bytes > kStagingBytes / 2) return fail(HC_E_UNSUPPORTED, "batch too large for the staging area");
+  char* rd_dev = pool->storage + pool->L.stage_off + kStagingBytes / 2;
+  Pinned* pin = pool->pinned(rd_bytes);
+  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  std::memcpy(pin->ptr, row_dst.data(), rd_bytes);
+  cudaError_t err = cudaMemcpyAsync(rd_dev, pin->ptr, rd_bytes, cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) return cuda_fail(err, "projection descriptor upload");
+  cudaEventRecord(pin->ev, s);
+  pin->pending = true;
+  DenseParams dp{};
+  dp.a = x;
+  dp.w = pool->storage + pool->L.wq_off;
+  dp.bias = reinterpret_cast<const float*>(pool->storage + pool->L.bq_off);   // [b_Q | b_int] (zeros if absent)
+  dp.M = n_req;
+  dp.N = 3 * d;
+  dp.K = d;
+  dp.epi = 1;
+  dp.out = q_out;
+  dp.pool = pool->storage + pool->L.blocks_off;
+  dp.row_dst = reinterpret_cast<const int32_t*>(rd_dev);
+  dp.d = d;
+  dp.H = pool->cfg.n_heads;
+  dp.dh = pool->cfg.head_dim;
+  dp.B = B;
+  if (pool->dense_tc_ok) {
+    CUtensorMap ta;
+    if (!make_tmap_rows(&ta, x, n_req, d)) return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (x)");
+    err = launch_dense_tc(dp, &ta, &pool->tmap_wqkv, pool->num_sms, s);
+  } else {
+    err = launch_dense_simt(dp, pool->cfg.dtype, s);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "projection kernel");
+  pool->last_launches = launches + 1;
+  return HC_OK;
+}
+
+hc_status hc_output_projection(hc_pool* pool, int32_t n_req, const void* o, void* y, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req == 0) return HC_OK;
+  if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
+  if (!pool->L.has_o) return fail(HC_E_UNSUPPORTED, "pool was created without w_o");
+  if (!o || !y) return fail(HC_E_INVALID, "o / y is null");
+  const int d = pool->cfg.d_model;
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DenseParams dp{};
+  dp.a = o;
+  dp.w = pool->storage + pool->L.wo_off;
+  dp.bias = reinterpret_cast<const float*>(pool->storage + pool->L.bo_off);
+  dp.M = n_req;
+  dp.N = d;
+  dp.K = d;
+  dp.epi = 2;
+  dp.out = y;
+  dp.d = d;
+  dp.H = pool->cfg.n_heads;
+  dp.dh = pool->cfg.head_dim;
+  dp.B = pool->cfg.block_size;
+  cudaError_t err;
+  if (pool->dense_tc_ok) {
+    CUtensorMap ta;
+    if (!make_tmap_rows(&ta, o, n_req, d)) return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (o)");
+    err = launch_dense_tc(dp, &ta, &pool->tmap_wo, pool->num_sms, s);
+  } else {
+    err = launch_dense_simt(dp, pool->cfg.dtype, s);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "output projection kernel");
+  pool->last_launches = 1;
+  return HC_OK;
+}
+
+size_t hc_layer_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes) {
+  if (!pool || n_req < 0 || (n_req > 0 && (!req_ids || !modes))) {
+    g_err = "invalid arguments";
+    return 0;
+  }
+  if (n_req == 0) return kAlign;
+  std::vector<Req> tmp(n_req);
+  std::vector<const Req*> rs(n_req);
+  for (int32_t i = 0; i < n_req; ++i) {
+    auto it = pool->reqs.find(req_ids[i]);
+    tmp[i].mode = it != pool->reqs.end() ? it->second.mode : modes[i];
+    tmp[i].n = (it != pool->reqs.end() ? it->second.n : 0) + 1;
+    rs[i] = &tmp[i];
+  }
+  const size_t qa = align_up((size_t)n_req * pool->cfg.d_model * pool->elem, kAlign);
+  return 2 * qa + pool->plan(rs).total;
+}
+
+hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                          const void* x, float scale, void* y, float* lse, void* workspace, size_t ws_bytes,
+                          void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  if (n_req == 0) {
+    pool->last_launches = 0;
+    return HC_OK;
+  }
+  const size_t need = hc_layer_workspace_size(pool, n_req, req_ids, modes);
+  if (need == 0) return fail(HC_E_INVALID, "invalid arguments");
+  if (!workspace || ws_bytes < need) return fail(HC_E_WORKSPACE, "workspace smaller than hc_layer_workspace_size()");
+  if (!y) return fail(HC_E_INVALID, "y is null");
+  const size_t qa = align_up((size_t)n_req * pool->cfg.d_model * pool->elem, kAlign);
+  char* ws = static_cast<char*>(workspace);
+  hc_status st = hc_project_append(pool, n_req, req_ids, modes, x, ws, stream);
+  if (st != HC_OK) return st;
+  int launches = pool->last_launches;
+  st = hc_decode_attention(pool, n_req, req_ids, ws, scale, ws + qa, lse, ws + 2 * qa, ws_bytes - 2 * qa, stream);
+  if (st != HC_OK) return st;
+  launches += pool->last_launches;
+  st = hc_output_projection(pool, n_req, ws + qa, y, stream);
+  if (st != HC_OK) return st;
+  pool->last_launches = launches + pool->last_launches;
   return HC_OK;
 }
 

@@ -37,6 +37,7 @@ class PoolConfig(ctypes.Structure):
         ("flags", ctypes.c_int32), ("storage", ctypes.c_void_p), ("storage_bytes", ctypes.c_size_t),
         ("w_kv", ctypes.c_void_p), ("b_kv", ctypes.c_void_p), ("device", ctypes.c_int32),
         ("split_tokens", ctypes.c_int32),
+        ("w_q", ctypes.c_void_p), ("b_q", ctypes.c_void_p), ("w_o", ctypes.c_void_p), ("b_o", ctypes.c_void_p),
     ]
 
 
@@ -55,6 +56,10 @@ def _load() -> ctypes.CDLL:
         "hc_free": (I32, [P, I64, pI64]),
         "hc_workspace_size": (SZ, [P, I32, pI64]),
         "hc_decode_attention": (I32, [P, I32, pI64, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
+        "hc_project_append": (I32, [P, I32, pI64, pI32, VP, VP, VP]),
+        "hc_output_projection": (I32, [P, I32, VP, VP, VP]),
+        "hc_layer_workspace_size": (SZ, [P, I32, pI64, pI32]),
+        "hc_decode_layer": (I32, [P, I32, pI64, pI32, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
         "hc_pool_num_free": (I64, [P]),
         "hc_request_info": (I32, [P, I64, pI32, pI64, pI64]),
         "hc_request_blocks": (I32, [P, I64, I32, pI32, I64, pI64]),
@@ -139,6 +144,27 @@ def hc_decode_attention(h, req_ids, q, scale, out, lse, workspace, stream=None) 
                                    if workspace is not None else 0, _stream(stream)))
 
 
+def hc_project_append(h, req_ids, modes, x, q_out, stream=None) -> None:
+    _check(lib.hc_project_append(h, len(req_ids), _i64(req_ids), _i32(modes), _ptr(x), _ptr(q_out), _stream(stream)))
+
+
+def hc_output_projection(h, n_req, o, y, stream=None) -> None:
+    _check(lib.hc_output_projection(h, int(n_req), _ptr(o), _ptr(y), _stream(stream)))
+
+
+def hc_layer_workspace_size(h, req_ids, modes) -> int:
+    n = int(lib.hc_layer_workspace_size(h, len(req_ids), _i64(req_ids), _i32(modes)))
+    if n == 0 and len(req_ids) > 0:
+        raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
+    return n
+
+
+def hc_decode_layer(h, req_ids, modes, x, scale, y, lse, workspace, stream=None) -> None:
+    _check(lib.hc_decode_layer(h, len(req_ids), _i64(req_ids), _i32(modes), _ptr(x), float(scale), _ptr(y),
+                               _ptr(lse), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                               _stream(stream)))
+
+
 # ------------------------------------------------------------------ convenience owner
 _TORCH_DT = {HC_BF16: torch.bfloat16, HC_F32: torch.float32}
 
@@ -148,7 +174,9 @@ class HybridCachePool:
 
     def __init__(self, d_model: int, n_heads: int, head_dim: int, block_size: int, num_blocks: int,
                  dtype: int, w_kv: Optional[torch.Tensor] = None, b_kv: Optional[torch.Tensor] = None,
-                 device: int = 0, flags: int = 0, split_tokens: int = 0):
+                 device: int = 0, flags: int = 0, split_tokens: int = 0,
+                 w_q: Optional[torch.Tensor] = None, b_q: Optional[torch.Tensor] = None,
+                 w_o: Optional[torch.Tensor] = None, b_o: Optional[torch.Tensor] = None):
         self.cfg = PoolConfig(d_model, n_heads, head_dim, block_size, num_blocks, dtype, flags, None, 0,
                               None, None, device, split_tokens)
         self.dtype = dtype
@@ -157,6 +185,18 @@ class HybridCachePool:
         self.device = device
         self.storage = None
         if not flags & HC_FLAG_ACCOUNTING_ONLY:
+            # optional projection weights first: the storage layout depends on them
+            self._keep = []
+            for name, t, shape, dt in (("w_q", w_q, (d_model, d_model), self.tdtype),
+                                       ("b_q", b_q, (d_model,), torch.float32),
+                                       ("w_o", w_o, (d_model, d_model), self.tdtype),
+                                       ("b_o", b_o, (d_model,), torch.float32)):
+                if t is None:
+                    continue
+                assert t.is_cuda and t.dtype == dt and tuple(t.shape) == shape, name
+                t = t.contiguous()
+                self._keep.append(t)
+                setattr(self.cfg, name, t.data_ptr())
             nbytes = hc_pool_storage_bytes(self.cfg)
             if nbytes == 0:
                 raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
@@ -173,6 +213,7 @@ class HybridCachePool:
                 assert b_kv.is_cuda and b_kv.dtype == torch.float32 and b_kv.numel() == 2 * d_model
                 self._b_keep = b_kv.contiguous()
                 self.cfg.b_kv = self._b_keep.data_ptr()
+
         self.handle = hc_pool_create(self.cfg)
         self._ws = None
 
@@ -229,6 +270,31 @@ class HybridCachePool:
         ws = workspace if workspace is not None else self.workspace(req_ids)
         hc_decode_attention(self.handle, req_ids, q, scale, out, lse, ws, stream)
         return out, lse
+
+    # -- the rest of the attention module (f1)
+    def project_append(self, req_ids, modes, x, q_out=None, stream=None):
+        assert x.is_cuda and x.dtype == self.tdtype and x.is_contiguous() and tuple(x.shape) == (len(req_ids), self.d)
+        if q_out is None:
+            q_out = torch.empty_like(x)
+        hc_project_append(self.handle, req_ids, modes, x, q_out, stream)
+        return q_out
+
+    def output_projection(self, o, y=None, stream=None):
+        assert o.is_cuda and o.dtype == self.tdtype and o.is_contiguous() and o.shape[1] == self.d
+        if y is None:
+            y = torch.empty_like(o)
+        hc_output_projection(self.handle, o.shape[0], o, y, stream)
+        return y
+
+    def decode_layer(self, req_ids, modes, x, scale, y=None, want_lse=True, stream=None):
+        n = len(req_ids)
+        assert x.is_cuda and x.dtype == self.tdtype and x.is_contiguous() and tuple(x.shape) == (n, self.d)
+        if y is None:
+            y = torch.empty_like(x)
+        lse = torch.empty((n, self.H), dtype=torch.float32, device=x.device) if want_lse else None
+        ws = torch.empty(hc_layer_workspace_size(self.handle, req_ids, modes), dtype=torch.uint8, device=x.device)
+        hc_decode_layer(self.handle, req_ids, modes, x, scale, y, lse, ws, stream)
+        return y, lse
 
     # -- measurement hooks
     def last_launch_count(self) -> int:

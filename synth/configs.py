@@ -115,6 +115,33 @@ class Workload:
                                                  offset=r * d)
         return out
 
+    def _square(self, stream, device, rows=None):
+        d = self.shape.d
+        a, b = rows if rows is not None else (0, d)
+        return rng.normal_tensor(self.seed, stream, 0, [b - a, d], 1.0 / math.sqrt(d), self.torch_dtype, device,
+                                 offset=a * d)
+
+    def w_q(self, device="cpu", rows=None) -> torch.Tensor:
+        """W_Q [d, d] (q = W_Q x, Eq. 1), N(0, 1/d)."""
+        return self._square(rng.STREAM_WQ, device, rows)
+
+    def w_o(self, device="cpu", rows=None) -> torch.Tensor:
+        """W_O [d, d] (output map of Eq. 3), N(0, 1/d)."""
+        return self._square(rng.STREAM_WO, device, rows)
+
+    def b_q(self, device="cpu") -> Optional[torch.Tensor]:
+        return rng.normal_tensor(self.seed, rng.STREAM_B, 1, [self.shape.d], 0.02, torch.float32, device) \
+            if self.bias else None
+
+    def b_o(self, device="cpu") -> Optional[torch.Tensor]:
+        return rng.normal_tensor(self.seed, rng.STREAM_B, 2, [self.shape.d], 0.02, torch.float32, device) \
+            if self.bias else None
+
+    def x_t(self, i: int, device="cpu") -> torch.Tensor:
+        """Layer input of request i's current token (attention-layer step), N(0,1)."""
+        return rng.normal_tensor(self.seed, rng.STREAM_XT, self.req_ids[i], [self.shape.d], 1.0,
+                                 self.torch_dtype, device)
+
     def b_kv(self, device="cpu") -> Optional[torch.Tensor]:
         """Optional bias [2d] (fp32), None when disabled (Eq. 1 has no bias; SURVEY §8(c) #4)."""
         if not self.bias:

@@ -29,6 +29,9 @@ STREAM_V = 3
 STREAM_X = 4
 STREAM_W = 5
 STREAM_B = 6
+STREAM_WQ = 7
+STREAM_WO = 8
+STREAM_XT = 9   # layer input of the current (new) token
 
 _IH4_STD = 65536.0 / math.sqrt(3.0)  # std of (k1+k2+k3+k4) for k_i ~ U{0..65535}
 _IH4_MEAN = 4 * 32767.5

@@ -289,3 +289,64 @@ def test_fused_and_unfused_agree_bitwise(hc, monkeypatch):
     monkeypatch.setenv("HC_FUSED", "0")
     _, b, lb = _run(w, split_tokens=64)
     assert np.array_equal(a, b) and np.array_equal(la, lb)
+
+
+# ------------------------------------------------------------------ attention layer (NEXT row f1)
+LAYER_CASES = [
+    ("tiny-f32", None),
+    ("bf16-256", (256, 2, 128, 16)),     # 3d = 768: 256-wide pair tiles for the projection GEMM
+    ("bf16-512", (512, 4, 128, 16)),     # 3d = 1536: 512-wide pair tiles
+    ("bf16-dh64", (512, 8, 64, 32)),
+]
+
+
+@pytest.mark.parametrize("name,shape", LAYER_CASES)
+def test_decode_layer_vs_oracle(hc, name, shape):
+    """x_t -> [q,k,v = W x_t, k/v or x_t appended] -> attention -> y = W_O o (+b), against
+    oracle.attention_layer; the appended K/V (or x_t) are then re-checked by a plain
+    decode_attention over the updated cache."""
+    if shape is None:
+        w = C.tiny(bias=True)
+        tol = TOL_F32
+    else:
+        d, H, dh, B = shape
+        w = _bf16_workload(d, H, dh, B, n=[1, 2, 17, 129, 300, 33], bias=True)
+        tol = TOL_BF16
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w)
+    T.fill(pool, T.prefix_workload(w))
+    x = torch.stack([w.x_t(i, device=dev) for i in range(len(w.n))]).contiguous()
+    y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
+    torch.cuda.synchronize()
+    y, lse = y.float().cpu().numpy(), lse.cpu().numpy()
+    from oracle import hc_oracle as O
+    for i in range(len(w.n)):
+        y_ref, q_ref, l_ref, ctx = T.oracle_layer(w, i)
+        assert O.max_rel_err(y[i][None], y_ref[None], w.shape.H) <= tol, (name, i)
+        assert np.abs(lse[i] - l_ref).max() <= (1e-4 if shape is None else 5e-2)
+        assert pool.request_info(w.req_ids[i])[1] == w.n[i]
+    # the cache now holds the current token: attend again with the layer's own q
+    q = torch.stack([torch.tensor(T.oracle_layer(w, i)[1]) for i in range(len(w.n))]).to(w.torch_dtype).to(dev)
+    out, lse2 = pool.decode(w.req_ids, q.contiguous(), w.scale)
+    out = out.float().cpu().numpy()
+    for i in range(len(w.n)):
+        _, q_ref, _, ctx = T.oracle_layer(w, i)
+        qd = q.float().cpu().numpy()[i]
+        if ctx["mode"] == 1:
+            K, V = O.hidden_request_kv(ctx["X"], w.w_kv(), w.b_kv())
+        else:
+            K, V = ctx["K"], ctx["V"]
+        ref, _ = O.attend(qd, K, V, w.shape.H, w.scale)
+        assert O.max_rel_err(out[i][None], ref[None], w.shape.H) <= tol, (name, "cache", i)
+
+
+def test_project_append_errors(hc):
+    w = _bf16_workload(256, 2, 128, 16, n=[5])
+    pool = T.make_pool(w)       # created without w_q / w_o
+    x = torch.zeros((1, 256), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(hc.HcError) as e:
+        pool.project_append([0], [0], x)
+    assert e.value.status == hc.HC_E_UNSUPPORTED
+    with pytest.raises(hc.HcError) as e:
+        pool.output_projection(x)
+    assert e.value.status == hc.HC_E_UNSUPPORTED

@@ -216,3 +216,43 @@ def test_max_rel_err_definition():
 def test_zero_context_is_rejected():
     with pytest.raises(AssertionError):
         O.attend(np.zeros(4), np.zeros((0, 4)), np.zeros((0, 4)), 1, 1.0)
+
+
+# ---------------------------------------------------------------- attention layer (f1)
+def test_layer_identity_maps_reduce_to_decode():
+    """W_Q = I, W_O = I, W_KV = [I; I]: q = x_t, k_t = v_t = x_t, y = o — the layer is the
+    decode step over the cache extended by x_t (hidden) or (x_t, x_t) (KV)."""
+    d, H, n = 12, 3, 9
+    I = np.eye(d)
+    x = _rand(d, 40)
+    X = _rand((n, d), 41)
+    y, q, lse, ctx = O.attention_layer(x, {"mode": 1, "X": X}, I, np.vstack([I, I]), I, H, 0.5)
+    assert np.array_equal(q, x)
+    o, l = O.attend(x, np.vstack([X, x]), np.vstack([X, x]), H, 0.5)
+    assert np.allclose(y, o, atol=1e-14) and np.allclose(lse, l, atol=1e-14)
+    K, V = _rand((n, d), 42), _rand((n, d), 43)
+    y2, _, _, ctx2 = O.attention_layer(x, {"mode": 0, "K": K, "V": V}, I, np.vstack([I, I]), I, H, 0.5)
+    assert np.array_equal(ctx2["K"][-1], x) and np.array_equal(ctx2["V"][-1], x)
+
+
+def test_layer_hidden_equals_kv_twin_and_matches_torch():
+    """hidden(X + x_t) == KV(K, V projected from X + x_t) through the whole layer, and the
+    layer equals a torch float64 composition (linear -> SDPA -> linear)."""
+    d, H, n = 16, 2, 11
+    W_Q, W_KV, W_O = _rand((d, d), 44, 0.3), _rand((2 * d, d), 45, 0.3), _rand((d, d), 46, 0.3)
+    b_Q, b_KV, b_O = _rand(d, 47, 0.1), _rand(2 * d, 48, 0.1), _rand(d, 49, 0.1)
+    x, X = _rand(d, 50), _rand((n, d), 51)
+    yh, qh, lh, _ = O.attention_layer(x, {"mode": 1, "X": X}, W_Q, W_KV, W_O, H, 0.25, b_Q, b_KV, b_O)
+    KV = X @ W_KV.T + b_KV
+    yk, qk, lk, _ = O.attention_layer(x, {"mode": 0, "K": KV[:, :d], "V": KV[:, d:]}, W_Q, W_KV, W_O, H, 0.25,
+                                      b_Q, b_KV, b_O)
+    assert np.allclose(yh, yk, atol=1e-12) and np.allclose(lh, lk, atol=1e-12)
+    tX = torch.tensor(np.vstack([X, x]))
+    kv = torch.nn.functional.linear(tX, torch.tensor(W_KV), torch.tensor(b_KV))
+    q = torch.nn.functional.linear(torch.tensor(x), torch.tensor(W_Q), torch.tensor(b_Q))
+    dh = d // H
+    att = torch.nn.functional.scaled_dot_product_attention(
+        q.view(1, H, 1, dh), kv[:, :d].view(-1, H, dh).transpose(0, 1).unsqueeze(0),
+        kv[:, d:].view(-1, H, dh).transpose(0, 1).unsqueeze(0), scale=0.25).reshape(d)
+    y_t = torch.nn.functional.linear(att, torch.tensor(W_O), torch.tensor(b_O)).numpy()
+    assert np.allclose(yh, y_t, atol=1e-12)
