@@ -161,6 +161,52 @@ hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, 
                           const void* x, float scale, void* y, float* lse, void* workspace, size_t ws_bytes,
                           void* stream);
 
+/* ---- adaptive scheduler (host only; NEXT row f2; §4.2, §5) ---- */
+typedef struct {
+  double rho;            /* seconds of extra projection time per memory unit (Eq. 6, t = rho m) */
+  double total_units;    /* M~: pool capacity in memory units */
+  double ttft_slo;       /* seconds; a waiting request with p > ttft_slo has violated its SLO (<= 0: never) */
+  double tbt_slo;        /* seconds; a running request with p > tbt_slo has violated its SLO (<= 0: never) */
+  int32_t fallback;      /* SLO-aware fallback: 0 = near-zero constant eps, 1 = decay factor */
+  double eps;            /* near-zero value (default 1e-6 s) */
+  double decay;          /* decay factor (0.4 in §6.5) */
+  int32_t hybrid;        /* 1: hidden cache allowed; 0: KV-only ablation */
+  int32_t block_size;    /* memory unit granularity: a KV request of L tokens needs 2*ceil(L/B) units (B=1: tokens) */
+} hc_sched_config;
+
+typedef struct {
+  int64_t id;
+  int32_t running;         /* 1: in the running queue R^e (decode phase, cache resident); 0: waiting W^e */
+  int32_t has_token;       /* has received an output token (pending time since the last token) */
+  double arrival_time;     /* seconds */
+  double last_token_time;  /* seconds (used when has_token) */
+  int64_t seq_len;         /* tokens cached (running) or to prefill (waiting: prompt + generated, P:297 fn) */
+} hc_sched_request;
+
+typedef struct {
+  int32_t iter_type;       /* 0 decode, 1 prefill, -1 idle (both queues empty) */
+  int32_t n_candidates;    /* |U^e| */
+  double budget;           /* M^e (Eq. 7 right-hand side) */
+  double objective;        /* sum_i g_i alpha_i (Definition 1) */
+  double memory_used;      /* sum_i (1 - beta_i/2) m_i alpha_i */
+} hc_sched_result;
+
+/* One scheduling decision for iteration e at time `now`.  Tracks p_i and m_i
+ * (m_i = KV units of seq_len + 1, the token produced this iteration), picks the
+ * iteration type by the larger cumulative pending time (ties -> decode), the candidate set
+ * U^e and budget M^e, values g_i = p_i - beta_i (|W|+|R|) rho m_i (Eq. 5-6) with the
+ * SLO fallback applied to p_i, then the marginal-gain greedy (hidden / upgrade /
+ * direct-KV stages, refinement when p/m < 2 N rho; ties theta desc, delta-m asc, index asc)
+ * compared against the best single feasible assignment (KV or hidden; R14).
+ * alpha[i], beta[i] (n each, host) receive the decision for every input request (0 for
+ * requests outside U^e); g (nullable) receives each candidate's value at its decided beta.
+ * Pure host computation; errors: HC_E_INVALID. */
+hc_status hc_schedule(const hc_sched_config* cfg, int32_t n, const hc_sched_request* reqs, double now,
+                      int32_t* alpha, int32_t* beta, double* g, hc_sched_result* result);
+/* Least-squares slope through the origin, rho = sum m t / sum m^2 (the "approximately 30
+ * seconds" pre-serving fit of Eq. 6).  Returns -1 if n < 1 or all m are 0. */
+double hc_calibrate_rho(int32_t n, const double* m, const double* t);
+
 /* ---- introspection (host-side, no device work) ------------------------------------ */
 int64_t hc_pool_num_free(const hc_pool* pool);
 /* mode (hc_mode), cached tokens and unit blocks of a request; HC_E_UNKNOWN_REQ if absent */

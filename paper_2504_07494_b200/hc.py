@@ -41,6 +41,23 @@ class PoolConfig(ctypes.Structure):
     ]
 
 
+class SchedConfig(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_double), ("total_units", ctypes.c_double), ("ttft_slo", ctypes.c_double),
+                ("tbt_slo", ctypes.c_double), ("fallback", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("decay", ctypes.c_double), ("hybrid", ctypes.c_int32), ("block_size", ctypes.c_int32)]
+
+
+class SchedRequest(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int64), ("running", ctypes.c_int32), ("has_token", ctypes.c_int32),
+                ("arrival_time", ctypes.c_double), ("last_token_time", ctypes.c_double),
+                ("seq_len", ctypes.c_int64)]
+
+
+class SchedResult(ctypes.Structure):
+    _fields_ = [("iter_type", ctypes.c_int32), ("n_candidates", ctypes.c_int32), ("budget", ctypes.c_double),
+                ("objective", ctypes.c_double), ("memory_used", ctypes.c_double)]
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not built (run __graft_entry__.build() or "
@@ -66,6 +83,9 @@ def _load() -> ctypes.CDLL:
         "hc_last_launch_count": (I32, [P]),
         "hc_set_profiling": (I32, [P, I32]),
         "hc_kernel_times": (I32, [P, pF, pI32]),
+        "hc_schedule": (I32, [ctypes.POINTER(SchedConfig), I32, ctypes.POINTER(SchedRequest), ctypes.c_double,
+                              pI32, pI32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(SchedResult)]),
+        "hc_calibrate_rho": (ctypes.c_double, [I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "hc_last_error": (ctypes.c_char_p, []),
         "hc_version": (ctypes.c_char_p, []),
     }
@@ -163,6 +183,27 @@ def hc_decode_layer(h, req_ids, modes, x, scale, y, lse, workspace, stream=None)
     _check(lib.hc_decode_layer(h, len(req_ids), _i64(req_ids), _i32(modes), _ptr(x), float(scale), _ptr(y),
                                _ptr(lse), _ptr(workspace), workspace.numel() * workspace.element_size(),
                                _stream(stream)))
+
+
+def schedule(cfg: dict, reqs, now: float):
+    """hc_schedule: returns (alpha, beta, g, result-dict) for dict-described requests
+    (keys of SchedRequest) under dict cfg (keys of SchedConfig)."""
+    n = len(reqs)
+    c = SchedConfig(*[cfg[k] for k, _ in SchedConfig._fields_])
+    arr = (SchedRequest * max(1, n))(*[SchedRequest(*[r[k] for k, _ in SchedRequest._fields_]) for r in reqs])
+    a, b = (ctypes.c_int32 * max(1, n))(), (ctypes.c_int32 * max(1, n))()
+    g = (ctypes.c_double * max(1, n))()
+    res = SchedResult()
+    _check(lib.hc_schedule(ctypes.byref(c), n, arr, float(now), a, b, g, ctypes.byref(res)))
+    return list(a[:n]), list(b[:n]), list(g[:n]), {k: getattr(res, k) for k, _ in SchedResult._fields_}
+
+
+def calibrate_rho(m, t) -> float:
+    n = len(m)
+    r = lib.hc_calibrate_rho(n, (ctypes.c_double * max(1, n))(*m), (ctypes.c_double * max(1, n))(*t))
+    if r < 0:
+        raise HcError(HC_E_INVALID, "degenerate calibration samples")
+    return r
 
 
 # ------------------------------------------------------------------ convenience owner
