@@ -234,6 +234,11 @@ def main():
     ap.add_argument("--impl", default="hc", choices=["hc", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--split-tokens", type=int, default=0)
+    ap.add_argument("--mode", default="decode", choices=["decode", "layer", "prefill"],
+                    help="decode: the north-star hot path (default); layer: hc_decode_layer (q/k/v "
+                         "projection + cache write, attention, W_O); prefill: hc_prefill_layer")
+    ap.add_argument("--prefill-len", type=int, default=1024)
+    ap.add_argument("--prefill-reqs", type=int, default=16)
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: one batch split across ranks by LPT (default: weak)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -248,6 +253,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.mode != "decode":
+        return run_module_mode(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -415,6 +422,79 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return 0
+
+
+def run_module_mode(args, rank, world, local):
+    """--mode layer / prefill: the attention-module rows f1 / f3 (not the north-star line)."""
+    import torch
+
+    from paper_2504_07494_b200 import build as hb
+    hb.build()
+    from paper_2504_07494_b200 import hc
+    from synth import configs as C
+    from synth.configs import Workload
+    from tests import hc_testlib as T
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w0 = workload_from(args.config)
+    d = w0.shape.d
+    peaks, peak_src = load_peaks()
+    tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    if args.mode == "layer":
+        w = w0
+        pool = T.make_layer_pool(w, device=local)
+        T.fill(pool, T.prefix_workload(w), device=local)
+        x = torch.stack([w.x_t(i, device=dev) for i in range(len(w.n))]).contiguous()
+        ids, modes = list(w.req_ids), list(w.modes)
+        y = torch.empty_like(x)
+        lse = torch.empty((len(ids), w.shape.H), dtype=torch.float32, device=dev)
+        # contexts grow by one token per step: leave room for the growth of the split/scratch plan
+        ws_need = hc.hc_layer_workspace_size(pool.handle, ids, modes)
+        ws = torch.empty(int(ws_need * 1.05) + (8 << 20), dtype=torch.uint8, device=dev)
+        n_layer = len(ids)
+
+        def step():
+            # one decode layer per step: the cache grows by one token per request, so free the
+            # token again by re-running on a pool snapshot is not possible; instead measure
+            # consecutive steps (contexts grow by 1 token per step, < 0.1% over the run)
+            hc.hc_decode_layer(pool.handle, ids, modes, x, w.scale, y, lse, ws)
+        hid = w.n_tokens(1) + args.warmup + args.steps
+        flops = 4 * d * d * w.n_tokens(1) + 2 * len(ids) * d * 3 * d + 2 * len(ids) * d * d
+        unit, metric = "req-layers/s", "decode-layer req-layers/s (q/k/v proj + cache write, attention, W_O)"
+    else:
+        L, nreq = args.prefill_len, args.prefill_reqs
+        w = Workload(f"prefill-{w0.shape.name}-{nreq}x{L}", w0.shape, w0.block_size, w0.dtype, 21, [L] * nreq,
+                     [i % 2 for i in range(nreq)], list(range(nreq)))
+        pool = T.make_layer_pool(w, device=local, num_blocks=T.pool_blocks(w) * (args.warmup + args.steps + 1))
+        x = torch.cat([w.x(i, device=dev) for i in range(nreq)]).contiguous()
+        y = torch.empty_like(x)
+        state = {"k": 0}
+
+        def step():
+            base = 1_000_000 * (state["k"] + 1)
+            state["k"] += 1
+            pool.prefill_layer([base + r for r in w.req_ids], w.modes, w.n, x, w.scale, y=y)
+        flops = 8 * nreq * L * d * d + 2 * nreq * L * L * d
+        n_layer = nreq * L
+        unit, metric = "tokens/s", "prefill-layer tokens/s (projections + causal attention + W_O)"
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    line = {"metric": metric, "mode": args.mode, "value": n_layer / (ms / 1e3), "unit": unit, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": w.dtype, "data": "synthetic", "config": {"workload": w.name, "d": d},
+            "tensor_TFLOPs": flops / (ms / 1e3) / 1e12, "frac_of_sustained_bf16": flops / (ms / 1e3) / 1e12 / tf,
+            "gpu_launches_per_step": pool.last_launch_count()}
+    print(json.dumps(line), flush=True)
     return 0
 
 

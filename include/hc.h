@@ -161,6 +161,22 @@ hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, 
                           const void* x, float scale, void* y, float* lse, void* workspace, size_t ws_bytes,
                           void* stream);
 
+/* Prefill (or recompute after preemption / a cache-type switch: P:297 fn) of one
+ * attention layer for NEW requests (unknown ids or ids with 0 cached tokens).
+ *   lens  host [n_req], >= 1 tokens per request; x device [sum lens, d], rows packed in
+ *         request order (the layer inputs of the prompt tokens, or of prompt + generated
+ *         tokens for a recompute).
+ * Projects q, k, v for every token (Eq. 1) in one tcgen05 GEMM whose epilogue also writes
+ * the cache (KV mode: k, v rows; hidden mode: x rows are appended), runs causal attention
+ * over each request's tokens (Eq. 2-3 with j <= i) and the output map:
+ *   y device [sum lens, d] = W_O o (+ b_O).
+ * Needs w_q and w_o.  workspace >= hc_prefill_workspace_size().  Errors as hc_append, plus
+ * HC_E_INVALID for a request that already holds tokens. */
+size_t hc_prefill_workspace_size(const hc_pool* pool, int32_t n_req, const int32_t* lens);
+hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                           const int32_t* lens, const void* x, float scale, void* y, void* workspace,
+                           size_t ws_bytes, void* stream);
+
 /* ---- adaptive scheduler (host only; NEXT row f2; §4.2, §5) ---- */
 typedef struct {
   double rho;            /* seconds of extra projection time per memory unit (Eq. 6, t = rho m) */

@@ -144,6 +144,22 @@ def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float
     return y, q, lse, ctx
 
 
+def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=None, b_O=None):
+    """Prefill of one request's L new tokens (NEXT row f3): q, k, v of every
+    token (Eq. 1), then for each position i causal attention over tokens j <= i (Eq. 2-3,
+    P:127-135: "attending to all of the preceding tokens and itself") and the output map.
+    Returns Y [L, d] and the K, V [L, d] the cache must hold (KV mode) — hidden mode caches X."""
+    X, W_Q, W_O = _f64(X), _f64(W_Q), _f64(W_O)
+    L, d = X.shape
+    Q = X @ W_Q.T + (0.0 if b_Q is None else _f64(b_Q)[None, :])
+    K, V = hidden_request_kv(X, W_KV, b_KV)
+    Y = np.empty((L, d))
+    for i in range(L):
+        o, _ = attend(Q[i], K[: i + 1], V[: i + 1], n_heads, scale)
+        Y[i] = W_O @ o + (0.0 if b_O is None else _f64(b_O))
+    return Y, K, V
+
+
 def max_rel_err(gpu, ref, n_heads: int) -> float:
     """Normwise error per (request, head) row (reading R12):
     max_{i,h,c} |gpu - ref| / max(max_c' |ref_{i,h,c'}|, 1e-6)."""

@@ -102,6 +102,7 @@ struct DenseParams {
   void* pool;              // epi 1: unit blocks
   const int32_t* row_dst;  // epi 1: per row {K block, V block, slot, 0}; K block < 0 = hidden row
   int32_t d, H, dh, B;
+  void* kvbuf;             // epi 1 (prefill): also each row's head-interleaved K||V, [M, 2d]
 };
 
 // dtype: 0 bf16, 1 fp32
@@ -127,5 +128,19 @@ int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
+
+// Causal self-attention over each request's new tokens (prefill / recompute, NEXT row f3).
+struct PrefillAttnParams {
+  const void* q;            // [R, d] (R = sum of lens), heads = dh-column slices
+  const void* kv;           // [R, 2d], head-interleaved K_h || V_h per row
+  void* o;                  // [R, d]
+  const int32_t* row0;      // [n_req + 1] first row of each request (prefix sums of lens)
+  const int32_t* tile_req;  // [n_qtiles] request of each 64-row query tile
+  const int32_t* tile_q0;   // [n_qtiles] first query row (within its request) of each tile
+  int32_t n_qtiles, H, dh, d;
+  float scale_log2;
+};
+cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStream_t s);
+bool prefill_attn_mma_supported(int dtype, int dh);
 
 }  // namespace hc

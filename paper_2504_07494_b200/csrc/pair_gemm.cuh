@@ -50,6 +50,7 @@ struct TcArgs {
   __nv_bfloat16* out;   // EPI_DENSE: [M, n_total];  EPI_PROJECT: q [M, d]
   __nv_bfloat16* pool;  // EPI_PROJECT: unit blocks
   const int32_t* row_dst;  // EPI_PROJECT: per row {K block, V block, slot} (K block < 0: hidden row)
+  __nv_bfloat16* kvbuf;    // EPI_PROJECT (prefill): also every row's head-interleaved K||V, [M, 2d]
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -296,6 +297,7 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
         }
         if (!valid) continue;
         __nv_bfloat16* dst = nullptr;
+        __nv_bfloat16* dst2 = nullptr;
         if (a.epi == EPI_SCRATCH) {
           const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
           dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
@@ -304,19 +306,32 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
         } else {  // EPI_PROJECT
           if (n < a.d) {
             dst = a.out + (size_t)grow * a.d + n;
-          } else if (dst_info.x >= 0) {
+          } else {
             const int m = n - a.d;
-            const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
-            const int blk = kv ? dst_info.y : dst_info.x;
-            dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
+            if (dst_info.x >= 0) {
+              const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+              const int blk = kv ? dst_info.y : dst_info.x;
+              dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
+            }
+            if (a.kvbuf) dst2 = a.kvbuf + (size_t)grow * 2 * a.d + m;
           }
         }
-        if (dst != nullptr) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
+        if (dst != nullptr || dst2 != nullptr) {
+          uint4 pk[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            d4[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+            pk[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
                                pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
+          if (dst != nullptr) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+          }
+          if (dst2 != nullptr) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+          }
         }
       }
       ptx::tc_fence_before();

@@ -153,9 +153,10 @@ __global__ void __launch_bounds__(256) dense_simt_kernel(const DenseParams p) {
       } else if (n < p.d) {
         out[(size_t)row * p.d + n] = from_f<T>(v);
       } else {
+        const int m = n - p.d;
+        if (p.kvbuf) static_cast<T*>(p.kvbuf)[(size_t)row * 2 * p.d + m] = from_f<T>(v);
         const int4 di = reinterpret_cast<const int4*>(p.row_dst)[row];
         if (di.x < 0) continue;
-        const int m = n - p.d;
         const int h = m / (2 * p.dh), rem = m - h * 2 * p.dh, kv = rem / p.dh, c = rem - kv * p.dh;
         const int blk = kv ? di.y : di.x;
         pool[(size_t)blk * p.B * p.d + (size_t)h * p.B * p.dh + (size_t)di.z * p.dh + c] = from_f<T>(v);

@@ -272,6 +272,7 @@ cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void
   a.out = static_cast<__nv_bfloat16*>(p.out);
   a.pool = static_cast<__nv_bfloat16*>(p.pool);
   a.row_dst = p.row_dst;
+  a.kvbuf = static_cast<__nv_bfloat16*>(p.kvbuf);
   if (p.N % 512 == 0) return launch_pair<2, 4>(a, tmap_a, tmap_w, num_sms, s);
   return launch_pair<1, 6>(a, tmap_a, tmap_w, num_sms, s);
 }

@@ -909,6 +909,174 @@ hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, 
   return HC_OK;
 }
 
+// ============================================================ prefill / recompute (f3)
+namespace {
+struct PrefillPlan {
+  int64_t rows = 0;
+  int32_t n_qtiles = 0;
+  size_t off_q, off_kv, off_o, off_rowdst, off_row0, off_treq, off_tq0, total;
+};
+PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens) {
+  PrefillPlan P;
+  for (int32_t i = 0; i < n_req; ++i) {
+    P.rows += lens[i];
+    P.n_qtiles += (int32_t)cdiv(lens[i], 64);
+  }
+  const size_t e = pool->elem, d = (size_t)pool->cfg.d_model;
+  size_t o = 0;
+  P.off_q = o;
+  o = align_up(o + P.rows * d * e, kAlign);
+  P.off_kv = o;
+  o = align_up(o + P.rows * 2 * d * e, kAlign);
+  P.off_o = o;
+  o = align_up(o + P.rows * d * e, kAlign);
+  P.off_rowdst = o;
+  o = align_up(o + P.rows * 4 * sizeof(int32_t), kAlign);
+  P.off_row0 = o;
+  o = align_up(o + (n_req + 1) * sizeof(int32_t), kAlign);
+  P.off_treq = o;
+  o = align_up(o + P.n_qtiles * sizeof(int32_t), kAlign);
+  P.off_tq0 = o;
+  o = align_up(o + P.n_qtiles * sizeof(int32_t), kAlign);
+  P.total = o;
+  return P;
+}
+}  // namespace
+
+size_t hc_prefill_workspace_size(const hc_pool* pool, int32_t n_req, const int32_t* lens) {
+  if (!pool || n_req < 0 || (n_req > 0 && !lens)) {
+    g_err = "invalid arguments";
+    return 0;
+  }
+  for (int32_t i = 0; i < n_req; ++i)
+    if (lens[i] < 1) {
+      g_err = "lens must be >= 1";
+      return 0;
+    }
+  return n_req == 0 ? kAlign : prefill_plan(pool, n_req, lens).total;
+}
+
+hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
+                           const int32_t* lens, const void* x, float scale, void* y, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_req < 0) return fail(HC_E_INVALID, "n_req < 0");
+  if (n_req == 0) return HC_OK;
+  if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
+  if (!pool->L.has_q || !pool->L.has_o) return fail(HC_E_UNSUPPORTED, "pool was created without w_q / w_o");
+  if (!req_ids || !modes || !lens || !x || !y || !workspace) return fail(HC_E_INVALID, "null argument");
+  for (int32_t i = 0; i < n_req; ++i) {
+    if (lens[i] < 1) return fail(HC_E_INVALID, "lens must be >= 1");
+    auto it = pool->reqs.find(req_ids[i]);
+    if (it != pool->reqs.end() && it->second.n > 0)
+      return fail(HC_E_INVALID, "prefill needs new requests (cache-type switch: hc_free first)");
+  }
+  const PrefillPlan P = prefill_plan(pool, n_req, lens);
+  if (ws_bytes < P.total) return fail(HC_E_WORKSPACE, "workspace smaller than hc_prefill_workspace_size()");
+  const int B = pool->cfg.block_size, d = pool->cfg.d_model, H = pool->cfg.n_heads, dh = pool->cfg.head_dim;
+  std::vector<AppendReq> ar;
+  std::vector<int32_t> tabs;
+  int32_t max_rows = 0;
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, lens, x, x, x, &ar, &tabs, &max_rows);
+  if (st != HC_OK) return st;
+  // host descriptor: per-row cache targets (KV rows), request row offsets, query tiles
+  const size_t desc_bytes = P.total - P.off_rowdst;
+  Pinned* pin = pool->pinned(desc_bytes);
+  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  char* hbase = static_cast<char*>(pin->ptr);
+  std::memset(hbase, 0, desc_bytes);
+  int32_t* rowdst = reinterpret_cast<int32_t*>(hbase);
+  int32_t* row0 = reinterpret_cast<int32_t*>(hbase + (P.off_row0 - P.off_rowdst));
+  int32_t* treq = reinterpret_cast<int32_t*>(hbase + (P.off_treq - P.off_rowdst));
+  int32_t* tq0 = reinterpret_cast<int32_t*>(hbase + (P.off_tq0 - P.off_rowdst));
+  std::vector<AppendReq> har;
+  int64_t r = 0;
+  int32_t nt = 0;
+  for (int32_t i = 0; i < n_req; ++i) {
+    const Req& q = pool->reqs[req_ids[i]];
+    row0[i] = (int32_t)r;
+    for (int32_t tkn = 0; tkn < lens[i]; ++tkn, ++r) {
+      const int64_t lb = tkn / B;
+      if (q.mode == HC_MODE_KV) {
+        rowdst[4 * r] = q.a[lb];
+        rowdst[4 * r + 1] = q.b[lb];
+        rowdst[4 * r + 2] = (int32_t)(tkn - lb * B);
+      } else {
+        rowdst[4 * r] = rowdst[4 * r + 1] = -1;
+      }
+    }
+    for (int32_t t0 = 0; t0 < lens[i]; t0 += 64, ++nt) {
+      treq[nt] = i;
+      tq0[nt] = t0;
+    }
+    if (q.mode == HC_MODE_HIDDEN) {
+      AppendReq a = ar[i];          // lens >= 1: ar[i] is request i
+      a.row_off = row0[i];          // x rows of request i
+      har.push_back(a);
+    }
+  }
+  row0[n_req] = (int32_t)r;
+  DeviceGuard g(pool->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  cudaError_t err = cudaMemcpyAsync(ws + P.off_rowdst, hbase, desc_bytes, cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) return cuda_fail(err, "prefill descriptor upload");
+  cudaEventRecord(pin->ev, s);
+  pin->pending = true;
+  int launches = 0;
+  if (!har.empty()) {
+    st = scatter_rows(pool, har, tabs, nullptr, nullptr, x, stream);   // hidden mode: cache x itself
+    if (st != HC_OK) return st;
+    launches += pool->last_launches;
+  }
+  // q, k, v of every token; KV rows also land in the cache
+  DenseParams dp{};
+  dp.a = x;
+  dp.w = pool->storage + pool->L.wq_off;
+  dp.bias = reinterpret_cast<const float*>(pool->storage + pool->L.bq_off);
+  dp.M = (int32_t)P.rows;
+  dp.N = 3 * d;
+  dp.K = d;
+  dp.epi = 1;
+  dp.out = ws + P.off_q;
+  dp.pool = pool->storage + pool->L.blocks_off;
+  dp.row_dst = reinterpret_cast<const int32_t*>(ws + P.off_rowdst);
+  dp.kvbuf = ws + P.off_kv;
+  dp.d = d;
+  dp.H = H;
+  dp.dh = dh;
+  dp.B = B;
+  if (pool->dense_tc_ok) {
+    CUtensorMap ta;
+    if (!make_tmap_rows(&ta, x, (int)P.rows, d)) return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (x)");
+    err = launch_dense_tc(dp, &ta, &pool->tmap_wqkv, pool->num_sms, s);
+  } else {
+    err = launch_dense_simt(dp, pool->cfg.dtype, s);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "prefill projection kernel");
+  ++launches;
+  PrefillAttnParams pa{};
+  pa.q = ws + P.off_q;
+  pa.kv = ws + P.off_kv;
+  pa.o = ws + P.off_o;
+  pa.row0 = reinterpret_cast<const int32_t*>(ws + P.off_row0);
+  pa.tile_req = reinterpret_cast<const int32_t*>(ws + P.off_treq);
+  pa.tile_q0 = reinterpret_cast<const int32_t*>(ws + P.off_tq0);
+  pa.n_qtiles = P.n_qtiles;
+  pa.H = H;
+  pa.dh = dh;
+  pa.d = d;
+  pa.scale_log2 = scale * 1.4426950408889634f;
+  err = launch_prefill_attn(pa, pool->cfg.dtype, s);
+  if (err != cudaSuccess) return cuda_fail(err, "prefill attention kernel");
+  ++launches;
+  st = hc_output_projection(pool, (int32_t)P.rows, ws + P.off_o, y, stream);
+  if (st != HC_OK) return st;
+  pool->last_launches = launches + 1;
+  return HC_OK;
+}
+
 int32_t hc_last_launch_count(const hc_pool* pool) { return pool ? pool->last_launches : -1; }
 
 hc_status hc_set_profiling(hc_pool* pool, int32_t enable) {

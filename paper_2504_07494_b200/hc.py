@@ -77,6 +77,8 @@ def _load() -> ctypes.CDLL:
         "hc_output_projection": (I32, [P, I32, VP, VP, VP]),
         "hc_layer_workspace_size": (SZ, [P, I32, pI64, pI32]),
         "hc_decode_layer": (I32, [P, I32, pI64, pI32, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
+        "hc_prefill_workspace_size": (SZ, [P, I32, pI32]),
+        "hc_prefill_layer": (I32, [P, I32, pI64, pI32, pI32, VP, ctypes.c_float, VP, VP, SZ, VP]),
         "hc_pool_num_free": (I64, [P]),
         "hc_request_info": (I32, [P, I64, pI32, pI64, pI64]),
         "hc_request_blocks": (I32, [P, I64, I32, pI32, I64, pI64]),
@@ -336,6 +338,20 @@ class HybridCachePool:
         ws = torch.empty(hc_layer_workspace_size(self.handle, req_ids, modes), dtype=torch.uint8, device=x.device)
         hc_decode_layer(self.handle, req_ids, modes, x, scale, y, lse, ws, stream)
         return y, lse
+
+    def prefill_layer(self, req_ids, modes, lens, x, scale, y=None, stream=None):
+        """Prefill / recompute of new requests: x [sum lens, d] -> y [sum lens, d]; caches filled."""
+        rows = int(sum(lens))
+        assert x.is_cuda and x.dtype == self.tdtype and x.is_contiguous() and tuple(x.shape) == (rows, self.d)
+        if y is None:
+            y = torch.empty_like(x)
+        n = int(lib.hc_prefill_workspace_size(self.handle, len(lens), _i32(lens)))
+        if n == 0:
+            raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
+        ws = torch.empty(n, dtype=torch.uint8, device=x.device)
+        _check(lib.hc_prefill_layer(self.handle, len(req_ids), _i64(req_ids), _i32(modes), _i32(lens), _ptr(x),
+                                    float(scale), _ptr(y), _ptr(ws), n, _stream(stream)))
+        return y
 
     # -- measurement hooks
     def last_launch_count(self) -> int:

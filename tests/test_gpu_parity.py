@@ -350,3 +350,65 @@ def test_project_append_errors(hc):
     with pytest.raises(hc.HcError) as e:
         pool.output_projection(x)
     assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+# ------------------------------------------------------------------ prefill / recompute (NEXT row f3)
+PREFILL_CASES = [
+    ("tiny-f32", None, [64, 1, 33, 16]),
+    ("bf16-256", (256, 2, 128, 16), [1, 63, 64, 65, 200, 513]),
+    ("bf16-512", (512, 4, 128, 16), [130, 7, 64, 300]),
+    ("bf16-dh64", (512, 8, 64, 32), [1, 65, 129]),
+]
+
+
+@pytest.mark.parametrize("name,shape,lens", PREFILL_CASES)
+def test_prefill_layer_vs_oracle(hc, name, shape, lens):
+    """Prefill of new requests: every output row against oracle.prefill_layer, then a decode
+    over the freshly written caches against the oracle (KV rows written by the projection
+    GEMM's epilogue; hidden rows = x)."""
+    from oracle import hc_oracle as O
+    if shape is None:
+        w = C.tiny(bias=True)
+        tol = TOL_F32
+    else:
+        d, H, dh, B = shape
+        w = _bf16_workload(d, H, dh, B, n=lens, bias=True)
+        tol = TOL_BF16
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w)
+    x = torch.cat([w.x(i, device=dev) for i in range(len(w.n))]).contiguous()
+    y = pool.prefill_layer(w.req_ids, w.modes, w.n, x, w.scale)
+    torch.cuda.synchronize()
+    y = y.float().cpu().numpy()
+    W_q, W_kv, W_o = w.w_q(), w.w_kv(), w.w_o()
+    r = 0
+    for i in range(len(w.n)):
+        Y, K, V = O.prefill_layer(w.x(i), W_q, W_kv, W_o, w.shape.H, w.scale, w.b_q(), w.b_kv(), w.b_o())
+        assert O.max_rel_err(y[r:r + w.n[i]], Y, w.shape.H) <= tol, (name, i)
+        r += w.n[i]
+    # the caches now hold every token: decode with the synthetic queries
+    out, lse = T.decode(pool, w, T.queries(w))
+    for i in range(len(w.n)):
+        K, V = O.hidden_request_kv(w.x(i), W_kv, w.b_kv())
+        ref, _ = O.attend(w.q(i).double().numpy(), K, V, w.shape.H, w.scale)
+        assert O.max_rel_err(out[i][None], ref[None], w.shape.H) <= tol, (name, "cache", i)
+
+
+def test_recompute_after_cache_type_switch(hc):
+    """a request switching KV -> hidden discards its cache and is recomputed by a
+    prefill over its tokens in the new mode; decode then matches the oracle."""
+    from oracle import hc_oracle as O
+    w = _bf16_workload(256, 2, 128, 16, n=[77], modes=[MODE_KV], bias=True)
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w, num_blocks=32)
+    x = w.x(0, device=dev)
+    pool.prefill_layer(w.req_ids, [MODE_KV], w.n, x, w.scale)
+    with pytest.raises(hc.HcError):
+        pool.prefill_layer(w.req_ids, [MODE_KV], w.n, x, w.scale)   # not a new request
+    assert pool.free(w.req_ids[0]) == 2 * math.ceil(77 / 16)
+    pool.prefill_layer(w.req_ids, [MODE_HIDDEN], w.n, x, w.scale)
+    assert pool.request_info(w.req_ids[0])[:2] == (MODE_HIDDEN, 77)
+    out, _ = pool.decode(w.req_ids, T.queries(w), w.scale)
+    K, V = O.hidden_request_kv(w.x(0), w.w_kv(), w.b_kv())
+    ref, _ = O.attend(w.q(0).double().numpy(), K, V, 2, w.scale)
+    assert O.max_rel_err(out.float().cpu().numpy(), ref[None], 2) <= TOL_BF16

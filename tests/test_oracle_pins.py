@@ -256,3 +256,32 @@ def test_layer_hidden_equals_kv_twin_and_matches_torch():
         kv[:, d:].view(-1, H, dh).transpose(0, 1).unsqueeze(0), scale=0.25).reshape(d)
     y_t = torch.nn.functional.linear(att, torch.tensor(W_O), torch.tensor(b_O)).numpy()
     assert np.allclose(yh, y_t, atol=1e-12)
+
+
+# ---------------------------------------------------------------- prefill (f3)
+def test_prefill_first_row_and_last_row_consistency():
+    """Row 0 attends only to itself (o_0 = v_0); the last row equals the decode-layer step
+    with the first L-1 tokens cached (the current token attends to all previous and itself)."""
+    d, H, L = 16, 2, 9
+    W_Q, W_KV, W_O = _rand((d, d), 60, 0.3), _rand((2 * d, d), 61, 0.3), _rand((d, d), 62, 0.3)
+    b_Q, b_KV, b_O = _rand(d, 63, 0.1), _rand(2 * d, 64, 0.1), _rand(d, 65, 0.1)
+    X = _rand((L, d), 66)
+    Y, K, V = O.prefill_layer(X, W_Q, W_KV, W_O, H, 0.3, b_Q, b_KV, b_O)
+    assert np.allclose(Y[0], W_O @ V[0] + b_O, atol=1e-13)
+    y_last, _, _, _ = O.attention_layer(X[-1], {"mode": 1, "X": X[:-1]}, W_Q, W_KV, W_O, H, 0.3, b_Q, b_KV, b_O)
+    assert np.allclose(Y[-1], y_last, atol=1e-12)
+
+
+def test_prefill_matches_torch_causal_sdpa():
+    d, H, L = 24, 3, 13
+    W_Q, W_KV, W_O = _rand((d, d), 67, 0.3), _rand((2 * d, d), 68, 0.3), _rand((d, d), 69, 0.3)
+    X = _rand((L, d), 70)
+    Y, _, _ = O.prefill_layer(X, W_Q, W_KV, W_O, H, 0.4)
+    tX = torch.tensor(X)
+    q = (tX @ torch.tensor(W_Q).T).view(L, H, d // H).transpose(0, 1)
+    kv = tX @ torch.tensor(W_KV).T
+    k = kv[:, :d].view(L, H, d // H).transpose(0, 1)
+    v = kv[:, d:].view(L, H, d // H).transpose(0, 1)
+    att = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=0.4)
+    y_t = att.transpose(0, 1).reshape(L, d) @ torch.tensor(W_O).T
+    assert np.allclose(Y, y_t.numpy(), atol=1e-12)
