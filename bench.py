@@ -297,6 +297,7 @@ def main():
         step()
     torch.cuda.synchronize()
     launches_per_step = pool.last_launch_count()
+    decode_path = pool.last_decode_path()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -372,7 +373,7 @@ def main():
     d, s = w.shape.d, w.elem_bytes
     hbm = peaks["hbm_gbs"]
     tf_burst, tf_sus = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    fused = t_att == 0.0 and t_rec > 0.0
+    fused = decode_path == 1
     kernels = {
         ("fused_step" if fused else "recon_gemm"): {
             "ms": t_rec, "bound": "tensor", "unit": "TFLOP/s",

@@ -236,6 +236,10 @@ hc_status hc_request_blocks(const hc_pool* pool, int64_t req_id, int32_t kind, i
 /* ---- measurement hooks --------------------------------------------------------------- */
 /* Kernels launched by the last hc_decode_attention / hc_append call on this pool. */
 int32_t hc_last_launch_count(const hc_pool* pool);
+/* Kernel path of the last hc_decode_attention: 0 = reconstruction GEMM + attention kernels,
+ * 1 = fused step kernel (GEMM and attention warps in one launch), 2 = attention only (no
+ * hidden-mode request), -1 = none. */
+int32_t hc_last_decode_path(const hc_pool* pool);
 /* When enabled, hc_decode_attention records CUDA events around each of its kernels on
  * the stream it launches them on.  hc_kernel_times() synchronises on all events recorded
  * since the previous read and returns, summed over those calls, the milliseconds of

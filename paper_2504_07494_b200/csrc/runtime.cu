@@ -171,6 +171,7 @@ struct hc_pool {
   std::array<Pinned, kRing> ring{};
   int ring_next = 0;
   int32_t last_launches = 0;
+  int32_t last_path = -1;
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, 5>> prof_pending;
   std::vector<cudaEvent_t> ev_free;
@@ -696,6 +697,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.B = B;
   ap.d = pool->cfg.d_model;
   ap.scale_log2 = scale * 1.4426950408889634f;
+  pool->last_path = P.fused ? 1 : (P.n_hb > 0 ? 0 : 2);
   if (P.fused) {
     ap.kv_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_kvsplit);
     ap.hid_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_hidsplit);
@@ -1078,6 +1080,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
 }
 
 int32_t hc_last_launch_count(const hc_pool* pool) { return pool ? pool->last_launches : -1; }
+int32_t hc_last_decode_path(const hc_pool* pool) { return pool ? pool->last_path : -1; }
 
 hc_status hc_set_profiling(hc_pool* pool, int32_t enable) {
   if (!pool) return fail(HC_E_INVALID, "pool is null");

@@ -5,9 +5,11 @@ TAG=${1:-r01}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 python bench.py > $OUT/bench_cfg4.json 2> $OUT/bench_cfg4.err
 timeout 600 python bench.py --config cfg5:0.0 --no-cpu-baseline > $OUT/bench_cfg5_h0.json 2>/dev/null
-timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"recon|attn|combine" \
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"recon|attn|combine|fused" \
    --csv --log-file $OUT/launches_cfg4.csv python bench.py --profile-steps 3 > /dev/null 2>&1
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"recon_tc2" -c 1 \
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"fused_step" -c 1 \
+   -o $OUT/full_fused_cfg4 python bench.py --profile-steps 1 > /dev/null 2>&1
+HC_FUSED=0 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"recon_tc2" -c 1 \
    -o $OUT/full_recon_cfg4 python bench.py --profile-steps 1 > /dev/null 2>&1
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"attn_pipe" -c 1 \
    -o $OUT/full_attn_cfg5h0 python bench.py --config cfg5:0.0 --profile-steps 1 > /dev/null 2>&1
