@@ -82,6 +82,13 @@ typedef struct {
   const float* b_q;
   const void* w_o;
   const float* b_o;
+  /* Rotary position embedding (NEXT row f4; LLaMA/Yi-style models): 0 = none (OPT,
+   * absolute positions before layer 1).  > 0: base theta of the NeoX "rotate_half" RoPE;
+   * rebuilt K rows are rotated at their token positions in the reconstruction epilogue, and
+   * hc_project_append / hc_prefill_layer rotate q and k at the new tokens' positions.
+   * Callers of hc_decode_attention pass q already rotated.  Requires the bf16 tcgen05 path
+   * and head_dim % 64 == 0 (HC_E_UNSUPPORTED otherwise). */
+  float rope_theta;
 } hc_pool_config;
 
 /* Bytes of device storage a pool with this config needs: the unit blocks, the

@@ -43,6 +43,29 @@ def _f64(a) -> np.ndarray:
     return np.asarray(a, dtype=np.float64)
 
 
+def rope(U, positions, theta: float, n_heads: int):
+    """Rotary position embedding (NEXT row f4; the LLaMA / Yi models of §6.6), NeoX
+    "rotate_half" convention, fp64: per head u = [u1, u2] (halves of dh),
+        u' = [u1 cos(p w) - u2 sin(p w),  u2 cos(p w) + u1 sin(p w)],  w_c = theta^(-2c/dh).
+    U: [n, d] rows at token positions `positions` [n].  theta = 0 returns U unchanged."""
+    U = _f64(U)
+    if theta == 0:
+        return U
+    n, d = U.shape
+    dh = d // n_heads
+    half = dh // 2
+    w = theta ** (-2.0 * np.arange(half) / dh)
+    ang = np.asarray(positions, dtype=np.float64)[:, None] * w[None, :]
+    cs, sn = np.cos(ang), np.sin(ang)
+    out = U.copy()
+    for h in range(n_heads):
+        a = U[:, h * dh:h * dh + half]
+        b = U[:, h * dh + half:(h + 1) * dh]
+        out[:, h * dh:h * dh + half] = a * cs - b * sn
+        out[:, h * dh + half:(h + 1) * dh] = b * cs + a * sn
+    return out
+
+
 def reconstruct_kv(X, W_K, W_V, b_K=None, b_V=None):
     """Eq. 1 applied to every cached hidden state:
     K = X W_K^T (+ b_K), V = X W_V^T (+ b_V).  X: [n, d]; W_K, W_V: [d, d] with
@@ -93,14 +116,16 @@ def hidden_request_kv(X, W_KV, b_KV=None):
     return reconstruct_kv(X, W_KV[:d], W_KV[d:], bK, bV)
 
 
-def decode_batch(requests: Sequence[dict], W_KV, n_heads: int, scale: float, b_KV=None):
+def decode_batch(requests: Sequence[dict], W_KV, n_heads: int, scale: float, b_KV=None, rope_theta: float = 0.0):
     """Hybrid-cache decode step for a batch.  Each request dict has 'q' [d] and either
-    'mode' 0 with 'K', 'V' [n, d] or 'mode' 1 with 'X' [n, d].
-    Returns out [n_req, d], lse [n_req, H]."""
+    'mode' 0 with 'K', 'V' [n, d] or 'mode' 1 with 'X' [n, d].  With RoPE, rebuilt keys are
+    rotated at their token positions 0..n-1 (cached KV-mode keys are stored rotated; q is
+    given rotated).  Returns out [n_req, d], lse [n_req, H]."""
     outs, lses = [], []
     for r in requests:
         if r["mode"] == 1:
             K, V = hidden_request_kv(r["X"], W_KV, b_KV)
+            K = rope(K, np.arange(K.shape[0]), rope_theta, n_heads)
         else:
             K, V = r["K"], r["V"]
         o, l = attend(r["q"], K, V, n_heads, scale)
@@ -118,7 +143,7 @@ def head_output(q_h, X, W_K_h, W_V_h, scale: float, b_K_h=None, b_V_h=None):
 
 
 def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float,
-                    b_Q=None, b_KV=None, b_O=None):
+                    b_Q=None, b_KV=None, b_O=None, rope_theta: float = 0.0):
     """One attention layer for one decode step of one request (NEXT row f1):
     q = W_Q x_t (+b_Q) and, for the current token, k, v = W_K x_t, W_V x_t (+b)  (Eq. 1,
     P:121-125); the current token joins the context: KV mode appends (k, v) to
@@ -132,19 +157,25 @@ def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float
     q = W_Q @ x_t + (0.0 if b_Q is None else _f64(b_Q))
     if cache["mode"] == 1:
         X = np.concatenate([_f64(cache["X"]).reshape(-1, d), x_t[None, :]])
+        pos = X.shape[0] - 1
         K, V = hidden_request_kv(X, W_KV, b_KV)
+        K = rope(K, np.arange(X.shape[0]), rope_theta, n_heads)
         ctx = {"mode": 1, "X": X}
     else:
         kv = W_KV @ x_t + (0.0 if b_KV is None else _f64(b_KV))
+        pos = _f64(cache["K"]).reshape(-1, d).shape[0]
+        kv[:d] = rope(kv[None, :d], [pos], rope_theta, n_heads)[0]
         K = np.concatenate([_f64(cache["K"]).reshape(-1, d), kv[None, :d]])
         V = np.concatenate([_f64(cache["V"]).reshape(-1, d), kv[None, d:]])
         ctx = {"mode": 0, "K": K, "V": V}
+    q = rope(q[None, :], [pos], rope_theta, n_heads)[0]
     o, lse = attend(q, K, V, n_heads, scale)
     y = W_O @ o + (0.0 if b_O is None else _f64(b_O))
     return y, q, lse, ctx
 
 
-def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=None, b_O=None):
+def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=None, b_O=None,
+                  rope_theta: float = 0.0):
     """Prefill of one request's L new tokens (NEXT row f3): q, k, v of every
     token (Eq. 1), then for each position i causal attention over tokens j <= i (Eq. 2-3,
     P:127-135: "attending to all of the preceding tokens and itself") and the output map.
@@ -153,6 +184,8 @@ def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=
     L, d = X.shape
     Q = X @ W_Q.T + (0.0 if b_Q is None else _f64(b_Q)[None, :])
     K, V = hidden_request_kv(X, W_KV, b_KV)
+    Q = rope(Q, np.arange(L), rope_theta, n_heads)
+    K = rope(K, np.arange(L), rope_theta, n_heads)
     Y = np.empty((L, d))
     for i in range(L):
         o, _ = attend(Q[i], K[: i + 1], V[: i + 1], n_heads, scale)

@@ -153,6 +153,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.scr_k = static_cast<__nv_bfloat16*>(rp.scr_k);
   a.scr_v = static_cast<__nv_bfloat16*>(rp.scr_v);
   a.bias = rp.b_int;
+  a.rope_inv = rp.rope_inv;
+  a.row_pos = rp.hblk_pos;
   a.group_m = -2;
   a.l2_hint = 0;
   a.sync_w = 8;

@@ -68,6 +68,8 @@ struct ReconParams {
   void* scr_v;
   int32_t d, H, dh, B;
   int32_t* sync_counter;  // >= 32*num_sms zeroed ints (pair progress words)
+  const int32_t* hblk_pos;  // RoPE: token position of row 0 of each hidden block (nullable)
+  const double* rope_inv;   // RoPE: inv_freq table [dh/2] (nullable = no RoPE)
 };
 
 struct AppendReq {
@@ -103,6 +105,7 @@ struct DenseParams {
   const int32_t* row_dst;  // epi 1: per row {K block, V block, slot, 0}; K block < 0 = hidden row
   int32_t d, H, dh, B;
   void* kvbuf;             // epi 1 (prefill): also each row's head-interleaved K||V, [M, 2d]
+  const double* rope_inv;  // epi 1: rotate q and k at row_dst[4r+3] (nullable = no RoPE)
 };
 
 // dtype: 0 bf16, 1 fp32

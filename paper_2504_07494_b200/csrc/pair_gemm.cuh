@@ -51,6 +51,9 @@ struct TcArgs {
   __nv_bfloat16* pool;  // EPI_PROJECT: unit blocks
   const int32_t* row_dst;  // EPI_PROJECT: per row {K block, V block, slot} (K block < 0: hidden row)
   __nv_bfloat16* kvbuf;    // EPI_PROJECT (prefill): also every row's head-interleaved K||V, [M, 2d]
+  // RoPE (NEXT row f4): rotate K (and q) columns at each row's token position
+  const double* rope_inv;  // nullable: inv_freq[c] = theta^(-2c/dh), c < dh/2
+  const int32_t* row_pos;  // EPI_SCRATCH: position of row 0 of each hidden block (lb * B)
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -107,6 +110,77 @@ __device__ __forceinline__ void red_release_add(int32_t* p, int32_t v) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ---- epilogue helpers ------------------------------------------------------------------
+__device__ __forceinline__ void load_chunk(uint32_t taddr, const float* bias, int n, float (&f)[32]) {
+  uint32_t v[32];
+  ptx::tmem_ld_32x32b_x32(taddr, v);
+  ptx::tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+  if (bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] += __ldg(bias + n + j);
+  }
+}
+
+// Rotate 32 (x, y) pairs = columns (c, c + dh/2) by angle pos * inv_freq[c] (NeoX / LLaMA
+// "rotate_half" convention).  The angle is reduced modulo 2 pi in fp64 so long positions
+// keep full fp32 accuracy in the sine and cosine.
+__device__ __forceinline__ void rope_rotate(float (&x)[32], float (&y)[32], int pos, const double* inv) {
+  constexpr double kTwoPi = 6.283185307179586476925286766559;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double ang = (double)pos * __ldg(inv + j);
+    const double k = rint(ang * (1.0 / kTwoPi));
+    const float th = (float)fma(-k, kTwoPi, ang);
+    float sn, cs;
+    __sincosf(th, &sn, &cs);
+    const float x0 = x[j], y0 = y[j];
+    x[j] = x0 * cs - y0 * sn;
+    y[j] = y0 * cs + x0 * sn;
+  }
+}
+
+__device__ __forceinline__ void store_chunk(const TcArgs& a, int n, const float (&f)[32], int grow, int g, int r,
+                                            const int4& dst_info) {
+  __nv_bfloat16* dst = nullptr;
+  __nv_bfloat16* dst2 = nullptr;
+  if (a.epi == EPI_SCRATCH) {
+    const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+    dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
+  } else if (a.epi == EPI_DENSE) {
+    dst = a.out + (size_t)grow * a.n_total + n;
+  } else {  // EPI_PROJECT
+    if (n < a.d) {
+      dst = a.out + (size_t)grow * a.d + n;
+    } else {
+      const int m = n - a.d;
+      if (dst_info.x >= 0) {
+        const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
+        const int blk = kv ? dst_info.y : dst_info.x;
+        dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
+      }
+      if (a.kvbuf) dst2 = a.kvbuf + (size_t)grow * 2 * a.d + m;
+    }
+  }
+  if (dst == nullptr && dst2 == nullptr) return;
+  uint4 pk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    pk[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
+                       pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
+  if (dst != nullptr) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+  }
+  if (dst2 != nullptr) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+  }
 }
 
 struct PairSmem {
@@ -282,57 +356,33 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       const int g = grow / a.B, r = grow - g * a.B;
       int4 dst_info = make_int4(-1, -1, 0, 0);
       if (a.epi == EPI_PROJECT && valid) dst_info = *reinterpret_cast<const int4*>(a.row_dst + 4 * grow);
+      const int pos = a.rope_inv == nullptr ? 0
+                      : (a.epi == EPI_SCRATCH ? (valid ? a.row_pos[g] + r : 0) : dst_info.w);
 #pragma unroll 1
       for (int c = 0; c < PC::TILE_N / 32; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, v);
-        ptx::tmem_ld_wait();
         const int n = nt * PC::TILE_N + c * 32;
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        if (a.bias) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] += __ldg(a.bias + n + j);
+        // RoPE pairs columns (c0, c0 + dh/2) of a rotated head segment (K; and q in EPI_PROJECT)
+        int seg_c0 = -1;   // column within the rotated head segment, or -1
+        if (a.rope_inv != nullptr && a.epi != EPI_DENSE) {
+          const int m = (a.epi == EPI_PROJECT) ? n - a.d : n;
+          if (a.epi == EPI_PROJECT && n < a.d) {
+            seg_c0 = n % a.dh;                                   // q
+          } else {
+            const int rem = m % (2 * a.dh);
+            if (rem < a.dh) seg_c0 = rem;                        // K half of K_h || V_h
+          }
+        }
+        if (seg_c0 >= a.dh / 2) continue;   // written together with its partner chunk
+        float f[32], f2[32];
+        load_chunk(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, a.bias, n, f);
+        if (seg_c0 >= 0) {
+          const int half = a.dh / 2;
+          load_chunk(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32 + half, a.bias, n + half, f2);
+          rope_rotate(f, f2, pos, a.rope_inv + seg_c0);
         }
         if (!valid) continue;
-        __nv_bfloat16* dst = nullptr;
-        __nv_bfloat16* dst2 = nullptr;
-        if (a.epi == EPI_SCRATCH) {
-          const int h = n / (2 * a.dh), rem = n - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
-          dst = (kv ? a.scr_v : a.scr_k) + (((size_t)g * a.H + h) * a.B + r) * a.dh + c0;
-        } else if (a.epi == EPI_DENSE) {
-          dst = a.out + (size_t)grow * a.n_total + n;
-        } else {  // EPI_PROJECT
-          if (n < a.d) {
-            dst = a.out + (size_t)grow * a.d + n;
-          } else {
-            const int m = n - a.d;
-            if (dst_info.x >= 0) {
-              const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
-              const int blk = kv ? dst_info.y : dst_info.x;
-              dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
-            }
-            if (a.kvbuf) dst2 = a.kvbuf + (size_t)grow * 2 * a.d + m;
-          }
-        }
-        if (dst != nullptr || dst2 != nullptr) {
-          uint4 pk[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            pk[j] = make_uint4(pack_bf16(f[8 * j], f[8 * j + 1]), pack_bf16(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16(f[8 * j + 4], f[8 * j + 5]), pack_bf16(f[8 * j + 6], f[8 * j + 7]));
-          if (dst != nullptr) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) d4[j] = pk[j];
-          }
-          if (dst2 != nullptr) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst2);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) d4[j] = pk[j];
-          }
-        }
+        store_chunk(a, n, f, grow, g, r, dst_info);
+        if (seg_c0 >= 0) store_chunk(a, n + a.dh / 2, f2, grow, g, r, dst_info);
       }
       ptx::tc_fence_before();
       if (a.tile_done) __threadfence();   // this warp's rows are globally visible before the count

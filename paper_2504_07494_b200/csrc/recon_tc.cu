@@ -273,6 +273,7 @@ cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void
   a.pool = static_cast<__nv_bfloat16*>(p.pool);
   a.row_dst = p.row_dst;
   a.kvbuf = static_cast<__nv_bfloat16*>(p.kvbuf);
+  a.rope_inv = p.rope_inv;
   if (p.N % 512 == 0) return launch_pair<2, 4>(a, tmap_a, tmap_w, num_sms, s);
   return launch_pair<1, 6>(a, tmap_a, tmap_w, num_sms, s);
 }
@@ -304,6 +305,8 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   a.scr_k = static_cast<__nv_bfloat16*>(p.scr_k);
   a.scr_v = static_cast<__nv_bfloat16*>(p.scr_v);
   a.bias = p.b_int;
+  a.rope_inv = p.rope_inv;
+  a.row_pos = p.hblk_pos;
   // Default schedule: n-major raster with 2 n-tiles per group, so pairs p and p^1 of a wave
   // share one A panel and every wave shares the group's W panels; the partner lockstep
   // makes the shared A panel hit in L2 (measured: DRAM reads 190 GB -> ~60 GB at OPT-66B).
@@ -312,7 +315,7 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   const int sw = getenv_int("HC_SYNC_W");
   a.sync_w = sw != 0 ? sw : 8;
   a.sync = (a.sync_w > 0 && a.group_m == -2) ? p.sync_counter : nullptr;
-  const bool pair_mode = (p.B <= 128 || p.B % 256 == 0) && getenv_int("HC_TC_1SM") == 0;
+  const bool pair_mode = (p.B <= 128 || p.B % 256 == 0) && (getenv_int("HC_TC_1SM") == 0 || p.rope_inv);
   if (pair_mode) {
     const int nsub_env = getenv_int("HC_TC_NSUB");
     const bool can2 = (2 * p.d) % 512 == 0;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -56,6 +57,7 @@ struct Layout {  // storage layout
   size_t bq_off;          // b_Q [d] fp32 directly in front of b_int
   size_t b_off, b_bytes;  // head-interleaved b_KV [2d] fp32
   size_t wo_off, bo_off;  // W_O [d,d], b_O [d] (when configured)
+  size_t rope_off;        // RoPE inv_freq [dh/2] fp64 (when rope_theta > 0)
   size_t stage_off, total;
   bool has_q, has_o;
 };
@@ -83,6 +85,11 @@ bool layout_for(const hc_pool_config* c, Layout* L) {
     L->wo_off = o;
     L->bo_off = align_up(L->wo_off + d * d * e, kAlign);
     o = align_up(L->bo_off + d * sizeof(float), kAlign);
+  }
+  L->rope_off = 0;
+  if (c->rope_theta > 0.f) {
+    L->rope_off = o;
+    o = align_up(o + (size_t)c->head_dim / 2 * sizeof(double), kAlign);
   }
   L->stage_off = align_up(o, kAlign);
   L->total = align_up(L->stage_off + kStagingBytes, kAlign);
@@ -148,7 +155,7 @@ struct Plan {
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
   int32_t gemm_m_tiles = 0, gemm_n_tiles = 0;
   int64_t n_tab = 0;
-  size_t off_reqs, off_splits, off_tabs, off_gather, off_kvsplit, off_hidsplit, off_tiledone, desc_bytes;
+  size_t off_reqs, off_splits, off_tabs, off_gather, off_hpos, off_kvsplit, off_hidsplit, off_tiledone, desc_bytes;
   size_t off_ml, off_acc, off_sk, off_sv, total;
 };
 
@@ -270,6 +277,8 @@ struct hc_pool {
     o += sizeof(int32_t) * P.n_tab;
     P.off_gather = o = align_up(o, 64);
     o += sizeof(int32_t) * P.n_hb;
+    P.off_hpos = o = align_up(o, 64);
+    o += cfg.rope_theta > 0.f ? sizeof(int32_t) * P.n_hb : 0;
     P.off_kvsplit = o = align_up(o, 64);
     o += P.fused ? sizeof(int32_t) * P.n_kv_splits : 0;
     P.off_hidsplit = o = align_up(o, 64);
@@ -314,6 +323,12 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   if (cfg->num_blocks > INT32_MAX || (int64_t)cfg->num_blocks * cfg->block_size > INT32_MAX)
     return fail(HC_E_UNSUPPORTED, "num_blocks * block_size must fit in int32");
   const bool accounting = (cfg->flags & HC_FLAG_ACCOUNTING_ONLY) != 0;
+  if (cfg->rope_theta < 0.f) return fail(HC_E_INVALID, "rope_theta < 0");
+  if (cfg->rope_theta > 0.f &&
+      (cfg->dtype != HC_BF16 || (cfg->flags & HC_FLAG_FORCE_SIMT) || cfg->head_dim % 64 != 0 ||
+       !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size) ||
+       !dense_tc_supported(cfg->d_model) || !(cfg->block_size <= 128 || cfg->block_size % 256 == 0)))
+    return fail(HC_E_UNSUPPORTED, "RoPE needs the bf16 tcgen05 path and head_dim % 64 == 0");
   if (!accounting) {
     if (!cfg->storage || cfg->storage_bytes < L.total)
       return fail(HC_E_INVALID, "storage null or smaller than hc_pool_storage_bytes()");
@@ -352,6 +367,12 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     if (err == cudaSuccess && L.has_o)
       err = cfg->b_o ? cudaMemcpy(p->storage + L.bo_off, cfg->b_o, dbytes, cudaMemcpyDeviceToDevice)
                      : cudaMemset(p->storage + L.bo_off, 0, dbytes);
+    if (err == cudaSuccess && cfg->rope_theta > 0.f) {
+      std::vector<double> inv(cfg->head_dim / 2);
+      for (int c = 0; c < cfg->head_dim / 2; ++c)
+        inv[c] = std::pow((double)cfg->rope_theta, -2.0 * c / cfg->head_dim);
+      err = cudaMemcpy(p->storage + L.rope_off, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
     if (err == cudaSuccess) err = cudaDeviceSynchronize();
     if (err != cudaSuccess) {
       delete p;
@@ -618,6 +639,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   int32_t* tab = reinterpret_cast<int32_t*>(h + P.off_tabs);
   int32_t* gat = reinterpret_cast<int32_t*>(h + P.off_gather);
   int32_t* kvs = reinterpret_cast<int32_t*>(h + P.off_kvsplit);
+  const bool rope = pool->cfg.rope_theta > 0.f;
+  int32_t* hpos = reinterpret_cast<int32_t*>(h + P.off_hpos);
   int32_t* hds = reinterpret_cast<int32_t*>(h + P.off_hidsplit);
   int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0;
   if (P.fused) std::memset(h + P.off_tiledone, 0, P.desc_bytes - P.off_tiledone);
@@ -636,7 +659,10 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       }
     } else {
       d.scratch_blk0 = n_hb;
-      for (int32_t lb = 0; lb < nb; ++lb) gat[n_hb++] = r.a[lb];
+      for (int32_t lb = 0; lb < nb; ++lb) {
+        if (rope) hpos[n_hb] = lb * B;
+        gat[n_hb++] = r.a[lb];
+      }
     }
     for (int32_t lb = 0; lb < nb; lb += P.split_blocks) {
       SplitDesc s{};
@@ -680,6 +706,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.dh = pool->cfg.head_dim;
   rp.B = B;
   rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
+  rp.hblk_pos = rope ? reinterpret_cast<const int32_t*>(ws + P.off_hpos) : nullptr;
+  rp.rope_inv = rope ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
   AttnParams ap{};
   ap.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
   ap.splits = reinterpret_cast<const SplitDesc*>(ws + P.off_splits);
@@ -775,6 +803,7 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = pool->reqs[req_ids[i]];
     const int64_t pos = r.n - 1, lb = pos / B;
+    row_dst[4 * i + 3] = (int32_t)pos;   // RoPE position of the new token
     if (r.mode == HC_MODE_KV) {
       row_dst[4 * i] = r.a[lb];
       row_dst[4 * i + 1] = r.b[lb];
@@ -814,6 +843,7 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   dp.out = q_out;
   dp.pool = pool->storage + pool->L.blocks_off;
   dp.row_dst = reinterpret_cast<const int32_t*>(rd_dev);
+  dp.rope_inv = pool->cfg.rope_theta > 0.f ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
   dp.d = d;
   dp.H = pool->cfg.n_heads;
   dp.dh = pool->cfg.head_dim;
@@ -1000,6 +1030,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
     row0[i] = (int32_t)r;
     for (int32_t tkn = 0; tkn < lens[i]; ++tkn, ++r) {
       const int64_t lb = tkn / B;
+      rowdst[4 * r + 3] = tkn;           // RoPE position
       if (q.mode == HC_MODE_KV) {
         rowdst[4 * r] = q.a[lb];
         rowdst[4 * r + 1] = q.b[lb];
@@ -1045,6 +1076,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   dp.pool = pool->storage + pool->L.blocks_off;
   dp.row_dst = reinterpret_cast<const int32_t*>(ws + P.off_rowdst);
   dp.kvbuf = ws + P.off_kv;
+  dp.rope_inv = pool->cfg.rope_theta > 0.f ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
   dp.d = d;
   dp.H = H;
   dp.dh = dh;

@@ -38,6 +38,7 @@ class PoolConfig(ctypes.Structure):
         ("w_kv", ctypes.c_void_p), ("b_kv", ctypes.c_void_p), ("device", ctypes.c_int32),
         ("split_tokens", ctypes.c_int32),
         ("w_q", ctypes.c_void_p), ("b_q", ctypes.c_void_p), ("w_o", ctypes.c_void_p), ("b_o", ctypes.c_void_p),
+        ("rope_theta", ctypes.c_float),
     ]
 
 
@@ -220,9 +221,11 @@ class HybridCachePool:
                  dtype: int, w_kv: Optional[torch.Tensor] = None, b_kv: Optional[torch.Tensor] = None,
                  device: int = 0, flags: int = 0, split_tokens: int = 0,
                  w_q: Optional[torch.Tensor] = None, b_q: Optional[torch.Tensor] = None,
-                 w_o: Optional[torch.Tensor] = None, b_o: Optional[torch.Tensor] = None):
+                 w_o: Optional[torch.Tensor] = None, b_o: Optional[torch.Tensor] = None,
+                 rope_theta: float = 0.0):
         self.cfg = PoolConfig(d_model, n_heads, head_dim, block_size, num_blocks, dtype, flags, None, 0,
                               None, None, device, split_tokens)
+        self.cfg.rope_theta = float(rope_theta)
         self.dtype = dtype
         self.tdtype = _TORCH_DT[dtype]
         self.d, self.H, self.dh, self.B = d_model, n_heads, head_dim, block_size

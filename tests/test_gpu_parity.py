@@ -412,3 +412,56 @@ def test_recompute_after_cache_type_switch(hc):
     K, V = O.hidden_request_kv(w.x(0), w.w_kv(), w.b_kv())
     ref, _ = O.attend(w.q(0).double().numpy(), K, V, 2, w.scale)
     assert O.max_rel_err(out.float().cpu().numpy(), ref[None], 2) <= TOL_BF16
+
+
+# ------------------------------------------------------------------ RoPE (NEXT row f4)
+ROPE_THETA = 500000.0   # LLaMA-3 base
+
+
+@pytest.mark.parametrize("shape", [(512, 4, 128, 16), (512, 8, 64, 32)])
+def test_rope_decode_vs_oracle(hc, monkeypatch, shape):
+    """Rebuilt K rows rotated at their token positions in the GEMM epilogue (fused and
+    two-kernel paths), contexts up to 3000 tokens."""
+    d, H, dh, B = shape
+    w = _bf16_workload(d, H, dh, B, n=[1, 17, 300, 3000, 129, 64], bias=True)
+    for fused in ("1", "0"):
+        monkeypatch.setenv("HC_FUSED", fused)
+        pool = T.make_pool(w, rope_theta=ROPE_THETA)
+        T.fill(pool, w)
+        out, lse = T.decode(pool, w, T.queries(w))
+        err, lerr = T.compare(w, out, lse, range(len(w.n)), rope_theta=ROPE_THETA)
+        assert err <= TOL_BF16, (fused, err)
+        pool.close()
+
+
+def test_rope_layer_and_prefill_vs_oracle(hc):
+    """q and k rotated at the new tokens' positions by the projection epilogue (decode
+    layer) and at 0..L-1 (prefill)."""
+    from oracle import hc_oracle as O
+    d, H, dh, B = 512, 4, 128, 16
+    dev = torch.device("cuda", 0)
+    w = _bf16_workload(d, H, dh, B, n=[1, 40, 700, 129], bias=True)
+    pool = T.make_layer_pool(w, rope_theta=ROPE_THETA)
+    T.fill(pool, T.prefix_workload(w))
+    x = torch.stack([w.x_t(i, device=dev) for i in range(len(w.n))]).contiguous()
+    y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
+    y = y.float().cpu().numpy()
+    for i in range(len(w.n)):
+        y_ref, _, _, _ = T.oracle_layer(w, i, rope_theta=ROPE_THETA)
+        assert O.max_rel_err(y[i][None], y_ref[None], H) <= TOL_BF16, ("layer", i)
+    w2 = _bf16_workload(d, H, dh, B, n=[65, 1, 300], bias=True, seed=13)
+    pool2 = T.make_layer_pool(w2, rope_theta=ROPE_THETA)
+    xs = torch.cat([w2.x(i, device=dev) for i in range(len(w2.n))]).contiguous()
+    yp = pool2.prefill_layer(w2.req_ids, w2.modes, w2.n, xs, w2.scale).float().cpu().numpy()
+    r = 0
+    for i in range(len(w2.n)):
+        Y, _, _ = O.prefill_layer(w2.x(i), w2.w_q(), w2.w_kv(), w2.w_o(), H, w2.scale, w2.b_q(), w2.b_kv(),
+                                  w2.b_o(), ROPE_THETA)
+        assert O.max_rel_err(yp[r:r + w2.n[i]], Y, H) <= TOL_BF16, ("prefill", i)
+        r += w2.n[i]
+
+
+def test_rope_unsupported_paths(hc):
+    with pytest.raises(hc.HcError) as e:
+        T.make_pool(C.tiny(), rope_theta=10000.0)      # fp32 / SIMT path
+    assert e.value.status == hc.HC_E_UNSUPPORTED

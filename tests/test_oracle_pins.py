@@ -285,3 +285,45 @@ def test_prefill_matches_torch_causal_sdpa():
     att = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=0.4)
     y_t = att.transpose(0, 1).reshape(L, d) @ torch.tensor(W_O).T
     assert np.allclose(Y, y_t.numpy(), atol=1e-12)
+
+
+# ---------------------------------------------------------------- RoPE (f4)
+def test_rope_identity_norm_and_relative_position():
+    """Position 0 is the identity; rotations preserve per-head norms; the score of a
+    rotated pair depends only on the position difference (the defining RoPE property)."""
+    d, H, theta = 32, 2, 10000.0
+    U = _rand((5, d), 80)
+    assert np.array_equal(O.rope(U, [0] * 5, theta, H), U)
+    R = O.rope(U, [3, 17, 1000, 123456, 7], theta, H)
+    for h in range(H):
+        c = slice(h * 16, (h + 1) * 16)
+        assert np.allclose(np.linalg.norm(R[:, c], axis=1), np.linalg.norm(U[:, c], axis=1), atol=1e-12)
+    q, k = _rand((1, d), 81), _rand((1, d), 82)
+    s1 = O.rope(q, [10], theta, H) @ O.rope(k, [4], theta, H).T
+    s2 = O.rope(q, [1006], theta, H) @ O.rope(k, [1000], theta, H).T
+    assert np.allclose(s1, s2, atol=1e-10)
+
+
+def test_rope_matches_hf_rotate_half_in_torch():
+    """Library-style formula (HF LlamaRotaryEmbedding + rotate_half) in torch float64."""
+    d, H, theta, n = 24, 2, 500000.0, 9
+    dh = d // H
+    U = _rand((n, d), 83)
+    pos = torch.arange(n, dtype=torch.float64) * 37
+    inv = 1.0 / (theta ** (torch.arange(0, dh, 2, dtype=torch.float64) / dh))
+    emb = torch.cat([pos[:, None] * inv[None, :]] * 2, dim=-1)
+    u = torch.tensor(U).view(n, H, dh)
+    rot = torch.cat([-u[..., dh // 2:], u[..., :dh // 2]], dim=-1)
+    ref = (u * emb.cos()[:, None, :] + rot * emb.sin()[:, None, :]).reshape(n, d)
+    assert np.allclose(O.rope(U, pos.numpy(), theta, H), ref.numpy(), atol=1e-12)
+
+
+def test_rope_hidden_equals_rotated_kv_twin():
+    """hidden(X) with RoPE == KV twin holding rotated keys (P:269 + rotation at position j)."""
+    d, H, n, theta = 16, 2, 12, 10000.0
+    W, X, q = _rand((2 * d, d), 84, 0.3), _rand((n, d), 85), _rand(d, 86)
+    K, V = O.hidden_request_kv(X, W)
+    Kr = O.rope(K, np.arange(n), theta, H)
+    oh, lh = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.3, rope_theta=theta)
+    ok, lk = O.decode_batch([{"mode": 0, "q": q, "K": Kr, "V": V}], W, H, 0.3)
+    assert np.allclose(oh, ok, atol=1e-13) and np.allclose(lh, lk, atol=1e-13)
