@@ -241,6 +241,9 @@ def main():
     ap.add_argument("--prefill-reqs", type=int, default=16)
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: one batch split across ranks by LPT (default: weak)")
+    ap.add_argument("--absorb", action="store_true",
+                    help="NON-PAPER variant (NEXT row f4 (ii)): hidden requests attend through "
+                         "q~ = W_K^T q and W_V (sum a x) instead of rebuilding K/V")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -274,7 +277,8 @@ def main():
         w = strong_shard(w0, rank, world)
     else:
         w = C.shard_for_rank(w0, rank, world)
-    pool = T.make_pool(w, device=local, split_tokens=args.split_tokens)
+    pool = T.make_pool(w, device=local, split_tokens=args.split_tokens,
+                       flags=hc.HC_FLAG_ABSORB_HIDDEN if args.absorb else 0)
     T.fill(pool, w, device=local)
     q = T.queries(w, device=local)
     ids = list(w.req_ids)
@@ -374,6 +378,12 @@ def main():
     hbm = peaks["hbm_gbs"]
     tf_burst, tf_sus = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     fused = decode_path == 1
+    absorbed = decode_path == 3
+    if absorbed:
+        n_h = sum(1 for m in w.modes if m == 1)
+        ab_bytes = 2 * hid_tok * d * s + 2 * d * d * s + 4 * n_h * d * 2 * 2
+        B_alg = kv_tok * 2 * d * s + hid_tok * d * s + 2 * d * d * s + 2 * n_req * d * s
+        F_alg = 0
     kernels = {
         ("fused_step" if fused else "recon_gemm"): {
             "ms": t_rec, "bound": "tensor", "unit": "TFLOP/s",
@@ -385,9 +395,23 @@ def main():
         "combine": {"ms": t_comb},
         "descriptor_upload": {"ms": t_up},
     }
-    dom = ("fused_step" if fused else "recon_gemm") if t_rec >= t_att else "attention"
+    if absorbed:
+        del kernels["recon_gemm"]
+        kernels["attention"]["bytes_per_launch"] = kv_tok * 2 * d * s
+        kernels["attention"]["achieved"] = (kv_tok * 2 * d * s / (t_att / 1e3) / 1e9) if t_att > 0 else None
+        kernels["absorbed_hidden"] = {
+            "ms": t_rec, "bound": "hbm", "unit": "GB/s", "bytes_per_launch": ab_bytes,
+            "achieved": (ab_bytes / (t_rec / 1e3) / 1e9) if t_rec > 0 else None,
+            "note": "5 kernels: q~, scores, stats, Z, W_V; bytes = x read twice + W_K + W_V + q~/Z round trips"}
+        dom = "absorbed_hidden" if t_rec >= t_att else "attention"
+    else:
+        dom = ("fused_step" if fused else "recon_gemm") if t_rec >= t_att else "attention"
     k = kernels[dom]
-    if dom != "attention":
+    if dom == "absorbed_hidden":
+        roof = {"bound": "hbm", "kernel": "absorbed qt/score/stats/z/wv kernels", "achieved": k["achieved"],
+                "peak": hbm, "unit": "GB/s", "frac": k["achieved"] / hbm, "traffic": None,
+                "peak_kind": "HBM copy, " + peak_src}
+    elif dom != "attention":
         peak = tf_sus
         roof = {"bound": "tensor", "kernel": "fused_step_kernel<4,2>" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
@@ -407,7 +431,9 @@ def main():
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
-                   "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note},
+                   "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
+                   "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
+                   else "paper (hidden K/V rebuilt every step)"},
         "roofline": roof,
         "step_roofline": {"T_roof_ms": T_roof * 1e3, "frac": T_roof * 1e3 / ms, "alg_bytes": B_alg,
                           "alg_flops": F_alg, "alg_GBps": B_alg / (ms / 1e3) / 1e9,

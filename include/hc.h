@@ -56,6 +56,12 @@ typedef enum { HC_BF16 = 0, HC_F32 = 1 } hc_dtype;
                                        work; hc_decode_attention returns HC_E_UNSUPPORTED */
 #define HC_FLAG_FORCE_SIMT 0x2      /* rebuild K/V with the SIMT GEMM even in bf16 (cross-check) */
 #define HC_FLAG_GENERIC_ATTN 0x4    /* use the generic (unpipelined) attention kernel */
+#define HC_FLAG_ABSORB_HIDDEN 0x8   /* NON-PAPER variant: hidden-mode
+                                       requests attend through q~ = W_K,h^T q_h and
+                                       o_h = W_V,h (sum_j a_j x_j) + b_V,h instead of rebuilding
+                                       K/V; same Eq. 2-3 by associativity.  bf16,
+                                       no RoPE, d % 128 == 0, head_dim % 16 == 0, <= 128,
+                                       n_heads <= 128; else hc_pool_create -> HC_E_UNSUPPORTED */
 
 typedef struct hc_pool hc_pool;
 
@@ -245,7 +251,7 @@ hc_status hc_request_blocks(const hc_pool* pool, int64_t req_id, int32_t kind, i
 int32_t hc_last_launch_count(const hc_pool* pool);
 /* Kernel path of the last hc_decode_attention: 0 = reconstruction GEMM + attention kernels,
  * 1 = fused step kernel (GEMM and attention warps in one launch), 2 = attention only (no
- * hidden-mode request), -1 = none. */
+ * hidden-mode request), 3 = absorbed hidden attention (HC_FLAG_ABSORB_HIDDEN), -1 = none. */
 int32_t hc_last_decode_path(const hc_pool* pool);
 /* When enabled, hc_decode_attention records CUDA events around each of its kernels on
  * the stream it launches them on.  hc_kernel_times() synchronises on all events recorded

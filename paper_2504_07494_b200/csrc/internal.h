@@ -1,6 +1,7 @@
 // Internal types shared by the host runtime (runtime.cu) and the kernels.
 // Not part of the C ABI.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
@@ -145,5 +146,32 @@ struct PrefillAttnParams {
 };
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStream_t s);
 bool prefill_attn_mma_supported(int dtype, int dh);
+
+// Absorbed hidden-cache attention (NEXT row f4 (ii), opt-in, absorbed.cu).  Hidden request
+// r (0..n_h-1) owns gathered rows [hrow0[r], hrow0[r] + hntok[r]) (row g*B + t = slot t of
+// pool block gather[g]); its tokens are split into 64-row score tiles (tile_req, tile_t0).
+struct AbsorbParams {
+  const int32_t* gather;   // pool block id of each hidden block (request order)
+  const int32_t* hreq;     // [n_h] batch index of each hidden request
+  const int32_t* hrow0;    // [n_h] first gathered row
+  const int32_t* hntok;    // [n_h] cached tokens
+  const int32_t* tile_req; // [n_tiles]
+  const int32_t* tile_t0;  // [n_tiles]
+  const void* pool;
+  const void* q;           // [n_req, d]
+  const void* w_int;       // head-interleaved W_KV: row h*2dh + kv*dh + c
+  const float* b_int;      // nullable, same interleaving
+  __nv_bfloat16* qt;       // [n_h][H][d]   q~ = W_K,h^T q_h
+  float* s;                // [rows][Hp]    raw scores q~ . x
+  __nv_bfloat16* pm;       // [rows][Hp]    2^(scaled score - m)
+  float* ml;               // [n_h][H][3]   m (log2 domain), l, q_h . b_K,h
+  __nv_bfloat16* z;        // [n_h][H][d]   sum_j 2^(s_j - m) x_j
+  void* out;               // [n_req, d]
+  float* lse;              // nullable [n_req, H]
+  int32_t n_h, n_tiles, H, Hp, dh, d, B;
+  float scale, scale_log2;
+};
+bool absorb_supported(int dtype, int d, int dh, int H);
+cudaError_t launch_absorbed(const AbsorbParams& p, cudaStream_t s);
 
 }  // namespace hc

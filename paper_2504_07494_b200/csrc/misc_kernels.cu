@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
   if (w >= p.n_req * p.H) return;
   const int r = w / p.H, h = w - r * p.H;
   const ReqDesc rq = p.reqs[r];
+  if (rq.split_count == 0) return;   // absorbed hidden request: written by wv_kernel
   const int H = p.H, dh = p.dh;
   float M = -INFINITY;
   for (int s = lane; s < rq.split_count; s += 32)

@@ -153,10 +153,14 @@ struct Plan {
   int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1;
   int32_t n_kv_splits = 0, n_hid_splits = 0;
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
+  bool absorb = false;                // hidden requests through absorbed.cu (f4 (ii)), no splits
+  int32_t n_h = 0, n_atiles = 0, Hp = 0;
   int32_t gemm_m_tiles = 0, gemm_n_tiles = 0;
   int64_t n_tab = 0;
   size_t off_reqs, off_splits, off_tabs, off_gather, off_hpos, off_kvsplit, off_hidsplit, off_tiledone, desc_bytes;
   size_t off_ml, off_acc, off_sk, off_sv, total;
+  size_t off_hreq, off_hrow0, off_hntok, off_treq, off_tt0;   // absorb descriptor
+  size_t off_qt, off_s, off_pm, off_abml, off_z;              // absorb workspace
 };
 
 }  // namespace
@@ -248,21 +252,29 @@ struct hc_pool {
     const int B = cfg.block_size, H = cfg.n_heads, dh = cfg.head_dim;
     P.n_req = (int32_t)rs.size();
     P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
+    P.absorb = (cfg.flags & HC_FLAG_ABSORB_HIDDEN) != 0;
     for (auto* r : rs) {
       const int64_t nb = cdiv(r->n, B);
       const int32_t ns = (int32_t)cdiv(nb, P.split_blocks);
-      P.n_splits += ns;
       if (r->mode == HC_MODE_KV) {
+        P.n_splits += ns;
         P.n_tab += 2 * nb;
         P.n_kv_splits += ns;
       } else {
         P.n_hb += (int32_t)nb;
-        P.n_hid_splits += ns;
+        if (P.absorb) {
+          ++P.n_h;
+          P.n_atiles += (int32_t)cdiv(r->n, 64);
+        } else {
+          P.n_splits += ns;
+          P.n_hid_splits += ns;
+        }
       }
     }
+    P.Hp = (int32_t)align_up((size_t)H, 16);
     const char* fe = std::getenv("HC_FUSED");
     const int fused_env = fe ? std::atoi(fe) : -1;
-    P.fused = tc_ok && P.n_hb > 0 && fused_env != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
+    P.fused = !P.absorb && tc_ok && P.n_hb > 0 && fused_env != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
               fused_supported(cfg.d_model, cfg.n_heads, cfg.head_dim, B);
     if (P.fused) {
       P.gemm_m_tiles = (int32_t)cdiv((int64_t)P.n_hb * B, fused_tile_m());
@@ -285,14 +297,38 @@ struct hc_pool {
     o += P.fused ? sizeof(int32_t) * P.n_hid_splits : 0;
     P.off_tiledone = o = align_up(o, 64);
     o += P.fused ? sizeof(int32_t) * (size_t)P.gemm_m_tiles * P.gemm_n_tiles : 0;
+    P.off_hreq = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_h;
+    P.off_hrow0 = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_h;
+    P.off_hntok = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_h;
+    P.off_treq = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_atiles;
+    P.off_tt0 = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_atiles;
     P.desc_bytes = align_up(o, kAlign);
     const size_t n_tasks = (size_t)P.n_splits * H;
     P.off_ml = P.desc_bytes;
     P.off_acc = align_up(P.off_ml + n_tasks * 2 * sizeof(float), kAlign);
-    const size_t scr = (size_t)P.n_hb * H * B * dh * elem;
+    const size_t scr = P.absorb ? 0 : (size_t)P.n_hb * H * B * dh * elem;
     P.off_sk = align_up(P.off_acc + n_tasks * dh * sizeof(float), 1024);
     P.off_sv = align_up(P.off_sk + scr, 1024);
-    P.total = align_up(P.off_sv + scr, kAlign);
+    size_t e = align_up(P.off_sv + scr, kAlign);
+    if (P.absorb) {
+      const size_t rows = (size_t)P.n_hb * B, d = cfg.d_model;
+      P.off_qt = e;
+      e = align_up(e + (size_t)P.n_h * H * d * 2, kAlign);
+      P.off_s = e;
+      e = align_up(e + rows * P.Hp * sizeof(float), kAlign);
+      P.off_pm = e;
+      e = align_up(e + rows * P.Hp * 2, kAlign);
+      P.off_abml = e;
+      e = align_up(e + (size_t)P.n_h * H * 3 * sizeof(float), kAlign);
+      P.off_z = e;
+      e = align_up(e + (size_t)P.n_h * H * d * 2, kAlign);
+    }
+    P.total = e;
     return P;
   }
 };
@@ -329,6 +365,11 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
        !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size) ||
        !dense_tc_supported(cfg->d_model) || !(cfg->block_size <= 128 || cfg->block_size % 256 == 0)))
     return fail(HC_E_UNSUPPORTED, "RoPE needs the bf16 tcgen05 path and head_dim % 64 == 0");
+  if ((cfg->flags & HC_FLAG_ABSORB_HIDDEN) &&
+      (cfg->rope_theta > 0.f || !absorb_supported(cfg->dtype, cfg->d_model, cfg->head_dim, cfg->n_heads)))
+    return fail(HC_E_UNSUPPORTED,
+                "HC_FLAG_ABSORB_HIDDEN needs bf16, no RoPE, d % 128 == 0, head_dim % 16 == 0, head_dim <= 128, "
+                "n_heads <= 128");
   if (!accounting) {
     if (!cfg->storage || cfg->storage_bytes < L.total)
       return fail(HC_E_INVALID, "storage null or smaller than hc_pool_storage_bytes()");
@@ -642,7 +683,12 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   const bool rope = pool->cfg.rope_theta > 0.f;
   int32_t* hpos = reinterpret_cast<int32_t*>(h + P.off_hpos);
   int32_t* hds = reinterpret_cast<int32_t*>(h + P.off_hidsplit);
-  int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0;
+  int32_t* ahreq = reinterpret_cast<int32_t*>(h + P.off_hreq);
+  int32_t* ahrow0 = reinterpret_cast<int32_t*>(h + P.off_hrow0);
+  int32_t* ahntok = reinterpret_cast<int32_t*>(h + P.off_hntok);
+  int32_t* atreq = reinterpret_cast<int32_t*>(h + P.off_treq);
+  int32_t* att0 = reinterpret_cast<int32_t*>(h + P.off_tt0);
+  int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0, n_ah = 0, n_at = 0;
   if (P.fused) std::memset(h + P.off_tiledone, 0, P.desc_bytes - P.off_tiledone);
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = *rs[i];
@@ -659,12 +705,23 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       }
     } else {
       d.scratch_blk0 = n_hb;
+      if (P.absorb) {
+        ahreq[n_ah] = i;
+        ahrow0[n_ah] = n_hb * B;
+        ahntok[n_ah] = (int32_t)r.n;
+        for (int32_t t0 = 0; t0 < r.n; t0 += 64) {
+          atreq[n_at] = n_ah;
+          att0[n_at++] = t0;
+        }
+        ++n_ah;
+      }
       for (int32_t lb = 0; lb < nb; ++lb) {
         if (rope) hpos[n_hb] = lb * B;
         gat[n_hb++] = r.a[lb];
       }
     }
-    for (int32_t lb = 0; lb < nb; lb += P.split_blocks) {
+    const bool absorbed = P.absorb && r.mode == HC_MODE_HIDDEN;
+    for (int32_t lb = 0; lb < nb && !absorbed; lb += P.split_blocks) {
       SplitDesc s{};
       s.req = i;
       s.lb0 = lb;
@@ -725,8 +782,49 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.B = B;
   ap.d = pool->cfg.d_model;
   ap.scale_log2 = scale * 1.4426950408889634f;
-  pool->last_path = P.fused ? 1 : (P.n_hb > 0 ? 0 : 2);
-  if (P.fused) {
+  pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
+  if (P.absorb) {
+    // f4 (ii): hidden requests never rebuild K/V; KV requests take the split-K path
+    if (P.n_h > 0) {
+      AbsorbParams bp{};
+      bp.gather = rp.gather;
+      bp.hreq = reinterpret_cast<const int32_t*>(ws + P.off_hreq);
+      bp.hrow0 = reinterpret_cast<const int32_t*>(ws + P.off_hrow0);
+      bp.hntok = reinterpret_cast<const int32_t*>(ws + P.off_hntok);
+      bp.tile_req = reinterpret_cast<const int32_t*>(ws + P.off_treq);
+      bp.tile_t0 = reinterpret_cast<const int32_t*>(ws + P.off_tt0);
+      bp.pool = blocks;
+      bp.q = q;
+      bp.w_int = rp.w_int;
+      bp.b_int = rp.b_int;
+      bp.qt = reinterpret_cast<__nv_bfloat16*>(ws + P.off_qt);
+      bp.s = reinterpret_cast<float*>(ws + P.off_s);
+      bp.pm = reinterpret_cast<__nv_bfloat16*>(ws + P.off_pm);
+      bp.ml = reinterpret_cast<float*>(ws + P.off_abml);
+      bp.z = reinterpret_cast<__nv_bfloat16*>(ws + P.off_z);
+      bp.out = out;
+      bp.lse = lse;
+      bp.n_h = P.n_h;
+      bp.n_tiles = P.n_atiles;
+      bp.H = H;
+      bp.Hp = P.Hp;
+      bp.dh = pool->cfg.head_dim;
+      bp.d = pool->cfg.d_model;
+      bp.B = B;
+      bp.scale = scale;
+      bp.scale_log2 = ap.scale_log2;
+      err = launch_absorbed(bp, s);
+      if (err != cudaSuccess) return cuda_fail(err, "absorbed hidden attention");
+      launches += 5;
+    }
+    if (pool->profiling) cudaEventRecord(ev[2], s);
+    if (P.n_splits > 0) {
+      err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
+      if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
+      ++launches;
+    }
+    if (pool->profiling) cudaEventRecord(ev[3], s);
+  } else if (P.fused) {
     ap.kv_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_kvsplit);
     ap.hid_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_hidsplit);
     ap.n_kv_tasks = P.n_kv_splits * H;

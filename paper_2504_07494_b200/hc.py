@@ -21,7 +21,7 @@ STATUS_NAMES = {0: "HC_OK", 1: "HC_E_INVALID", 2: "HC_E_OOM", 3: "HC_E_UNKNOWN_R
                 4: "HC_E_MODE_MISMATCH", 5: "HC_E_CUDA", 6: "HC_E_UNSUPPORTED", 7: "HC_E_WORKSPACE"}
 HC_MODE_KV, HC_MODE_HIDDEN = 0, 1
 HC_BF16, HC_F32 = 0, 1
-HC_FLAG_ACCOUNTING_ONLY, HC_FLAG_FORCE_SIMT, HC_FLAG_GENERIC_ATTN = 1, 2, 4
+HC_FLAG_ACCOUNTING_ONLY, HC_FLAG_FORCE_SIMT, HC_FLAG_GENERIC_ATTN, HC_FLAG_ABSORB_HIDDEN = 1, 2, 4, 8
 
 
 class HcError(RuntimeError):

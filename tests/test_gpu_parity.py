@@ -465,3 +465,89 @@ def test_rope_unsupported_paths(hc):
     with pytest.raises(hc.HcError) as e:
         T.make_pool(C.tiny(), rope_theta=10000.0)      # fp32 / SIMT path
     assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+# ------------------------------------------------------------------ absorbed hidden attention (NEXT row f4 (ii))
+ABSORB_SHAPES = [
+    (256, 2, 128, 16),
+    (512, 8, 64, 32),
+    (384, 3, 128, 8),
+    (256, 2, 128, 256),
+    (1152, 9, 128, 16),     # H = 9: score/Z tiles padded to 16 heads
+    (4608, 72, 64, 16),     # OPT-66B head count (Hp = 80: two 64-column halves of P)
+]
+
+
+@pytest.mark.parametrize("d,H,dh,B", ABSORB_SHAPES)
+def test_absorbed_mixed_batch_vs_oracle(hc, d, H, dh, B):
+    """HC_FLAG_ABSORB_HIDDEN: hidden requests through q~ = W_K^T q and W_V (sum a x), KV
+    requests through split-K attention; same oracle (Eq. 1-3), same bf16 bar."""
+    w = _bf16_workload(d, H, dh, B, bias=True)
+    pool, out, lse = _run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    assert pool.last_decode_path() == 3
+    assert pool.last_launch_count() == 7      # q~, scores, stats, Z, W_V, attention, combine
+    err, lerr = T.compare(w, out, lse, range(len(w.n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= 5e-2, lerr
+
+
+def test_absorbed_hidden_only_and_kv_only(hc):
+    n = [700, 1, 333, 1025, 64, 65, 4000]
+    w = _bf16_workload(512, 4, 128, 16, n=n, modes=[MODE_HIDDEN] * len(n), bias=True)
+    pool, out, lse = _run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    assert pool.last_launch_count() == 6      # no KV request: no attention kernel
+    assert T.compare(w, out, lse, range(len(n)))[0] <= TOL_BF16
+    w = _bf16_workload(512, 4, 128, 16, n=n, modes=[MODE_KV] * len(n), bias=True)
+    pool, out, lse = _run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    assert pool.last_decode_path() == 2
+    assert T.compare(w, out, lse, range(len(n)))[0] <= TOL_BF16
+
+
+def test_absorbed_matches_reconstruction_path(hc):
+    """Both hidden-mode paths approximate the same fp64 result; they agree with each other
+    within twice the bar and the KV rows are bit-identical (same kernels)."""
+    w = _bf16_workload(512, 4, 128, 16, bias=True)
+    _, a, la = _run(w, split_tokens=64)
+    _, b, lb = _run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN, split_tokens=64)
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    assert np.array_equal(a[kv], b[kv]) and np.array_equal(la[kv], lb[kv])
+    from oracle import hc_oracle as O
+    assert O.max_rel_err(a, b, 4) <= 2 * TOL_BF16
+
+
+def test_absorbed_opt66b_sampled(hc):
+    """cfg4 (OPT-66B, 256 requests, 50% hidden) in the bench's absorbed configuration."""
+    w = C.by_name("cfg4")
+    pool = T.make_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    T.fill(pool, w)
+    out, lse = T.decode(pool, w, T.queries(w))
+    assert np.isfinite(out).all()
+    idx = _sample(w)
+    heads = {i: [0, w.shape.H // 2, w.shape.H - 1] for i in idx if w.modes[i] == MODE_HIDDEN}
+    err, lerr = T.compare(w, out[idx], lse[idx], idx, heads)
+    assert err <= TOL_BF16, err
+    assert lerr <= 5e-2, lerr
+
+
+def test_absorbed_decode_layer(hc):
+    """hc_decode_layer on an absorbed pool: projection, append, absorbed attention, W_O."""
+    from oracle import hc_oracle as O
+    d, H, dh, B = 512, 4, 128, 16
+    dev = torch.device("cuda", 0)
+    w = _bf16_workload(d, H, dh, B, n=[1, 40, 700, 129, 2, 3000], bias=True)
+    pool = T.make_layer_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    T.fill(pool, T.prefix_workload(w))
+    x = torch.stack([w.x_t(i, device=dev) for i in range(len(w.n))]).contiguous()
+    y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
+    y = y.float().cpu().numpy()
+    for i in range(len(w.n)):
+        y_ref, _, _, _ = T.oracle_layer(w, i)
+        assert O.max_rel_err(y[i][None], y_ref[None], H) <= TOL_BF16, i
+
+
+def test_absorbed_unsupported_configs(hc):
+    for kw in ({"rope_theta": 10000.0}, {}):
+        w = C.tiny() if not kw else _bf16_workload(512, 4, 128, 16)
+        with pytest.raises(hc.HcError) as e:
+            T.make_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN, **kw)   # RoPE / fp32
+        assert e.value.status == hc.HC_E_UNSUPPORTED
