@@ -402,7 +402,7 @@ def main():
         kernels["absorbed_hidden"] = {
             "ms": t_rec, "bound": "hbm", "unit": "GB/s", "bytes_per_launch": ab_bytes,
             "achieved": (ab_bytes / (t_rec / 1e3) / 1e9) if t_rec > 0 else None,
-            "note": "5 kernels: q~, scores, stats, Z, W_V; bytes = x read twice + W_K + W_V + q~/Z round trips"}
+            "note": "5 kernels: q~ (warp MMA), scores (tcgen05), P rescale, Z (tcgen05), W_V (warp MMA); bytes = x read twice + W_K + W_V + q~/Z round trips"}
         dom = "absorbed_hidden" if t_rec >= t_att else "attention"
     else:
         dom = ("fused_step" if fused else "recon_gemm") if t_rec >= t_att else "attention"

@@ -7,17 +7,21 @@
 //                                              cancels in the softmax and only shifts lse)
 //     z_h  = sum_j a_j x_j,   o_h = W_V,h z_h + b_V,h       (sum_j a_j = 1)
 // so a hidden token costs two reads of x (4d bytes, like the K and V rows of a KV token)
-// plus O(d H) FLOPs, and the per-call work is two weight reads (W_K, W_V) — the path is
-// HBM-bound instead of tensor-bound.  Five kernels, all bf16 in / fp32 accumulate on
-// warp-level MMA (mma.sync.m16n8k16 + ldmatrix; the contractions are memory-bound):
-//   K1 qt_kernel     q~[r][h][:]  = W_K,h^T q_{r,h}            (per head: [n_h x dh][dh x d])
-//   K2 score_kernel  S[row][h]    = x_row . q~[r(row)][h]       (gathered hidden rows x H)
-//   K3 stats_kernel  per (r,h): m, l over the request's tokens; P[row][h] = 2^(s - m) (bf16)
-//   K4 z_kernel      Z[r][h][:]   = sum_rows P[row][h] x_row     (per request: [H x n][n x d])
-//   K5 wv_kernel     out[r][h*dh:] = W_V,h Z[r][h] / l + b_V,h;  lse
+// plus 4 Hp d FLOPs, and the per-call work is two weight reads (W_K, W_V) — the path is
+// HBM-bound instead of tensor-bound.  Five kernels, bf16 in / fp32 accumulate:
+//   K1 qt_kernel       q~[r][h][:] = W_K,h^T q_{r,h} (per head [n_h x dh][dh x d], warp MMA);
+//                      q_h . b_K,h
+//   K2 score_tc_kernel per 128-token tile of request r (tcgen05): s = x . q~[r][h]; tile max
+//                      m_t[h], P[row][h] = 2^(scaled s - m_t) (bf16), l_t[h] = sum P
+//   K3 rescale_kernel  m[h] = max_t m_t, P *= 2^(m_t - m), l = sum_t 2^(m_t - m) l_t
+//   K4 z_tc_kernel     Z[r][h][:] = sum_rows P[row][h] x_row (tcgen05, MN-major operands)
+//   K5 wv_kernel       out[r][h*dh:] = W_V,h Z[r][h] / l + b_V,h;  lse (warp MMA)
+// x is read exactly twice (K2, K4), straight from the pool blocks through TMA.
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace hc {
 namespace {
@@ -71,7 +75,14 @@ __global__ void __launch_bounds__(128) qt_kernel(const AbsorbParams p) {
   __shared__ __align__(128) uint8_t sB[128 * 256];     // dh rows x 128 cols bf16, as 2 x 64-wide halves
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n0 = blockIdx.x * 128, h = blockIdx.y, r0 = blockIdx.z * 64;
-  const int dh = p.dh, d = p.d;
+  const int dh = p.dh, d = p.d, Hp = p.Hp;
+  if (h >= p.H) {   // padding heads of q~ (rows H..Hp-1 of each request) are zero
+    for (int i = threadIdx.x; i < 64 * 16; i += 128) {
+      const int rr = r0 + (i >> 4);
+      if (rr < p.n_h) reinterpret_cast<uint4*>(p.qt + ((size_t)rr * Hp + h) * d + n0)[i & 15] = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
   const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.q);
   const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w_int);
   // A: rows r0.., columns [h*dh, h*dh+dh) of q; half k of 64 columns each
@@ -109,234 +120,355 @@ __global__ void __launch_bounds__(128) qt_kernel(const AbsorbParams p) {
       mma(acc[2 * nj + 1], a0, a1, a2, a3, b2, b3);
     }
   }
+  if (blockIdx.x == 0 && tid < 64 && r0 + tid < p.n_h) {   // c = q_h . b_K,h (shifts lse only)
+    float c = 0.f;
+    if (p.b_int) {
+      const __nv_bfloat16* qr = q + (size_t)p.hreq[r0 + tid] * d + h * dh;
+      for (int e = 0; e < dh; ++e) c += __bfloat162float(qr[e]) * p.b_int[h * 2 * dh + e];
+    }
+    p.ml[3 * ((size_t)(r0 + tid) * p.H + h) + 2] = c;
+  }
   const int g = lane >> 2, t4 = lane & 3;
   __nv_bfloat16* qt = p.qt;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int col = n0 + j * 8 + 2 * t4;
     const int ra = r0 + warp * 16 + g, rb = ra + 8;
-    if (ra < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)ra * p.H + h) * d + col) = pk(acc[j][0], acc[j][1]);
-    if (rb < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)rb * p.H + h) * d + col) = pk(acc[j][2], acc[j][3]);
+    if (ra < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)ra * Hp + h) * d + col) = pk(acc[j][0], acc[j][1]);
+    if (rb < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)rb * Hp + h) * d + col) = pk(acc[j][2], acc[j][3]);
   }
 }
 
-// ------------------------------------------------------------------ K2: S = X q~^T
-// CTA: 64 gathered rows of ONE hidden request x Hp (<= 128) heads, K loop over d in 64s.
-// A = X rows (gathered from pool blocks), B = q~[r] [Hp x d] (rows = heads, K contiguous).
-__global__ void __launch_bounds__(128) score_kernel(const AbsorbParams p) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  constexpr int ST = 2;
-  uint8_t* sA = sm;                       // ST x [64 x 64]
-  uint8_t* sB = sm + ST * 64 * 128;       // ST x [Hp x 64]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r = p.tile_req[blockIdx.x], t0 = p.tile_t0[blockIdx.x];
-  const int Hp = p.Hp, d = p.d, B = p.B, H = p.H;
-  const int row_base = p.hrow0[r];        // first gathered row of request r
-  const int ntok = p.hntok[r];
-  const __nv_bfloat16* pool = static_cast<const __nv_bfloat16*>(p.pool);
-  const __nv_bfloat16* qt = p.qt + (size_t)r * H * d;
-  auto load = [&](int kc, int buf) {
-    uint8_t* a = sA + buf * 64 * 128;
-    uint8_t* b = sB + buf * Hp * 128;
-    for (int i = tid; i < 64 * 8; i += 128) {
-      const int row = i >> 3, c = i & 7;
-      const int t = min(t0 + row, ntok - 1);
-      const int grow = row_base + t, g = grow / B;
-      cp16(a + sw64(row, c), pool + ((size_t)p.gather[g] * B + (grow - g * B)) * d + kc * 64 + c * 8);
+// ------------------------------------------------------------------ K2: scores on tcgen05
+// CTA: one 128-token tile of one hidden request.  S[128 x Hp] = X_tile q~[r]^T with
+// tcgen05.mma M=128 N=Hp K=16 (both operands K-major SWIZZLE_128B, A = the request's pool
+// blocks as TMA boxes — no gather copy — B = q~[r] rows), fp32 accumulators in TMEM.
+// Warp 0: TMA producer; warp 1: TMEM allocator + MMA issuer; warps 2-5: epilogue (thread =
+// token row): scaled scores -> smem (column-major), per-head tile max m_t and l_t =
+// sum 2^(s - m_t) by column scans, P = 2^(s - m_t) bf16 rows (0 for the padding slots of
+// the request's last block).
+constexpr int SC_ST = 3, SC_STAGE = 32768;   // 16 KiB A + <= 16 KiB B per stage
+constexpr int Z_ST = 3, Z_STAGE = 32768;     // 16 KiB P^T + 16 KiB X per stage
+constexpr int TC_THREADS = 192;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  const uint32_t a = ptx::smem_u32(p);
+  return p + ((1024 - (a & 1023)) & 1023);
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// UMMA descriptor, MN-major operand in the canonical SWIZZLE_128B layout: 128-B rows hold
+// 64 consecutive M/N elements of one k; 8 rows (8 k) form a 1024-B swizzle atom; atoms
+// stack along K at SBO = 1024 B; 64-element M/N chunks are LBO bytes apart.
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 2)
+    score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_qt,
+                    const AbsorbParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SC_ST * SC_STAGE);
+  uint64_t* empty = full + SC_ST;
+  uint64_t* tfull = empty + SC_ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* m_s = reinterpret_cast<float*>(tmem_slot + 4);   // [128]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, r = p.tile_req[tile], t0 = p.tile_t0[tile];
+  const int ntok = p.hntok[r], row_base = p.hrow0[r], Hp = p.Hp, B = p.B;
+  const int KC = p.d / 64;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_x);
+    ptx::prefetch_tmap(&tmap_qt);
+    for (int s = 0; s < SC_ST; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
     }
-    for (int i = tid; i < Hp * 8; i += 128) {
-      const int hh = i >> 3, c = i & 7;
-      cp16_zfill(b + sw64(hh, c), qt + (size_t)min(hh, H - 1) * d + kc * 64 + c * 8, hh < H);
-    }
-  };
-  const int NT = Hp / 8;   // n-tiles of 8 heads
-  float acc[16][4];
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<128>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      const int rpb = p.rpb, nbox = 128 / rpb;
+      int prow[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const int KC = d / 64;
-  load(0, 0);
-  cp_commit();
-  const int mat = lane >> 3, rr = lane & 7;
-  for (int kc = 0; kc < KC; ++kc) {
-    if (kc + 1 < KC) load(kc + 1, (kc + 1) & 1);
-    cp_commit();
-    cp_wait<1>();
-    __syncthreads();
-    const uint32_t a_s = saddr(sA + (kc & 1) * 64 * 128), b_s = saddr(sB + (kc & 1) * Hp * 128);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      uint32_t a0, a1, a2, a3;
-      ldsm4(a_s + sw64(warp * 16 + ((mat & 1) << 3) + rr, 2 * ks + (mat >> 1)), a0, a1, a2, a3);
-#pragma unroll
-      for (int nj = 0; nj < 8; ++nj) {
-        if (2 * nj < NT) {
-          uint32_t b0, b1, b2, b3;
-          ldsm4(b_s + sw64(nj * 16 + ((mat >> 1) << 3) + rr, 2 * ks + (mat & 1)), b0, b1, b2, b3);
-          mma(acc[2 * nj], a0, a1, a2, a3, b0, b1);
-          if (2 * nj + 1 < NT) mma(acc[2 * nj + 1], a0, a1, a2, a3, b2, b3);
+      for (int i = 0; i < 16; ++i) {
+        prow[i] = 0;
+        if (i < nbox) {
+          const int grow = row_base + t0 + i * rpb, g = grow / B;
+          if (g < p.n_hb) prow[i] = p.gather[g] * B + (grow - g * B);
+        }
+      }
+      const uint32_t bytes = 128 * 128 + Hp * 128;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        uint8_t* a = smem + stage * SC_STAGE;
+        for (int i = 0; i < nbox; ++i) ptx::tma_load_2d(a + i * rpb * 128, &tmap_x, kc * 64, prow[i], &full[stage]);
+        ptx::tma_load_2d(a + 16384, &tmap_qt, kc * 64, r * Hp, &full[stage]);
+        if (++stage == SC_ST) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
-    __syncthreads();
-  }
-  const int g = lane >> 2, t4 = lane & 3;
-  const int ta = t0 + warp * 16 + g, tb = ta + 8;
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16_f32(128, Hp);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t a = ptx::smem_u32(smem + stage * SC_STAGE), b = a + 16384;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j >= NT) break;
-    const int col = j * 8 + 2 * t4;
-    if (ta < ntok) *reinterpret_cast<float2*>(p.s + (size_t)(row_base + ta) * Hp + col) = make_float2(acc[j][0], acc[j][1]);
-    if (tb < ntok) *reinterpret_cast<float2*>(p.s + (size_t)(row_base + tb) * Hp + col) = make_float2(acc[j][2], acc[j][3]);
+        for (int k = 0; k < 4; ++k)
+          ptx::umma_f16_ss(tmem, ptx::umma_desc_k_sw128(a + k * 32), ptx::umma_desc_k_sw128(b + k * 32), idesc,
+                           (kc | k) != 0 ? 1u : 0u);
+        ptx::umma_commit(&empty[stage]);
+        if (++stage == SC_ST) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::umma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: thread = token row of the tile (TMEM lane quadrant = warp & 3)
+    const int q = warp & 3, row = q * 32 + lane;
+    const int nvalid = min(128, ntok - t0);
+    const int padded = (ntok + B - 1) / B * B;
+    const bool valid = row < nvalid, keep = t0 + row < padded;
+    ptx::mbar_wait(tfull, 0);
+    ptx::tc_fence_after();
+    float* S = reinterpret_cast<float*>(smem);   // [Hp][129] column-major (all MMAs retired)
+    const float sl = p.scale_log2;
+    for (int c = 0; c < Hp; c += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c + j < Hp) S[(c + j) * 129 + row] = __uint_as_float(v[j]) * sl;
+    }
+    epi_bar();
+    const int h = row;   // column scan: thread h owns head h
+    if (h < Hp) {
+      const float* col = S + h * 129;
+      float m = -INFINITY;
+      for (int i = 0; i < nvalid; ++i) m = fmaxf(m, col[i]);
+      float l = 0.f;
+      for (int i = 0; i < nvalid; ++i) l += exp2f(col[i] - m);
+      m_s[h] = m;
+      p.tml[2 * ((size_t)tile * Hp + h)] = m;
+      p.tml[2 * ((size_t)tile * Hp + h) + 1] = l;
+    }
+    epi_bar();
+    if (keep) {
+      uint4* dst = reinterpret_cast<uint4*>(p.pm + (size_t)(row_base + t0 + row) * Hp);
+      for (int c8 = 0; c8 < Hp / 8; ++c8) {
+        float e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = valid ? exp2f(S[(c8 * 8 + j) * 129 + row] - m_s[c8 * 8 + j]) : 0.f;
+        dst[c8] = make_uint4(pk(e[0], e[1]), pk(e[2], e[3]), pk(e[4], e[5]), pk(e[6], e[7]));
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<128>(tmem);
+}
+
+// ------------------------------------------------------------------ K3: request max, P rescale
+// CTA per 128-token tile: m = max over the request's tiles, P *= 2^(m_t - m); the request's
+// first tile also publishes m and l = sum_t 2^(m_t - m) l_t.
+__global__ void __launch_bounds__(128) rescale_kernel(const AbsorbParams p) {
+  __shared__ float f_s[128];
+  const int tid = threadIdx.x, tile = blockIdx.x;
+  const int r = p.tile_req[tile], t0 = p.tile_t0[tile], ntok = p.hntok[r], tile0 = p.htile0[r];
+  const int Hp = p.Hp, H = p.H, B = p.B;
+  const int nt = (ntok + 127) / 128;
+  if (tid < Hp) {
+    float m = -INFINITY;
+    for (int k = 0; k < nt; ++k) m = fmaxf(m, p.tml[2 * ((size_t)(tile0 + k) * Hp + tid)]);
+    f_s[tid] = exp2f(p.tml[2 * ((size_t)tile * Hp + tid)] - m);
+    if (tile == tile0 && tid < H) {
+      float l = 0.f;
+      for (int k = 0; k < nt; ++k) {
+        const float* t = p.tml + 2 * ((size_t)(tile0 + k) * Hp + tid);
+        l += exp2f(t[0] - m) * t[1];
+      }
+      p.ml[3 * ((size_t)r * H + tid)] = m;
+      p.ml[3 * ((size_t)r * H + tid) + 1] = l;
+    }
+  }
+  __syncthreads();
+  const int padded = (ntok + B - 1) / B * B;
+  const int nrows = min(128, padded - t0), c8n = Hp / 8;
+  uint4* P = reinterpret_cast<uint4*>(p.pm + (size_t)(p.hrow0[r] + t0) * Hp);
+  for (int i = tid; i < nrows * c8n; i += 128) {
+    const int c8 = i % c8n;
+    uint4 v = P[i];
+    __nv_bfloat162* e = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(e[j]);
+      e[j] = __floats2bfloat162_rn(f.x * f_s[c8 * 8 + 2 * j], f.y * f_s[c8 * 8 + 2 * j + 1]);
+    }
+    P[i] = v;
   }
 }
 
-// ------------------------------------------------------------------ K3: softmax statistics
-// One warp per (hidden request, head): m = max_j s_j, l = sum_j 2^(s_j - m) (log2 domain,
-// scores scaled by scale*log2 e); P[row][h] = 2^(s - m) in bf16 for the request's rows
-// (padding rows of the last block get P = 0); the key-bias constant q_h . b_K,h.
-__global__ void __launch_bounds__(128) stats_kernel(const AbsorbParams p) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= p.n_h * p.H) return;
-  const int r = w / p.H, h = w - r * p.H;
-  const int base = p.hrow0[r], ntok = p.hntok[r], Hp = p.Hp;
-  float m = -INFINITY;
-  for (int t = lane; t < ntok; t += 32) m = fmaxf(m, p.s[(size_t)(base + t) * Hp + h] * p.scale_log2);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
-  float l = 0.f;
-  for (int t = lane; t < ntok; t += 32) {
-    const float e = exp2f(p.s[(size_t)(base + t) * Hp + h] * p.scale_log2 - m);
-    l += e;
-    p.pm[(size_t)(base + t) * Hp + h] = __float2bfloat16_rn(e);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(FULL, l, o);
-  float c = 0.f;
-  if (p.b_int) {   // q_h . b_K,h
-    const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.q) + (size_t)p.hreq[r] * p.d + h * p.dh;
-    for (int e = lane; e < p.dh; e += 32) c += __bfloat162float(q[e]) * p.b_int[h * 2 * p.dh + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  }
-  if (lane == 0) {
-    p.ml[3 * (size_t)w] = m;
-    p.ml[3 * (size_t)w + 1] = l;
-    p.ml[3 * (size_t)w + 2] = c;
-  }
-}
-
-// ------------------------------------------------------------------ K4: Z = P^T X
-// CTA: one hidden request x 128 columns of d; M = Hp heads (<= 128), K loop over the
-// request's rows in 64s.  A = P^T (P tile [64 rows x Hp] -> ldmatrix.trans), B = X tile
-// [64 rows x 128 cols] (row-major K x N -> ldmatrix.trans).  4 warps split N (32 each).
-__global__ void __launch_bounds__(128) z_kernel(const AbsorbParams p) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  constexpr int ST = 2;
-  const int Hp = p.Hp;
-  const int PH = (Hp + 63) / 64;                  // 64-column halves of the P tile
-  uint8_t* sP = sm;                               // ST x [PH halves x 64 rows x 64 cols]
-  uint8_t* sX = sm + ST * PH * 64 * 128;          // ST x [64 rows x 128 cols] as 2 halves
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// ------------------------------------------------------------------ K4: Z = P^T X on tcgen05
+// CTA: one hidden request x 128 columns of d.  D[128 heads x 128 cols] += P^T X over the
+// request's 64-token k-blocks; A = P^T and B = X are both MN-major (P rows [token][Hp] and X
+// rows [token][d] as stored), SWIZZLE_128B, loaded by TMA (P: 2 boxes of 64 heads x 64
+// tokens, heads >= Hp zero-filled out of bounds; X: the request's pool blocks, 64-column
+// boxes).  Token rows past n in the last k-block are zeroed in smem by the MMA warp (pool
+// slots past n are never written; rows past the request's blocks belong to the next one).
+// Epilogue: thread = head, Z row slice -> bf16.
+__global__ void __launch_bounds__(TC_THREADS, 2)
+    z_tc_kernel(const __grid_constant__ CUtensorMap tmap_x64, const __grid_constant__ CUtensorMap tmap_p,
+                const AbsorbParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Z_ST * Z_STAGE);
+  uint64_t* empty = full + Z_ST;
+  uint64_t* tfull = empty + Z_ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * 128, r = blockIdx.y;
-  const int d = p.d, B = p.B, H = p.H;
-  const int base = p.hrow0[r], ntok = p.hntok[r];
-  const __nv_bfloat16* pool = static_cast<const __nv_bfloat16*>(p.pool);
-  // rows >= ntok are zero-filled in both operands (slots past n in the last block are
-  // never written by hc_append and may hold anything)
-  auto load = [&](int t0, int buf) {
-    uint8_t* ps = sP + buf * PH * 64 * 128;
-    uint8_t* xs = sX + buf * 64 * 256;
-    for (int i = tid; i < 64 * (Hp / 8); i += 128) {
-      const int row = i / (Hp / 8), c = i % (Hp / 8);
-      const bool ok = t0 + row < ntok;
-      cp16_zfill(ps + (c >> 3) * (64 * 128) + sw64(row, c & 7),
-                 p.pm + (size_t)(base + (ok ? t0 + row : 0)) * Hp + c * 8, ok);
+  const int ntok = p.hntok[r], base = p.hrow0[r], B = p.B, H = p.H, d = p.d;
+  const int nkb = (ntok + 63) / 64;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_x64);
+    ptx::prefetch_tmap(&tmap_p);
+    for (int s = 0; s < Z_ST; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
     }
-    for (int i = tid; i < 64 * 16; i += 128) {
-      const int row = i >> 4, c = i & 15;
-      const bool ok = t0 + row < ntok;
-      const int grow = base + (ok ? t0 + row : 0), g = grow / B;
-      cp16_zfill(xs + (c >> 3) * (64 * 128) + sw64(row, c & 7),
-                 pool + ((size_t)p.gather[g] * B + (grow - g * B)) * d + n0 + c * 8, ok);
-    }
-  };
-  const int MT = Hp / 16;
-  float acc[8][4][4];   // [m-tile (<= 8)][n-tile (4 x 8 cols)][frag]
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0.f;
-  const int nkt = (ntok + 63) / 64;
-  load(0, 0);
-  cp_commit();
-  const int mat = lane >> 3, rr = lane & 7;
-  for (int kt = 0; kt < nkt; ++kt) {
-    if (kt + 1 < nkt) load((kt + 1) * 64, (kt + 1) & 1);
-    cp_commit();
-    cp_wait<1>();
-    __syncthreads();
-    const uint32_t p_s = saddr(sP + (kt & 1) * PH * 64 * 128), x_s = saddr(sX + (kt & 1) * 64 * 256);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {   // 16 rows (K) per step
-      // B fragments for this warp's 32 columns: 2 x ldmatrix.x4.trans (16 cols each)
-      uint32_t b[4][2];
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        const int col_chunk = (warp * 32 + nb * 16) / 8 + (mat >> 1);
-        const int krow = ks * 16 + ((mat & 1) << 3) + rr;
-        uint32_t b0, b1, b2, b3;
-        ldsm4t(x_s + (col_chunk >> 3) * (64 * 128) + sw64(krow, col_chunk & 7), b0, b1, b2, b3);
-        b[2 * nb][0] = b0;
-        b[2 * nb][1] = b1;
-        b[2 * nb + 1][0] = b2;
-        b[2 * nb + 1][1] = b3;
-      }
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        if (mi >= MT) break;
-        // A = P^T rows (heads) mi*16.., k = rows ks*16..: transpose of the [row x head] tile
-        uint32_t a0, a1, a2, a3;
-        const int head_chunk = mi * 2 + (mat >> 1);   // 8 heads per chunk
-        const int krow = ks * 16 + ((mat & 1) << 3) + rr;
-        ldsm4t(p_s + (head_chunk >> 3) * (64 * 128) + sw64(krow, head_chunk & 7), a0, a1, a2, a3);
-        // ldmatrix.trans order: m0 (heads 0-7, k 0-7), m1 (heads 0-7, k 8-15), m2 (heads 8-15, k 0-7),
-        // m3 (heads 8-15, k 8-15) -> A fragment {a0: m0, a1: m2, a2: m1, a3: m3}
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) mma(acc[mi][nt], a0, a2, a1, a3, b[nt][0], b[nt][1]);
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<128>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      const int rpb = p.rpb64, nbox = 64 / rpb;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], Z_STAGE);
+        uint8_t* a = smem + stage * Z_STAGE;
+        uint8_t* b = a + 16384;
+        ptx::tma_load_2d(a, &tmap_p, 0, base + kb * 64, &full[stage]);
+        ptx::tma_load_2d(a + 8192, &tmap_p, 64, base + kb * 64, &full[stage]);
+        for (int i = 0; i < nbox; ++i) {
+          const int grow = base + kb * 64 + i * rpb, g = grow / B;
+          const int prow = g < p.n_hb ? p.gather[g] * B + (grow - g * B) : 0;
+          ptx::tma_load_2d(b + i * rpb * 128, &tmap_x64, n0, prow, &full[stage]);
+          ptx::tma_load_2d(b + 8192 + i * rpb * 128, &tmap_x64, n0 + 64, prow, &full[stage]);
+        }
+        if (++stage == Z_ST) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
     }
-    __syncthreads();
-  }
-  const int g = lane >> 2, t4 = lane & 3;
+  } else if (warp == 1) {
+    // (a = P^T: M = heads, MN-major, 64-head chunks 8 KiB apart; b = X: N = columns)
+    const uint32_t idesc = ptx::umma_idesc_bf16_f32(128, 128) | (1u << 15) | (1u << 16);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      ptx::mbar_wait(&full[stage], phase);
+      uint8_t* a = smem + stage * Z_STAGE;
+      const int valid = ntok - kb * 64;
+      if (valid < 64) {   // zero X rows [valid, 64) of both 64-column chunks
+        const int per = (64 - valid) * 8;
+        for (int i = lane; i < 2 * per; i += 32) {
+          const int ch = i / per, rem = i - ch * per;
+          *reinterpret_cast<uint4*>(a + 16384 + ch * 8192 + (valid + (rem >> 3)) * 128 + (rem & 7) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+        ptx::fence_proxy_async_smem();
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tc_fence_after();
+        const uint32_t aa = ptx::smem_u32(a), bb = aa + 16384;
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    if (mi >= MT) break;
+        for (int k = 0; k < 4; ++k)
+          ptx::umma_f16_ss(tmem, umma_desc_mn_sw128(aa + k * 2048, 8192), umma_desc_mn_sw128(bb + k * 2048, 8192),
+                           idesc, (kb | k) != 0 ? 1u : 0u);
+        ptx::umma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == Z_ST) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (lane == 0) ptx::umma_commit(tfull);
+    __syncwarp();
+  } else {
+    const int q = warp & 3, h = q * 32 + lane;
+    ptx::mbar_wait(tfull, 0);
+    ptx::tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+      ptx::tmem_ld_wait();
+      if (h < H) {
+        uint4* dst = reinterpret_cast<uint4*>(p.z + ((size_t)r * H + h) * d + n0 + c);
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int col = n0 + warp * 32 + nt * 8 + 2 * t4;
-      const int ha = mi * 16 + g, hb = ha + 8;
-      if (ha < H) *reinterpret_cast<uint32_t*>(p.z + ((size_t)r * H + ha) * d + col) = pk(acc[mi][nt][0], acc[mi][nt][1]);
-      if (hb < H) *reinterpret_cast<uint32_t*>(p.z + ((size_t)r * H + hb) * d + col) = pk(acc[mi][nt][2], acc[mi][nt][3]);
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pk(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
+                              pk(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                              pk(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                              pk(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+      }
     }
   }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<128>(tmem);
 }
 
 // ------------------------------------------------------------------ K5: o = W_V,h z / l + b_V
+constexpr int kST = 4;   // cp.async pipeline depth of K5
 // CTA: 64 hidden requests x dh outputs of one head, K loop over d in 64s.  A = Z[r][h]
 // rows (K contiguous), B = W_V,h [dh x d] rows (N x K, K contiguous -> non-trans).
 __global__ void __launch_bounds__(128) wv_kernel(const AbsorbParams p) {
   extern __shared__ __align__(128) uint8_t sm[];
-  constexpr int ST = 2;
   const int dh = p.dh, d = p.d, H = p.H;
-  uint8_t* sA = sm;                        // ST x [64 x 64]
-  uint8_t* sB = sm + ST * 64 * 128;        // ST x [dh x 64]
+  const int stage_bytes = 64 * 128 + dh * 128;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.x, r0 = blockIdx.y * 64;
   const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w_int);
-  auto load = [&](int kc, int buf) {
-    uint8_t* a = sA + buf * 64 * 128;
-    uint8_t* b = sB + buf * dh * 128;
+  auto load = [&](int kc, int st) {
+    uint8_t* a = sm + st * stage_bytes;
+    uint8_t* b = a + 64 * 128;
     for (int i = tid; i < 64 * 8; i += 128) {
       const int row = i >> 3, c = i & 7;
       const bool ok = r0 + row < p.n_h;
@@ -352,15 +484,16 @@ __global__ void __launch_bounds__(128) wv_kernel(const AbsorbParams p) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
   const int KC = d / 64;
-  load(0, 0);
-  cp_commit();
+#pragma unroll
+  for (int st = 0; st < kST - 1; ++st) {
+    if (st < KC) load(st, st);
+    cp_commit();
+  }
   const int mat = lane >> 3, rr = lane & 7;
   for (int kc = 0; kc < KC; ++kc) {
-    if (kc + 1 < KC) load(kc + 1, (kc + 1) & 1);
-    cp_commit();
-    cp_wait<1>();
+    cp_wait<kST - 2>();
     __syncthreads();
-    const uint32_t a_s = saddr(sA + (kc & 1) * 64 * 128), b_s = saddr(sB + (kc & 1) * dh * 128);
+    const uint32_t a_s = saddr(sm + (kc % kST) * stage_bytes), b_s = a_s + 64 * 128;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       uint32_t a0, a1, a2, a3;
@@ -375,8 +508,11 @@ __global__ void __launch_bounds__(128) wv_kernel(const AbsorbParams p) {
         }
       }
     }
-    __syncthreads();
+    const int nk = kc + kST - 1;
+    if (nk < KC) load(nk, nk % kST);
+    cp_commit();
   }
+  cp_wait<0>();
   const int g = lane >> 2, t4 = lane & 3;
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
 #pragma unroll
@@ -403,26 +539,37 @@ __global__ void __launch_bounds__(128) wv_kernel(const AbsorbParams p) {
 
 }  // namespace
 
-bool absorb_supported(int dtype, int d, int dh, int H) {
-  return dtype == 0 && d % 128 == 0 && dh % 16 == 0 && dh <= 128 && H <= 128;
+bool absorb_supported(int dtype, int d, int dh, int H, int B) {
+  return dtype == 0 && d % 128 == 0 && dh % 16 == 0 && dh <= 128 && H <= 128 && B % 8 == 0 &&
+         (128 % B == 0 || B % 128 == 0);
 }
 
-cudaError_t launch_absorbed(const AbsorbParams& p, cudaStream_t s) {
+int absorb_launches() { return 5; }
+
+cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
+                            const void* tmap_p, cudaStream_t s) {
   if (p.n_h <= 0) return cudaSuccess;
-  cudaError_t e;
-  qt_kernel<<<dim3(p.d / 128, p.H, (p.n_h + 63) / 64), 128, 0, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int smem2 = 2 * 64 * 128 + 2 * p.Hp * 128;
-  score_kernel<<<p.n_tiles, 128, smem2, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  stats_kernel<<<(p.n_h * p.H + 3) / 4, 128, 0, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int smem4 = 2 * ((p.Hp + 63) / 64) * 64 * 128 + 2 * 64 * 256;
-  static const cudaError_t attr = cudaFuncSetAttribute(z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 2 * 64 * 128 + 2 * 64 * 256);
+  constexpr int smem_tc = 1024 + 3 * 32768 + 256 + 512;
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(z_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(wv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kST * (64 * 128 + 128 * 128));
+    return e;
+  }();
   if (attr != cudaSuccess) return attr;
-  z_kernel<<<dim3(p.d / 128, p.n_h), 128, smem4, s>>>(p);
+  cudaError_t e;
+  qt_kernel<<<dim3(p.d / 128, p.Hp, (p.n_h + 63) / 64), 128, 0, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int smem5 = 2 * 64 * 128 + 2 * p.dh * 128;
+  score_tc_kernel<<<p.n_tiles, TC_THREADS, smem_tc, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
+                                                          *static_cast<const CUtensorMap*>(tmap_qt), p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  rescale_kernel<<<p.n_tiles, 128, 0, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  z_tc_kernel<<<dim3(p.d / 128, p.n_h), TC_THREADS, smem_tc, s>>>(*static_cast<const CUtensorMap*>(tmap_x64),
+                                                                   *static_cast<const CUtensorMap*>(tmap_p), p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int smem5 = kST * (64 * 128 + p.dh * 128);
   wv_kernel<<<dim3(p.H, (p.n_h + 63) / 64), 128, smem5, s>>>(p);
   return cudaGetLastError();
 }

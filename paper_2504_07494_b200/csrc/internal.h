@@ -149,29 +149,36 @@ bool prefill_attn_mma_supported(int dtype, int dh);
 
 // Absorbed hidden-cache attention (NEXT row f4 (ii), opt-in, absorbed.cu).  Hidden request
 // r (0..n_h-1) owns gathered rows [hrow0[r], hrow0[r] + hntok[r]) (row g*B + t = slot t of
-// pool block gather[g]); its tokens are split into 64-row score tiles (tile_req, tile_t0).
+// pool block gather[g]); its tokens are split into 128-row score tiles (tile_req, tile_t0).
 struct AbsorbParams {
   const int32_t* gather;   // pool block id of each hidden block (request order)
   const int32_t* hreq;     // [n_h] batch index of each hidden request
   const int32_t* hrow0;    // [n_h] first gathered row
   const int32_t* hntok;    // [n_h] cached tokens
   const int32_t* tile_req; // [n_tiles]
-  const int32_t* tile_t0;  // [n_tiles]
+  const int32_t* tile_t0;  // [n_tiles] (128-token tiles)
+  const int32_t* htile0;   // [n_h] first score tile of each hidden request
   const void* pool;
   const void* q;           // [n_req, d]
   const void* w_int;       // head-interleaved W_KV: row h*2dh + kv*dh + c
   const float* b_int;      // nullable, same interleaving
-  __nv_bfloat16* qt;       // [n_h][H][d]   q~ = W_K,h^T q_h
-  float* s;                // [rows][Hp]    raw scores q~ . x
-  __nv_bfloat16* pm;       // [rows][Hp]    2^(scaled score - m)
+  __nv_bfloat16* qt;       // [n_h][Hp][d]  q~ = W_K,h^T q_h (rows H..Hp-1 zero)
+  __nv_bfloat16* pm;       // [rows][Hp]    2^(scaled score - m_t), m_t = its tile's max
+  float* tml;              // [n_tiles][Hp][2] tile max m_t (log2 domain), tile sum l_t
   float* ml;               // [n_h][H][3]   m (log2 domain), l, q_h . b_K,h
   __nv_bfloat16* z;        // [n_h][H][d]   sum_j 2^(s_j - m) x_j
   void* out;               // [n_req, d]
   float* lse;              // nullable [n_req, H]
   int32_t n_h, n_tiles, H, Hp, dh, d, B;
+  int32_t n_hb;            // gathered hidden blocks
+  int32_t rpb, rpb64;      // rows per TMA box of the pool tensor maps: min(B,128), min(B,64)
   float scale, scale_log2;
 };
-bool absorb_supported(int dtype, int d, int dh, int H);
-cudaError_t launch_absorbed(const AbsorbParams& p, cudaStream_t s);
+bool absorb_supported(int dtype, int d, int dh, int H, int B);
+int absorb_launches();
+// tmap_x / tmap_x64: pool rows with {64 x min(B,128)} / {64 x min(B,64)} boxes; tmap_qt:
+// q~ [n_h*Hp, d] with {64 x Hp} boxes; tmap_p: P [rows, Hp] with {64 x 64} boxes.
+cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
+                            const void* tmap_p, cudaStream_t s);
 
 }  // namespace hc

@@ -159,8 +159,8 @@ struct Plan {
   int64_t n_tab = 0;
   size_t off_reqs, off_splits, off_tabs, off_gather, off_hpos, off_kvsplit, off_hidsplit, off_tiledone, desc_bytes;
   size_t off_ml, off_acc, off_sk, off_sv, total;
-  size_t off_hreq, off_hrow0, off_hntok, off_treq, off_tt0;   // absorb descriptor
-  size_t off_qt, off_s, off_pm, off_abml, off_z;              // absorb workspace
+  size_t off_hreq, off_hrow0, off_hntok, off_htile0, off_treq, off_tt0;   // absorb descriptor
+  size_t off_qt, off_tml, off_pm, off_abml, off_z;                        // absorb workspace
 };
 
 }  // namespace
@@ -175,7 +175,8 @@ struct hc_pool {
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_ids;
   std::unordered_map<int64_t, Req> reqs;
   CUtensorMap tmap_x{}, tmap_w{}, tmap_w_half{};
-  CUtensorMap tmap_wqkv{}, tmap_wo{};   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
+  CUtensorMap tmap_wqkv{}, tmap_wo{};
+  CUtensorMap tmap_x64{};               // pool rows, {64 x min(B,64)} boxes (absorbed Z GEMM)   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
   bool tc_ok = false;
   bool dense_tc_ok = false;             // bf16 tcgen05 path for the current-token / output GEMMs
   int num_sms = 148;
@@ -264,7 +265,7 @@ struct hc_pool {
         P.n_hb += (int32_t)nb;
         if (P.absorb) {
           ++P.n_h;
-          P.n_atiles += (int32_t)cdiv(r->n, 64);
+          P.n_atiles += (int32_t)cdiv(r->n, 128);
         } else {
           P.n_splits += ns;
           P.n_hid_splits += ns;
@@ -303,6 +304,8 @@ struct hc_pool {
     o += sizeof(int32_t) * P.n_h;
     P.off_hntok = o = align_up(o, 64);
     o += sizeof(int32_t) * P.n_h;
+    P.off_htile0 = o = align_up(o, 64);
+    o += sizeof(int32_t) * P.n_h;
     P.off_treq = o = align_up(o, 64);
     o += sizeof(int32_t) * P.n_atiles;
     P.off_tt0 = o = align_up(o, 64);
@@ -318,9 +321,9 @@ struct hc_pool {
     if (P.absorb) {
       const size_t rows = (size_t)P.n_hb * B, d = cfg.d_model;
       P.off_qt = e;
-      e = align_up(e + (size_t)P.n_h * H * d * 2, kAlign);
-      P.off_s = e;
-      e = align_up(e + rows * P.Hp * sizeof(float), kAlign);
+      e = align_up(e + (size_t)P.n_h * P.Hp * d * 2, kAlign);
+      P.off_tml = e;
+      e = align_up(e + (size_t)P.n_atiles * P.Hp * 2 * sizeof(float), kAlign);
       P.off_pm = e;
       e = align_up(e + rows * P.Hp * 2, kAlign);
       P.off_abml = e;
@@ -366,10 +369,12 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
        !dense_tc_supported(cfg->d_model) || !(cfg->block_size <= 128 || cfg->block_size % 256 == 0)))
     return fail(HC_E_UNSUPPORTED, "RoPE needs the bf16 tcgen05 path and head_dim % 64 == 0");
   if ((cfg->flags & HC_FLAG_ABSORB_HIDDEN) &&
-      (cfg->rope_theta > 0.f || !absorb_supported(cfg->dtype, cfg->d_model, cfg->head_dim, cfg->n_heads)))
+      (cfg->rope_theta > 0.f || (cfg->flags & HC_FLAG_FORCE_SIMT) ||
+       !absorb_supported(cfg->dtype, cfg->d_model, cfg->head_dim, cfg->n_heads, cfg->block_size) ||
+       !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)))
     return fail(HC_E_UNSUPPORTED,
                 "HC_FLAG_ABSORB_HIDDEN needs bf16, no RoPE, d % 128 == 0, head_dim % 16 == 0, head_dim <= 128, "
-                "n_heads <= 128");
+                "n_heads <= 128, block_size % 8 == 0 dividing or divisible by 128");
   if (!accounting) {
     if (!cfg->storage || cfg->storage_bytes < L.total)
       return fail(HC_E_INVALID, "storage null or smaller than hc_pool_storage_bytes()");
@@ -441,7 +446,10 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
                                     2 * (uint64_t)cfg->d_model, 64, 256);
       const bool ok3 = make_tmap_2d(&p->tmap_w_half, p->storage + L.w_off, (uint64_t)cfg->d_model,
                                     2 * (uint64_t)cfg->d_model, 64, 128);
-      if (!ok1 || !ok2 || !ok3) {
+      const bool ok4 = !(cfg->flags & HC_FLAG_ABSORB_HIDDEN) ||
+                       make_tmap_2d(&p->tmap_x64, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
+                                    (uint64_t)cfg->num_blocks * cfg->block_size, 64, (uint32_t)std::min(cfg->block_size, 64));
+      if (!ok1 || !ok2 || !ok3 || !ok4) {
         delete p;
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed");
       }
@@ -686,6 +694,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   int32_t* ahreq = reinterpret_cast<int32_t*>(h + P.off_hreq);
   int32_t* ahrow0 = reinterpret_cast<int32_t*>(h + P.off_hrow0);
   int32_t* ahntok = reinterpret_cast<int32_t*>(h + P.off_hntok);
+  int32_t* ahtile0 = reinterpret_cast<int32_t*>(h + P.off_htile0);
   int32_t* atreq = reinterpret_cast<int32_t*>(h + P.off_treq);
   int32_t* att0 = reinterpret_cast<int32_t*>(h + P.off_tt0);
   int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0, n_ah = 0, n_at = 0;
@@ -709,7 +718,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
         ahreq[n_ah] = i;
         ahrow0[n_ah] = n_hb * B;
         ahntok[n_ah] = (int32_t)r.n;
-        for (int32_t t0 = 0; t0 < r.n; t0 += 64) {
+        ahtile0[n_ah] = n_at;
+        for (int32_t t0 = 0; t0 < r.n; t0 += 128) {
           atreq[n_at] = n_ah;
           att0[n_at++] = t0;
         }
@@ -793,12 +803,13 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       bp.hntok = reinterpret_cast<const int32_t*>(ws + P.off_hntok);
       bp.tile_req = reinterpret_cast<const int32_t*>(ws + P.off_treq);
       bp.tile_t0 = reinterpret_cast<const int32_t*>(ws + P.off_tt0);
+      bp.htile0 = reinterpret_cast<const int32_t*>(ws + P.off_htile0);
       bp.pool = blocks;
       bp.q = q;
       bp.w_int = rp.w_int;
       bp.b_int = rp.b_int;
       bp.qt = reinterpret_cast<__nv_bfloat16*>(ws + P.off_qt);
-      bp.s = reinterpret_cast<float*>(ws + P.off_s);
+      bp.tml = reinterpret_cast<float*>(ws + P.off_tml);
       bp.pm = reinterpret_cast<__nv_bfloat16*>(ws + P.off_pm);
       bp.ml = reinterpret_cast<float*>(ws + P.off_abml);
       bp.z = reinterpret_cast<__nv_bfloat16*>(ws + P.off_z);
@@ -813,9 +824,16 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       bp.B = B;
       bp.scale = scale;
       bp.scale_log2 = ap.scale_log2;
-      err = launch_absorbed(bp, s);
+      bp.n_hb = P.n_hb;
+      bp.rpb = std::min(B, 128);
+      bp.rpb64 = std::min(B, 64);
+      CUtensorMap tm_qt, tm_p;
+      if (!make_tmap_2d(&tm_qt, ws + P.off_qt, (uint64_t)bp.d, (uint64_t)P.n_h * P.Hp, 64, (uint32_t)P.Hp) ||
+          !make_tmap_2d(&tm_p, ws + P.off_pm, (uint64_t)P.Hp, (uint64_t)P.n_hb * B, 64, 64))
+        return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (absorbed path)");
+      err = launch_absorbed(bp, &pool->tmap_x, &pool->tmap_x64, &tm_qt, &tm_p, s);
       if (err != cudaSuccess) return cuda_fail(err, "absorbed hidden attention");
-      launches += 5;
+      launches += absorb_launches();
     }
     if (pool->profiling) cudaEventRecord(ev[2], s);
     if (P.n_splits > 0) {

@@ -265,7 +265,7 @@ class HybridCachePool:
         self._ws = None
 
     def close(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and hc_pool_destroy is not None:   # None at interpreter exit
             hc_pool_destroy(self.handle)
             self.handle = None
 

@@ -485,7 +485,7 @@ def test_absorbed_mixed_batch_vs_oracle(hc, d, H, dh, B):
     w = _bf16_workload(d, H, dh, B, bias=True)
     pool, out, lse = _run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
     assert pool.last_decode_path() == 3
-    assert pool.last_launch_count() == 7      # q~, scores, stats, Z, W_V, attention, combine
+    assert pool.last_launch_count() == 7      # q~, scores, rescale, Z, W_V, attention, combine
     err, lerr = T.compare(w, out, lse, range(len(w.n)))
     assert err <= TOL_BF16, err
     assert lerr <= 5e-2, lerr
