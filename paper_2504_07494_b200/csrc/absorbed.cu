@@ -20,6 +20,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -147,8 +149,7 @@ __global__ void __launch_bounds__(128) qt_kernel(const AbsorbParams p) {
 // token row): scaled scores -> smem (column-major), per-head tile max m_t and l_t =
 // sum 2^(s - m_t) by column scans, P = 2^(s - m_t) bf16 rows (0 for the padding slots of
 // the request's last block).
-constexpr int SC_ST = 3, SC_STAGE = 32768;   // 16 KiB A + <= 16 KiB B per stage
-constexpr int Z_ST = 3, Z_STAGE = 32768;     // 16 KiB P^T + 16 KiB X per stage
+constexpr int SC_STAGE = 32768;   // 16 KiB A + <= 16 KiB B per stage
 constexpr int TC_THREADS = 192;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -170,12 +171,14 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint3
   return d;
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 2)
+template <int SC_ST>
+__global__ void __launch_bounds__(TC_THREADS, SC_ST == 2 ? 3 : 2)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_qt,
                     const AbsorbParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SC_ST * SC_STAGE);
+  // stages, then (after the MMAs retire) the [Hp][129] fp32 score staging of the epilogue
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + max(SC_ST * SC_STAGE, 128 * 129 * 4));
   uint64_t* empty = full + SC_ST;
   uint64_t* tfull = empty + SC_ST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
@@ -342,9 +345,11 @@ __global__ void __launch_bounds__(128) rescale_kernel(const AbsorbParams p) {
 // boxes).  Token rows past n in the last k-block are zeroed in smem by the MMA warp (pool
 // slots past n are never written; rows past the request's blocks belong to the next one).
 // Epilogue: thread = head, Z row slice -> bf16.
-__global__ void __launch_bounds__(TC_THREADS, 2)
+template <int BN, int ST>
+__global__ void __launch_bounds__(TC_THREADS, BN * ST <= 256 ? 3 : (BN == 128 ? 2 : 1))
     z_tc_kernel(const __grid_constant__ CUtensorMap tmap_x64, const __grid_constant__ CUtensorMap tmap_p,
                 const AbsorbParams p) {
+  constexpr int Z_ST = ST, Z_STAGE = 16384 + BN * 128, NCH = BN / 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Z_ST * Z_STAGE);
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   uint64_t* tfull = empty + Z_ST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 128, r = blockIdx.y;
+  const int n0 = blockIdx.x * BN, r = blockIdx.y;
   const int ntok = p.hntok[r], base = p.hrow0[r], B = p.B, H = p.H, d = p.d;
   const int nkb = (ntok + 63) / 64;
   if (warp == 0 && lane == 0) {
@@ -365,7 +370,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     ptx::mbar_init(tfull, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<128>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<BN>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -385,8 +390,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         for (int i = 0; i < nbox; ++i) {
           const int grow = base + kb * 64 + i * rpb, g = grow / B;
           const int prow = g < p.n_hb ? p.gather[g] * B + (grow - g * B) : 0;
-          ptx::tma_load_2d(b + i * rpb * 128, &tmap_x64, n0, prow, &full[stage]);
-          ptx::tma_load_2d(b + 8192 + i * rpb * 128, &tmap_x64, n0 + 64, prow, &full[stage]);
+#pragma unroll
+          for (int j = 0; j < NCH; ++j)
+            ptx::tma_load_2d(b + j * 8192 + i * rpb * 128, &tmap_x64, n0 + 64 * j, prow, &full[stage]);
         }
         if (++stage == Z_ST) {
           stage = 0;
@@ -396,16 +402,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
   } else if (warp == 1) {
     // (a = P^T: M = heads, MN-major, 64-head chunks 8 KiB apart; b = X: N = columns)
-    const uint32_t idesc = ptx::umma_idesc_bf16_f32(128, 128) | (1u << 15) | (1u << 16);
+    const uint32_t idesc = ptx::umma_idesc_bf16_f32(128, BN) | (1u << 15) | (1u << 16);
     int stage = 0;
     uint32_t phase = 0;
     for (int kb = 0; kb < nkb; ++kb) {
       ptx::mbar_wait(&full[stage], phase);
       uint8_t* a = smem + stage * Z_STAGE;
       const int valid = ntok - kb * 64;
-      if (valid < 64) {   // zero X rows [valid, 64) of both 64-column chunks
+      if (valid < 64) {   // zero X rows [valid, 64) of every 64-column chunk
         const int per = (64 - valid) * 8;
-        for (int i = lane; i < 2 * per; i += 32) {
+        for (int i = lane; i < NCH * per; i += 32) {
           const int ch = i / per, rem = i - ch * per;
           *reinterpret_cast<uint4*>(a + 16384 + ch * 8192 + (valid + (rem >> 3)) * 128 + (rem & 7) * 16) =
               make_uint4(0, 0, 0, 0);
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     ptx::mbar_wait(tfull, 0);
     ptx::tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
+    for (int c = 0; c < BN; c += 32) {
       uint32_t v[32];
       ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
       ptx::tmem_ld_wait();
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc<128>(tmem);
+  if (warp == 1) ptx::tmem_dealloc<BN>(tmem);
 }
 
 // ------------------------------------------------------------------ K5: o = W_V,h z / l + b_V
@@ -546,13 +552,33 @@ bool absorb_supported(int dtype, int d, int dh, int H, int B) {
 
 int absorb_launches() { return 5; }
 
+template <int BN, int ST>
+static cudaError_t launch_z(const AbsorbParams& p, const CUtensorMap& tx, const CUtensorMap& tp, cudaStream_t s) {
+  constexpr int smem = 1024 + ST * (16384 + BN * 128) + 256;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(z_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return attr;
+  z_tc_kernel<BN, ST><<<dim3(p.d / BN, p.n_h), TC_THREADS, smem, s>>>(tx, tp, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
                             const void* tmap_p, cudaStream_t s) {
   if (p.n_h <= 0) return cudaSuccess;
   constexpr int smem_tc = 1024 + 3 * 32768 + 256 + 512;
+  static const int zcfg = [] {   // Z GEMM tile width x pipeline depth (A/B knob; default 128x2: 3 CTAs per SM)
+    const char* e = std::getenv("HC_Z_CFG");
+    return e ? std::atoi(e) : 1282;
+  }();
+  static const int sst = [] {
+    const char* e = std::getenv("HC_SCORE_ST");   // A/B knob: 2 stages (3 CTAs/SM, default) or 3
+    return e ? std::atoi(e) : 2;
+  }();
+  constexpr int smem_s2 = 1024 + 128 * 129 * 4 + 256 + 512;
   static const cudaError_t attr = [] {
-    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(z_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
+    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(score_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s2);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(wv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kST * (64 * 128 + 128 * 128));
     return e;
@@ -561,13 +587,24 @@ cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const voi
   cudaError_t e;
   qt_kernel<<<dim3(p.d / 128, p.Hp, (p.n_h + 63) / 64), 128, 0, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  score_tc_kernel<<<p.n_tiles, TC_THREADS, smem_tc, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
-                                                          *static_cast<const CUtensorMap*>(tmap_qt), p);
+  if (sst == 2)
+    score_tc_kernel<2><<<p.n_tiles, TC_THREADS, smem_s2, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
+                                                              *static_cast<const CUtensorMap*>(tmap_qt), p);
+  else
+    score_tc_kernel<3><<<p.n_tiles, TC_THREADS, smem_tc, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
+                                                              *static_cast<const CUtensorMap*>(tmap_qt), p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   rescale_kernel<<<p.n_tiles, 128, 0, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  z_tc_kernel<<<dim3(p.d / 128, p.n_h), TC_THREADS, smem_tc, s>>>(*static_cast<const CUtensorMap*>(tmap_x64),
-                                                                   *static_cast<const CUtensorMap*>(tmap_p), p);
+  const CUtensorMap& tx = *static_cast<const CUtensorMap*>(tmap_x64);
+  const CUtensorMap& tp = *static_cast<const CUtensorMap*>(tmap_p);
+  if (zcfg == 2564 && p.d % 256 == 0)
+    e = launch_z<256, 4>(p, tx, tp, s);
+  else if (zcfg == 1283)
+    e = launch_z<128, 3>(p, tx, tp, s);
+  else
+    e = launch_z<128, 2>(p, tx, tp, s);
+  if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int smem5 = kST * (64 * 128 + p.dh * 128);
   wv_kernel<<<dim3(p.H, (p.n_h + 63) / 64), 128, smem5, s>>>(p);
