@@ -382,7 +382,8 @@ def main():
     if absorbed:
         n_h = sum(1 for m in w.modes if m == 1)
         ab_bytes = 2 * hid_tok * d * s + 2 * d * d * s + 4 * n_h * d * 2 * 2
-        B_alg = kv_tok * 2 * d * s + hid_tok * d * s + 2 * d * d * s + 2 * n_req * d * s
+        # the variant's own floor: x read twice (scores, then Z), W_K and W_V once, q/out
+        B_alg = kv_tok * 2 * d * s + 2 * hid_tok * d * s + 2 * d * d * s + 2 * n_req * d * s
         F_alg = 0
     kernels = {
         ("fused_step" if fused else "recon_gemm"): {
