@@ -158,19 +158,6 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// UMMA descriptor, MN-major operand in the canonical SWIZZLE_128B layout: 128-B rows hold
-// 64 consecutive M/N elements of one k; 8 rows (8 k) form a 1024-B swizzle atom; atoms
-// stack along K at SBO = 1024 B; 64-element M/N chunks are LBO bytes apart.
-__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
 template <int SC_ST>
 __global__ void __launch_bounds__(TC_THREADS, SC_ST == 2 ? 3 : 2)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_qt,
@@ -424,7 +411,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN * ST <= 256 ? 3 : (BN == 128 ? 
         const uint32_t aa = ptx::smem_u32(a), bb = aa + 16384;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          ptx::umma_f16_ss(tmem, umma_desc_mn_sw128(aa + k * 2048, 8192), umma_desc_mn_sw128(bb + k * 2048, 8192),
+          ptx::umma_f16_ss(tmem, ptx::umma_desc_mn_sw128(aa + k * 2048, 8192), ptx::umma_desc_mn_sw128(bb + k * 2048, 8192),
                            idesc, (kb | k) != 0 ? 1u : 0u);
         ptx::umma_commit(&empty[stage]);
       }

@@ -146,6 +146,12 @@ struct PrefillAttnParams {
 };
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStream_t s);
 bool prefill_attn_mma_supported(int dtype, int dh);
+// tcgen05 version (128-query tiles; tile_q0 multiples of 128): tmap_q over q [R, d] and
+// tmap_kv over kv [R, 2d], both {64 x 128} boxes.  HC_PREFILL_TC=0 selects the mma.sync kernel.
+bool prefill_attn_tc_enabled();
+int prefill_attn_tc_keys();   // keys per tile (tmap_kv box rows)
+cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_q, const void* tmap_kv,
+                                   cudaStream_t s);
 
 // Absorbed hidden-cache attention (NEXT row f4 (ii), opt-in, absorbed.cu).  Hidden request
 // r (0..n_h-1) owns gathered rows [hrow0[r], hrow0[r] + hntok[r]) (row g*B + t = slot t of

@@ -9,10 +9,17 @@
 // softmax in exp2 with the scale folded in; the S accumulator is re-packed in registers as
 // the A operand of P V.  (First version of this row: the sm_80-style tensor-core path;
 // a tcgen05/TMEM version is the next step.)
+// prefill_attn_tc_kernel (bf16, dh 64/128, default): the same computation on tcgen05 —
+// see the kernel's comment.  prefill_attn_mma_kernel stays as the cross-check path
+// (HC_PREFILL_TC=0).
 // prefill_attn_simt_kernel: one warp per (query row, head), any dtype / dh (fp32 mode).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace hc {
 namespace {
@@ -223,6 +230,228 @@ __global__ void __launch_bounds__(128) prefill_attn_mma_kernel(const PrefillAttn
   }
 }
 
+
+// ------------------------------------------------------------------ tcgen05 / TMEM version
+// CTA = 128 query rows of one (request, head); 6 warps:
+//   warp 0     TMA producer: Q tile once, then K and V tiles of 128 keys (64-column boxes of
+//              the head's K_h || V_h slices of the projection output), 2-stage ring.
+//   warp 1     TMEM allocator + MMA issuer: S_j = Q K_j^T (M=128, N=128 keys, K=dh; both
+//              operands K-major) into one of two TMEM S buffers, issued one tile ahead so it
+//              overlaps the softmax of the previous tile; O += P_j V_j (M=128, N=dh, K=128
+//              keys; P from shared memory K-major, V as stored = MN-major) into TMEM.
+//   warps 2-5  softmax, thread = query row (TMEM lane): tcgen05.ld the S row, causal and
+//              length mask, exp2 with the scale folded in, P row -> swizzled smem (bf16).
+//              Lazy rescaling (the reference max only moves when a row max exceeds it by
+//              more than 2^8): O rows are rescaled in TMEM (ld / scale / st) only then;
+//              P <= 2^8 in bf16 is exact enough and l is fp32.  Epilogue: O / l -> bf16.
+// TMEM: S0 cols [0,128), S1 [128,256), O [256, 256+dh).
+template <int DH, int BK>
+__global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
+    prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_kv,
+                           const PrefillAttnParams p) {
+  constexpr int BM = 128, NCH = DH / 64, ST = 2, NPC = BK / 64;
+  constexpr int QCH = 128 * 128;                   // Q / P chunk: 128 rows x 64 columns (16 KiB)
+  constexpr int KCH = BK * 128;                    // K / V chunk: BK rows x 64 columns
+  constexpr int Q_OFF = 0, K_OFF = NCH * QCH, V_OFF = K_OFF + ST * NCH * KCH;
+  constexpr int P_OFF = V_OFF + ST * NCH * KCH, BAR_OFF = P_OFF + NPC * QCH;
+  constexpr uint32_t O_COL = 2 * BK;               // TMEM: S buffers [0, 2 BK), O [2 BK, 2 BK + DH)
+  constexpr float kRescale = 8.f;                  // log2 headroom before O is rescaled
+  // no alignment slack (two CTAs per SM need every KiB): the dynamic window is 1024-aligned
+  // when the kernel has no static shared memory; trap otherwise rather than overflow
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem) & 1023) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;        // [ST]
+  uint64_t* kv_empty = bars + 3;       // [ST]
+  uint64_t* s_full = bars + 5;         // [2]
+  uint64_t* s_free = bars + 7;         // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_done = bars + 10;
+  uint64_t* o_final = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y;
+  const int req = p.tile_req[blockIdx.x], q0 = p.tile_q0[blockIdx.x];
+  const int row0 = p.row0[req], L = p.row0[req + 1] - row0;
+  const int nt = (min(q0 + BM, L) + BK - 1) / BK;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_q);
+    ptx::prefetch_tmap(&tmap_kv);
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < ST; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_free[i], 128);
+    }
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(o_done, 1);
+    ptx::mbar_init(o_final, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<(2 * BK + DH <= 256 ? 256 : 512)>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_o = tmem + O_COL;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(q_full, NCH * QCH);
+      for (int c = 0; c < NCH; ++c) ptx::tma_load_2d(smem + Q_OFF + c * QCH, &tmap_q, h * DH + c * 64, row0 + q0, q_full);
+      for (int t = 0; t < nt; ++t) {
+        const int st = t % ST;
+        ptx::mbar_wait(&kv_empty[st], ((t / ST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * NCH * KCH);
+        for (int c = 0; c < NCH; ++c) {
+          ptx::tma_load_2d(smem + K_OFF + (st * NCH + c) * KCH, &tmap_kv, h * 2 * DH + c * 64, row0 + t * BK,
+                           &kv_full[st]);
+          ptx::tma_load_2d(smem + V_OFF + (st * NCH + c) * KCH, &tmap_kv, h * 2 * DH + DH + c * 64, row0 + t * BK,
+                           &kv_full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = ptx::umma_idesc_bf16_f32(BM, BK);
+      constexpr uint32_t idesc_o = ptx::umma_idesc_bf16_f32(BM, DH) | (1u << 16);   // B (V) MN-major
+      const uint32_t sq = ptx::smem_u32(smem + Q_OFF), sp = ptx::smem_u32(smem + P_OFF);
+      auto issue_s = [&](int t) {
+        const int st = t % ST, b = t & 1;
+        ptx::mbar_wait(&kv_full[st], (t / ST) & 1);
+        ptx::mbar_wait(&s_free[b], ((t >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t sk = ptx::smem_u32(smem + K_OFF + st * NCH * KCH);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          ptx::umma_f16_ss(tmem + b * BK, ptx::umma_desc_k_sw128(sq + (kk >> 2) * QCH + (kk & 3) * 32),
+                           ptx::umma_desc_k_sw128(sk + (kk >> 2) * KCH + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
+        ptx::umma_commit(&s_full[b]);
+      };
+      ptx::mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int t = 0; t < nt; ++t) {
+        if (t + 1 < nt) issue_s(t + 1);
+        ptx::mbar_wait(p_full, t & 1);
+        ptx::tc_fence_after();
+        const uint32_t sv = ptx::smem_u32(smem + V_OFF + (t % ST) * NCH * KCH);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          ptx::umma_f16_ss(tmem_o, ptx::umma_desc_k_sw128(sp + (kk >> 2) * QCH + (kk & 3) * 32),
+                           ptx::umma_desc_mn_sw128(sv + kk * 2048, KCH), idesc_o, (t | kk) != 0 ? 1u : 0u);
+        ptx::umma_commit(&kv_empty[t % ST]);
+        ptx::umma_commit(o_done);
+      }
+      ptx::umma_commit(o_final);
+    }
+    __syncwarp();
+  } else {
+    const int quad = warp & 3, row = quad * 32 + lane;
+    const int qi = q0 + row;                       // query token index (>= L: padding row)
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float sl = p.scale_log2;
+    float m_ref = -INFINITY, l = 0.f;
+    uint8_t* sP = smem + P_OFF;
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      ptx::mbar_wait(&s_full[b], (t >> 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t v[BK / 32][32];
+#pragma unroll
+      for (int c = 0; c < BK / 32; ++c) ptx::tmem_ld_32x32b_x32(tmem + lane_off + b * BK + c * 32, v[c]);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&s_free[b]);
+      // keys k0 + j valid iff k0 + j <= qi and < L
+      const int lim = min(qi, L - 1) - t * BK;     // last valid j (may be >= BK-1 or < 0)
+      float sv[BK];
+#pragma unroll
+      for (int c = 0; c < BK / 32; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(v[c][j]) * sl;
+      if (lim < BK - 1) {   // diagonal / last tile: mask
+#pragma unroll
+        for (int j = 0; j < BK; ++j)
+          if (j > lim) sv[j] = -INFINITY;
+      }
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
+#pragma unroll
+      for (int j = 0; j < BK; ++j) mx4[j & 3] = fmaxf(mx4[j & 3], sv[j]);
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      float scale_o = 1.f;
+      if (t == 0) {
+        m_ref = mx;
+      } else if (mx > m_ref + kRescale) {
+        scale_o = ex2(m_ref - mx);
+        l *= scale_o;
+        m_ref = mx;
+      }
+      float ps4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[BK / 2];
+#pragma unroll
+      for (int j = 0; j < BK; j += 2) {
+        const float e0 = ex2(sv[j] - m_ref), e1 = ex2(sv[j + 1] - m_ref);   // ex2(-inf) = 0
+        ps4[(j >> 1) & 3] += e0 + e1;
+        pk[j / 2] = pack2(e0, e1);
+      }
+      l += (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
+      if (t > 0) {
+        ptx::mbar_wait(o_done, (t - 1) & 1);       // PV_{t-1} retired: P buffer free, O stable
+        ptx::tc_fence_after();
+        if (scale_o != 1.f) {
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(tmem_o + lane_off + c * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * scale_o);
+            ptx::tmem_st_32x32b_x32(tmem_o + lane_off + c * 32, o);
+          }
+          ptx::tmem_st_wait();
+        }
+      }
+      // P row -> K-major SWIZZLE_128B tile: chunk (8 keys) c of row r at (c ^ (r & 7)) within
+      // its 64-key chunk
+#pragma unroll
+      for (int c = 0; c < BK / 8; ++c) {
+        uint4* dst = reinterpret_cast<uint4*>(sP + (c >> 3) * QCH + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+        *dst = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+    }
+    ptx::mbar_wait(o_final, 0);
+    ptx::tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.o);
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t o[32];
+      ptx::tmem_ld_32x32b_x32(tmem_o + lane_off + c * 32, o);
+      ptx::tmem_ld_wait();
+      if (qi < L) {
+        uint4* dst = reinterpret_cast<uint4*>(O + (size_t)(row0 + qi) * p.d + h * DH + c * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack2(__uint_as_float(o[8 * j]) * inv, __uint_as_float(o[8 * j + 1]) * inv),
+                              pack2(__uint_as_float(o[8 * j + 2]) * inv, __uint_as_float(o[8 * j + 3]) * inv),
+                              pack2(__uint_as_float(o[8 * j + 4]) * inv, __uint_as_float(o[8 * j + 5]) * inv),
+                              pack2(__uint_as_float(o[8 * j + 6]) * inv, __uint_as_float(o[8 * j + 7]) * inv));
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<(2 * BK + DH <= 256 ? 256 : 512)>(tmem);
+}
+
 // ------------------------------------------------------------------ SIMT fallback
 template <typename T>
 __device__ __forceinline__ float ldf(const T* p);
@@ -300,6 +529,39 @@ __global__ void __launch_bounds__(128) prefill_attn_simt_kernel(const PrefillAtt
 }  // namespace
 
 bool prefill_attn_mma_supported(int dtype, int dh) { return dtype == 0 && (dh == 128 || dh == 64); }
+
+bool prefill_attn_tc_enabled() {   // read per call so tests can switch paths
+  const char* e = std::getenv("HC_PREFILL_TC");
+  return !e || std::atoi(e) != 0;
+}
+
+int prefill_attn_tc_keys() {   // keys per tile of the tcgen05 kernel (A/B knob HC_PREFILL_BK)
+  const char* e = std::getenv("HC_PREFILL_BK");
+  return e && std::atoi(e) == 128 ? 128 : 64;
+}
+
+template <int DH, int BK>
+static cudaError_t launch_tc(const PrefillAttnParams& p, const CUtensorMap& tq, const CUtensorMap& tkv,
+                             cudaStream_t s) {
+  constexpr int NCH = DH / 64;
+  constexpr int smem = NCH * 128 * 128 + 4 * NCH * BK * 128 + (BK / 64) * 128 * 128 + 128;
+  static const cudaError_t a =
+      cudaFuncSetAttribute(prefill_attn_tc_kernel<DH, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (a != cudaSuccess) return a;
+  prefill_attn_tc_kernel<DH, BK><<<dim3(p.n_qtiles, p.H), 192, smem, s>>>(tq, tkv, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_q, const void* tmap_kv,
+                                   cudaStream_t s) {
+  if (p.n_qtiles <= 0) return cudaSuccess;
+  const CUtensorMap& tq = *static_cast<const CUtensorMap*>(tmap_q);
+  const CUtensorMap& tkv = *static_cast<const CUtensorMap*>(tmap_kv);
+  const int bk = prefill_attn_tc_keys();
+  if (p.dh == 128) return bk == 128 ? launch_tc<128, 128>(p, tq, tkv, s) : launch_tc<128, 64>(p, tq, tkv, s);
+  if (p.dh == 64) return bk == 128 ? launch_tc<64, 128>(p, tq, tkv, s) : launch_tc<64, 64>(p, tq, tkv, s);
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStream_t s) {
   if (p.n_qtiles <= 0) return cudaSuccess;

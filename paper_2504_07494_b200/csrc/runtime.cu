@@ -175,8 +175,8 @@ struct hc_pool {
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_ids;
   std::unordered_map<int64_t, Req> reqs;
   CUtensorMap tmap_x{}, tmap_w{}, tmap_w_half{};
-  CUtensorMap tmap_wqkv{}, tmap_wo{};
-  CUtensorMap tmap_x64{};               // pool rows, {64 x min(B,64)} boxes (absorbed Z GEMM)   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
+  CUtensorMap tmap_wqkv{}, tmap_wo{};   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
+  CUtensorMap tmap_x64{};               // pool rows, {64 x min(B,64)} boxes (absorbed Z GEMM)
   bool tc_ok = false;
   bool dense_tc_ok = false;             // bf16 tcgen05 path for the current-token / output GEMMs
   int num_sms = 148;
@@ -1064,11 +1064,19 @@ struct PrefillPlan {
   int32_t n_qtiles = 0;
   size_t off_q, off_kv, off_o, off_rowdst, off_row0, off_treq, off_tq0, total;
 };
+// query rows per prefill attention tile: 128 on the tcgen05 kernel, 64 on the mma.sync one
+bool prefill_uses_tc(const hc_pool* pool) {
+  return prefill_attn_tc_enabled() && prefill_attn_mma_supported(pool->cfg.dtype, pool->cfg.head_dim) &&
+         !(pool->cfg.flags & HC_FLAG_FORCE_SIMT);
+}
+int prefill_tile_rows(const hc_pool* pool) { return prefill_uses_tc(pool) ? 128 : 64; }
+
 PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens) {
   PrefillPlan P;
+  const int tq = prefill_tile_rows(pool);
   for (int32_t i = 0; i < n_req; ++i) {
     P.rows += lens[i];
-    P.n_qtiles += (int32_t)cdiv(lens[i], 64);
+    P.n_qtiles += (int32_t)cdiv(lens[i], tq);
   }
   const size_t e = pool->elem, d = (size_t)pool->cfg.d_model;
   size_t o = 0;
@@ -1155,7 +1163,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
         rowdst[4 * r] = rowdst[4 * r + 1] = -1;
       }
     }
-    for (int32_t t0 = 0; t0 < lens[i]; t0 += 64, ++nt) {
+    for (int32_t t0 = 0; t0 < lens[i]; t0 += prefill_tile_rows(pool), ++nt) {
       treq[nt] = i;
       tq0[nt] = t0;
     }
@@ -1163,6 +1171,15 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
       AppendReq a = ar[i];          // lens >= 1: ar[i] is request i
       a.row_off = row0[i];          // x rows of request i
       har.push_back(a);
+    }
+  }
+  {  // causal work grows with the tile's position: launch the longest tiles first
+    std::vector<std::pair<int32_t, int32_t>> tl(nt);
+    for (int32_t k = 0; k < nt; ++k) tl[k] = {tq0[k], treq[k]};
+    std::stable_sort(tl.begin(), tl.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    for (int32_t k = 0; k < nt; ++k) {
+      tq0[k] = tl[k].first;
+      treq[k] = tl[k].second;
     }
   }
   row0[n_req] = (int32_t)r;
@@ -1218,7 +1235,15 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   pa.dh = dh;
   pa.d = d;
   pa.scale_log2 = scale * 1.4426950408889634f;
-  err = launch_prefill_attn(pa, pool->cfg.dtype, s);
+  if (prefill_uses_tc(pool)) {
+    CUtensorMap tq, tkv;
+    if (!make_tmap_2d(&tq, ws + P.off_q, (uint64_t)d, (uint64_t)P.rows, 64, 128) ||
+        !make_tmap_2d(&tkv, ws + P.off_kv, 2 * (uint64_t)d, (uint64_t)P.rows, 64, (uint32_t)prefill_attn_tc_keys()))
+      return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (prefill attention)");
+    err = launch_prefill_attn_tc(pa, &tq, &tkv, s);
+  } else {
+    err = launch_prefill_attn(pa, pool->cfg.dtype, s);
+  }
   if (err != cudaSuccess) return cuda_fail(err, "prefill attention kernel");
   ++launches;
   st = hc_output_projection(pool, (int32_t)P.rows, ws + P.off_o, y, stream);

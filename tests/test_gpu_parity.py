@@ -358,15 +358,20 @@ PREFILL_CASES = [
     ("bf16-256", (256, 2, 128, 16), [1, 63, 64, 65, 200, 513]),
     ("bf16-512", (512, 4, 128, 16), [130, 7, 64, 300]),
     ("bf16-dh64", (512, 8, 64, 32), [1, 65, 129]),
+    ("bf16-long", (512, 4, 128, 16), [1, 127, 128, 129, 700, 1500]),     # many 128-query tiles
+    ("bf16-dh64-long", (512, 8, 64, 32), [255, 256, 257, 1031]),
 ]
 
 
+@pytest.mark.parametrize("prefill_tc", ["1", "0"])
 @pytest.mark.parametrize("name,shape,lens", PREFILL_CASES)
-def test_prefill_layer_vs_oracle(hc, name, shape, lens):
+def test_prefill_layer_vs_oracle(hc, monkeypatch, name, shape, lens, prefill_tc):
     """Prefill of new requests: every output row against oracle.prefill_layer, then a decode
     over the freshly written caches against the oracle (KV rows written by the projection
-    GEMM's epilogue; hidden rows = x)."""
+    GEMM's epilogue; hidden rows = x).  prefill_tc: the tcgen05 attention kernel (default)
+    and the mma.sync one (HC_PREFILL_TC=0) meet the same bar."""
     from oracle import hc_oracle as O
+    monkeypatch.setenv("HC_PREFILL_TC", prefill_tc)
     if shape is None:
         w = C.tiny(bias=True)
         tol = TOL_F32
