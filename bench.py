@@ -220,7 +220,9 @@ def cpu_baseline(w, budget_s: float = 20.0):
     per_req = (1 - frac_h) * (t_kv / max(1, n_kv)) + frac_h * (t_h / max(1, n_h))
     cores = max([tp.get("num_threads", 1) for tp in threadpool_info()] + [1])
     return {"value": 1.0 / per_req if per_req > 0 else 0.0, "unit": "req-layers/s", "cores": cores,
-            "kind": "oracle",
+            "kind": "oracle", "extrapolated": True,
+            "kv_req_layers_per_s": n_kv / t_kv if t_kv > 0 else None,
+            "hidden_req_layers_per_s": n_h / t_h if t_h > 0 else None,
             "sample": f"{n_kv} KV + {n_h} hidden requests of {w.name} (seed 99, full heads, fp64 numpy), "
                       f"{t_used:.1f} s; value = 1 / (mix-weighted mean time per request)"}
 
@@ -310,18 +312,21 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
         step()
-    e1.record(stream)
+        evs[i + 1].record(stream)   # per-step boundaries (for percentiles; no sync inside)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     kt = pool.kernel_times()
     pool.set_profiling(False)
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = evs[0].elapsed_time(evs[-1]) / args.steps
+    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    pct = {"p10": per_step[int(0.1 * (len(per_step) - 1))], "p50": statistics.median(per_step),
+           "p90": per_step[int(0.9 * (len(per_step) - 1))]}
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -414,9 +419,10 @@ def main():
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
         peak = tf_sus
-        roof = {"bound": "tensor", "kernel": "fused_step_kernel<4,2>" if fused else "recon_tc2_kernel<2,4>",
+        roof = {"bound": "tensor", "kernel": "fused_step_kernel<3,4,2>" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
                 "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get(dom),
+                "ncu_tensor_pipe_pct": TRAFFIC.get(w.name, {}).get(dom + "_tensor_pipe_pct"),
                 "peak_kind": "bf16 sustained, " + peak_src}
     else:
         peak = hbm
@@ -426,7 +432,7 @@ def main():
     T_roof = max(F_alg / (tf_sus * 1e12), B_alg / (hbm * 1e9))
     line = {
         "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms, "step_ms_percentiles": pct, "higher_is_better": True,
         "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
