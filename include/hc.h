@@ -95,6 +95,16 @@ typedef struct {
    * Callers of hc_decode_attention pass q already rotated.  Requires the bf16 tcgen05 path
    * and head_dim % 64 == 0 (HC_E_UNSUPPORTED otherwise). */
   float rope_theta;
+  /* Optional pre-attention LayerNorm of the layer input (OPT; the
+   * paper's Eq. 1 multiplies the layer input directly and specifies none, DESIGN R4/R15):
+   * ln_gamma nullable device [d] fp32 (NULL = no LayerNorm), ln_beta nullable device [d]
+   * fp32 (NULL = 0), ln_eps.  Copied at create.  With it, hc_decode_layer and
+   * hc_prefill_layer normalise x before the projections, and the hidden cache holds the
+   * normalised vector u = LN(x) — the exact vector Eq. 1 multiplies — so reconstruction
+   * needs no extra work (DESIGN R15). */
+  const float* ln_gamma;
+  const float* ln_beta;
+  float ln_eps;
 } hc_pool_config;
 
 /* Bytes of device storage a pool with this config needs: the unit blocks, the
@@ -163,10 +173,14 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
  * Needs the pool's w_q.  Asynchronous on `stream`. */
 hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
                             const void* x, void* q_out, void* stream);
+/* u = LN(x) with the pool's ln_gamma / ln_beta / ln_eps (population variance over d,
+ * fp32 statistics): x, u device [n_rows, d] pool dtype (may alias).  HC_E_UNSUPPORTED if
+ * the pool has no LayerNorm.  hc_project_append takes the normalised input. */
+hc_status hc_layer_norm(hc_pool* pool, int32_t n_rows, const void* x, void* u, void* stream);
 /* y = W_O o (+ b_O): the output map of Eq. 3.  o, y device [n_req, d]. */
 hc_status hc_output_projection(hc_pool* pool, int32_t n_req, const void* o, void* y, void* stream);
-/* One attention layer for one decode step: hc_project_append, hc_decode_attention,
- * hc_output_projection in sequence.  `workspace` >= hc_layer_workspace_size() bytes,
+/* One attention layer for one decode step: [hc_layer_norm,] hc_project_append,
+ * hc_decode_attention, hc_output_projection in sequence.  `workspace` >= hc_layer_workspace_size() bytes,
  * sized for the batch AFTER the current token is appended (unknown ids count as n = 1).
  * lse (nullable) as hc_decode_attention. */
 size_t hc_layer_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes);

@@ -142,16 +142,31 @@ def head_output(q_h, X, W_K_h, W_V_h, scale: float, b_K_h=None, b_V_h=None):
     return o, l[0]
 
 
+def layer_norm(X, gamma, beta=None, eps: float = 1e-5):
+    """Pre-attention LayerNorm of OPT-style layers (the paper's Eq. 1
+    specifies none, DESIGN R4/R15): per row, (x - mean) / sqrt(var + eps) * gamma + beta
+    with the population variance over the d features."""
+    X = _f64(X)
+    mu = X.mean(axis=-1, keepdims=True)
+    var = ((X - mu) ** 2).mean(axis=-1, keepdims=True)
+    Y = (X - mu) / np.sqrt(var + eps) * _f64(gamma)
+    return Y + (0.0 if beta is None else _f64(beta))
+
+
 def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float,
-                    b_Q=None, b_KV=None, b_O=None, rope_theta: float = 0.0):
+                    b_Q=None, b_KV=None, b_O=None, rope_theta: float = 0.0, ln=None):
     """One attention layer for one decode step of one request (NEXT row f1):
     q = W_Q x_t (+b_Q) and, for the current token, k, v = W_K x_t, W_V x_t (+b)  (Eq. 1,
     P:121-125); the current token joins the context: KV mode appends (k, v) to
     the cached K, V; hidden mode appends x_t to the cached X and rebuilds K, V from all of X
     (P:269); then Eq. 2-3 with the output map y = W_O o (+b_O) (Eq. 3).
     cache = {'mode': 0, 'K': [n-1, d], 'V': [n-1, d]} or {'mode': 1, 'X': [n-1, d]}.
+    ln = (gamma, beta, eps) or None: the projections see u_t = LN(x_t), and a hidden cache
+    holds u (the vector Eq. 1 multiplies; reading R15) — cache['X'] rows are stored u's.
     Returns y [d], q [d], lse [H], and the context the attention saw (dict)."""
     x_t, W_Q, W_O = _f64(x_t), _f64(W_Q), _f64(W_O)
+    if ln is not None:
+        x_t = layer_norm(x_t[None, :], *ln)[0]
     W_KV = _f64(W_KV)
     d = x_t.shape[0]
     q = W_Q @ x_t + (0.0 if b_Q is None else _f64(b_Q))
@@ -175,12 +190,15 @@ def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float
 
 
 def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=None, b_O=None,
-                  rope_theta: float = 0.0):
+                  rope_theta: float = 0.0, ln=None):
     """Prefill of one request's L new tokens (NEXT row f3): q, k, v of every
     token (Eq. 1), then for each position i causal attention over tokens j <= i (Eq. 2-3,
     P:127-135: "attending to all of the preceding tokens and itself") and the output map.
-    Returns Y [L, d] and the K, V [L, d] the cache must hold (KV mode) — hidden mode caches X."""
+    Returns Y [L, d] and the K, V [L, d] the cache must hold (KV mode) — hidden mode caches X
+    (with ln = (gamma, beta, eps): every row is LN(x) first and the hidden cache holds it)."""
     X, W_Q, W_O = _f64(X), _f64(W_Q), _f64(W_O)
+    if ln is not None:
+        X = layer_norm(X, *ln)
     L, d = X.shape
     Q = X @ W_Q.T + (0.0 if b_Q is None else _f64(b_Q)[None, :])
     K, V = hidden_request_kv(X, W_KV, b_KV)

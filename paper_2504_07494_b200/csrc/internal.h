@@ -132,6 +132,9 @@ int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
+// u = (x - mean) / sqrt(var + eps) * gamma + beta per row of d (pre-attention LayerNorm, R15)
+cudaError_t launch_layer_norm(const void* x, void* u, const float* gamma, const float* beta, float eps, int rows,
+                              int d, int dtype, cudaStream_t s);
 
 // Causal self-attention over each request's new tokens (prefill / recompute, NEXT row f3).
 struct PrefillAttnParams {

@@ -141,4 +141,65 @@ cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ pre-attention LayerNorm
+// One CTA (256 threads) per row: two passes over the row (mean, then the centred second
+// moment — the population variance, as torch.nn.LayerNorm), fp32 statistics.
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// x and u may alias (each element is read before it is overwritten by the same thread)
+template <typename T>
+__global__ void __launch_bounds__(256) layer_norm_kernel(const T* x, T* u,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, float eps, int d) {
+  __shared__ float red[8];
+  const size_t row = blockIdx.x;
+  const T* xr = x + row * d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto block_sum = [&](float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    return t;
+  };
+  float s = 0.f;
+  for (int c = tid; c < d; c += 256) s += to_f(xr[c]);
+  const float mean = block_sum(s) / d;
+  float q = 0.f;
+  for (int c = tid; c < d; c += 256) {
+    const float t = to_f(xr[c]) - mean;
+    q += t * t;
+  }
+  const float rstd = rsqrtf(block_sum(q) / d + eps);
+  T* ur = u + row * d;
+  for (int c = tid; c < d; c += 256) ur[c] = from_f<T>((to_f(xr[c]) - mean) * rstd * gamma[c] + beta[c]);
+}
+
+cudaError_t launch_layer_norm(const void* x, void* u, const float* gamma, const float* beta, float eps, int rows,
+                              int d, int dtype, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (dtype == 1)
+    layer_norm_kernel<float><<<rows, 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(u), gamma, beta,
+                                                  eps, d);
+  else
+    layer_norm_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                          static_cast<__nv_bfloat16*>(u), gamma, beta, eps, d);
+  return cudaGetLastError();
+}
+
 }  // namespace hc

@@ -58,8 +58,9 @@ struct Layout {  // storage layout
   size_t b_off, b_bytes;  // head-interleaved b_KV [2d] fp32
   size_t wo_off, bo_off;  // W_O [d,d], b_O [d] (when configured)
   size_t rope_off;        // RoPE inv_freq [dh/2] fp64 (when rope_theta > 0)
+  size_t ln_off;          // LayerNorm gamma [d] then beta [d] fp32 (when ln_gamma != NULL)
   size_t stage_off, total;
-  bool has_q, has_o;
+  bool has_q, has_o, has_ln;
 };
 
 bool layout_for(const hc_pool_config* c, Layout* L) {
@@ -71,6 +72,7 @@ bool layout_for(const hc_pool_config* c, Layout* L) {
   const size_t d = (size_t)c->d_model;
   L->has_q = c->w_q != nullptr;
   L->has_o = c->w_o != nullptr;
+  L->has_ln = c->ln_gamma != nullptr;
   L->blocks_off = 0;
   L->blocks_bytes = (size_t)c->num_blocks * c->block_size * d * e;
   L->wq_off = align_up(L->blocks_off + L->blocks_bytes, 1024);
@@ -90,6 +92,11 @@ bool layout_for(const hc_pool_config* c, Layout* L) {
   if (c->rope_theta > 0.f) {
     L->rope_off = o;
     o = align_up(o + (size_t)c->head_dim / 2 * sizeof(double), kAlign);
+  }
+  L->ln_off = 0;
+  if (L->has_ln) {
+    L->ln_off = o;
+    o = align_up(o + 2 * d * sizeof(float), kAlign);
   }
   L->stage_off = align_up(o, kAlign);
   L->total = align_up(L->stage_off + kStagingBytes, kAlign);
@@ -363,6 +370,7 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     return fail(HC_E_UNSUPPORTED, "num_blocks * block_size must fit in int32");
   const bool accounting = (cfg->flags & HC_FLAG_ACCOUNTING_ONLY) != 0;
   if (cfg->rope_theta < 0.f) return fail(HC_E_INVALID, "rope_theta < 0");
+  if (cfg->ln_gamma && !(cfg->ln_eps >= 0.f)) return fail(HC_E_INVALID, "ln_eps < 0");
   if (cfg->rope_theta > 0.f &&
       (cfg->dtype != HC_BF16 || (cfg->flags & HC_FLAG_FORCE_SIMT) || cfg->head_dim % 64 != 0 ||
        !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size) ||
@@ -413,6 +421,12 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     if (err == cudaSuccess && L.has_o)
       err = cfg->b_o ? cudaMemcpy(p->storage + L.bo_off, cfg->b_o, dbytes, cudaMemcpyDeviceToDevice)
                      : cudaMemset(p->storage + L.bo_off, 0, dbytes);
+    if (err == cudaSuccess && L.has_ln) {
+      err = cudaMemcpy(p->storage + L.ln_off, cfg->ln_gamma, dbytes, cudaMemcpyDeviceToDevice);
+      if (err == cudaSuccess)
+        err = cfg->ln_beta ? cudaMemcpy(p->storage + L.ln_off + dbytes, cfg->ln_beta, dbytes, cudaMemcpyDeviceToDevice)
+                           : cudaMemset(p->storage + L.ln_off + dbytes, 0, dbytes);
+    }
     if (err == cudaSuccess && cfg->rope_theta > 0.f) {
       std::vector<double> inv(cfg->head_dim / 2);
       for (int c = 0; c < cfg->head_dim / 2; ++c)
@@ -976,6 +990,23 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   return HC_OK;
 }
 
+hc_status hc_layer_norm(hc_pool* pool, int32_t n_rows, const void* x, void* u, void* stream) {
+  if (!pool) return fail(HC_E_INVALID, "pool is null");
+  pool->last_launches = 0;
+  if (n_rows < 0) return fail(HC_E_INVALID, "n_rows < 0");
+  if (n_rows == 0) return HC_OK;
+  if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
+  if (!pool->L.has_ln) return fail(HC_E_UNSUPPORTED, "pool was created without ln_gamma");
+  if (!x || !u) return fail(HC_E_INVALID, "x / u is null");
+  DeviceGuard g(pool->cfg.device);
+  const float* gb = reinterpret_cast<const float*>(pool->storage + pool->L.ln_off);
+  cudaError_t err = launch_layer_norm(x, u, gb, gb + pool->cfg.d_model, pool->cfg.ln_eps, n_rows, pool->cfg.d_model,
+                                      pool->cfg.dtype, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "layer norm kernel");
+  pool->last_launches = 1;
+  return HC_OK;
+}
+
 hc_status hc_output_projection(hc_pool* pool, int32_t n_req, const void* o, void* y, void* stream) {
   if (!pool) return fail(HC_E_INVALID, "pool is null");
   pool->last_launches = 0;
@@ -1028,7 +1059,7 @@ size_t hc_layer_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t
     rs[i] = &tmp[i];
   }
   const size_t qa = align_up((size_t)n_req * pool->cfg.d_model * pool->elem, kAlign);
-  return 2 * qa + pool->plan(rs).total;
+  return (pool->L.has_ln ? 3 : 2) * qa + pool->plan(rs).total;
 }
 
 hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
@@ -1045,10 +1076,20 @@ hc_status hc_decode_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, 
   if (!y) return fail(HC_E_INVALID, "y is null");
   const size_t qa = align_up((size_t)n_req * pool->cfg.d_model * pool->elem, kAlign);
   char* ws = static_cast<char*>(workspace);
-  hc_status st = hc_project_append(pool, n_req, req_ids, modes, x, ws, stream);
+  // workspace: q | o | [u = LN(x)] | attention workspace
+  const size_t pre = (pool->L.has_ln ? 3 : 2) * qa;
+  int launches = 0;
+  hc_status st;
+  if (pool->L.has_ln) {
+    st = hc_layer_norm(pool, n_req, x, ws + 2 * qa, stream);
+    if (st != HC_OK) return st;
+    x = ws + 2 * qa;
+    launches = 1;
+  }
+  st = hc_project_append(pool, n_req, req_ids, modes, x, ws, stream);
   if (st != HC_OK) return st;
-  int launches = pool->last_launches;
-  st = hc_decode_attention(pool, n_req, req_ids, ws, scale, ws + qa, lse, ws + 2 * qa, ws_bytes - 2 * qa, stream);
+  launches += pool->last_launches;
+  st = hc_decode_attention(pool, n_req, req_ids, ws, scale, ws + qa, lse, ws + pre, ws_bytes - pre, stream);
   if (st != HC_OK) return st;
   launches += pool->last_launches;
   st = hc_output_projection(pool, n_req, ws + qa, y, stream);
@@ -1062,7 +1103,7 @@ namespace {
 struct PrefillPlan {
   int64_t rows = 0;
   int32_t n_qtiles = 0;
-  size_t off_q, off_kv, off_o, off_rowdst, off_row0, off_treq, off_tq0, total;
+  size_t off_q, off_kv, off_o, off_u, off_rowdst, off_row0, off_treq, off_tq0, total;
 };
 // query rows per prefill attention tile: 128 on the tcgen05 kernel, 64 on the mma.sync one
 bool prefill_uses_tc(const hc_pool* pool) {
@@ -1086,6 +1127,8 @@ PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens
   o = align_up(o + P.rows * 2 * d * e, kAlign);
   P.off_o = o;
   o = align_up(o + P.rows * d * e, kAlign);
+  P.off_u = o;   // LN(x) when the pool has a LayerNorm
+  o = align_up(o + (pool->L.has_ln ? P.rows * d * e : 0), kAlign);
   P.off_rowdst = o;
   o = align_up(o + P.rows * 4 * sizeof(int32_t), kAlign);
   P.off_row0 = o;
@@ -1191,6 +1234,13 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   cudaEventRecord(pin->ev, s);
   pin->pending = true;
   int launches = 0;
+  if (pool->L.has_ln) {   // u = LN(x): the projections' input and what the hidden cache holds (R15)
+    const float* gb = reinterpret_cast<const float*>(pool->storage + pool->L.ln_off);
+    err = launch_layer_norm(x, ws + P.off_u, gb, gb + d, pool->cfg.ln_eps, (int32_t)P.rows, d, pool->cfg.dtype, s);
+    if (err != cudaSuccess) return cuda_fail(err, "layer norm kernel");
+    x = ws + P.off_u;
+    ++launches;
+  }
   if (!har.empty()) {
     st = scatter_rows(pool, har, tabs, nullptr, nullptr, x, stream);   // hidden mode: cache x itself
     if (st != HC_OK) return st;

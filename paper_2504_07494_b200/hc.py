@@ -39,6 +39,7 @@ class PoolConfig(ctypes.Structure):
         ("split_tokens", ctypes.c_int32),
         ("w_q", ctypes.c_void_p), ("b_q", ctypes.c_void_p), ("w_o", ctypes.c_void_p), ("b_o", ctypes.c_void_p),
         ("rope_theta", ctypes.c_float),
+        ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
     ]
 
 
@@ -76,6 +77,7 @@ def _load() -> ctypes.CDLL:
         "hc_decode_attention": (I32, [P, I32, pI64, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
         "hc_project_append": (I32, [P, I32, pI64, pI32, VP, VP, VP]),
         "hc_output_projection": (I32, [P, I32, VP, VP, VP]),
+        "hc_layer_norm": (I32, [P, I32, VP, VP, VP]),
         "hc_layer_workspace_size": (SZ, [P, I32, pI64, pI32]),
         "hc_decode_layer": (I32, [P, I32, pI64, pI32, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
         "hc_prefill_workspace_size": (SZ, [P, I32, pI32]),
@@ -172,6 +174,10 @@ def hc_project_append(h, req_ids, modes, x, q_out, stream=None) -> None:
     _check(lib.hc_project_append(h, len(req_ids), _i64(req_ids), _i32(modes), _ptr(x), _ptr(q_out), _stream(stream)))
 
 
+def hc_layer_norm(h, n_rows, x, u, stream=None) -> None:
+    _check(lib.hc_layer_norm(h, int(n_rows), _ptr(x), _ptr(u), _stream(stream)))
+
+
 def hc_output_projection(h, n_req, o, y, stream=None) -> None:
     _check(lib.hc_output_projection(h, int(n_req), _ptr(o), _ptr(y), _stream(stream)))
 
@@ -222,10 +228,12 @@ class HybridCachePool:
                  device: int = 0, flags: int = 0, split_tokens: int = 0,
                  w_q: Optional[torch.Tensor] = None, b_q: Optional[torch.Tensor] = None,
                  w_o: Optional[torch.Tensor] = None, b_o: Optional[torch.Tensor] = None,
-                 rope_theta: float = 0.0):
+                 rope_theta: float = 0.0, ln_gamma: Optional[torch.Tensor] = None,
+                 ln_beta: Optional[torch.Tensor] = None, ln_eps: float = 1e-5):
         self.cfg = PoolConfig(d_model, n_heads, head_dim, block_size, num_blocks, dtype, flags, None, 0,
                               None, None, device, split_tokens)
         self.cfg.rope_theta = float(rope_theta)
+        self.cfg.ln_eps = float(ln_eps)
         self.dtype = dtype
         self.tdtype = _TORCH_DT[dtype]
         self.d, self.H, self.dh, self.B = d_model, n_heads, head_dim, block_size
@@ -237,7 +245,9 @@ class HybridCachePool:
             for name, t, shape, dt in (("w_q", w_q, (d_model, d_model), self.tdtype),
                                        ("b_q", b_q, (d_model,), torch.float32),
                                        ("w_o", w_o, (d_model, d_model), self.tdtype),
-                                       ("b_o", b_o, (d_model,), torch.float32)):
+                                       ("b_o", b_o, (d_model,), torch.float32),
+                                       ("ln_gamma", ln_gamma, (d_model,), torch.float32),
+                                       ("ln_beta", ln_beta, (d_model,), torch.float32)):
                 if t is None:
                     continue
                 assert t.is_cuda and t.dtype == dt and tuple(t.shape) == shape, name
@@ -325,6 +335,13 @@ class HybridCachePool:
             q_out = torch.empty_like(x)
         hc_project_append(self.handle, req_ids, modes, x, q_out, stream)
         return q_out
+
+    def layer_norm(self, x, u=None, stream=None):
+        """u = LN(x) with the pool's pre-attention LayerNorm (hc_layer_norm)."""
+        if u is None:
+            u = torch.empty_like(x)
+        hc_layer_norm(self.handle, x.shape[0], x, u, stream)
+        return u
 
     def output_projection(self, o, y=None, stream=None):
         assert o.is_cuda and o.dtype == self.tdtype and o.is_contiguous() and o.shape[1] == self.d

@@ -137,6 +137,14 @@ class Workload:
         return rng.normal_tensor(self.seed, rng.STREAM_B, 2, [self.shape.d], 0.02, torch.float32, device) \
             if self.bias else None
 
+    def ln_gamma(self, device="cpu") -> torch.Tensor:
+        """Pre-attention LayerNorm scale [d] fp32: 1 + N(0, 0.1^2) (optional f1 component)."""
+        return rng.normal_tensor(self.seed, rng.STREAM_B, 3, [self.shape.d], 0.1, torch.float32, device) + 1.0
+
+    def ln_beta(self, device="cpu") -> torch.Tensor:
+        """Pre-attention LayerNorm shift [d] fp32: N(0, 0.02^2)."""
+        return rng.normal_tensor(self.seed, rng.STREAM_B, 4, [self.shape.d], 0.02, torch.float32, device)
+
     def x_t(self, i: int, device="cpu") -> torch.Tensor:
         """Layer input of request i's current token (attention-layer step), N(0,1)."""
         return rng.normal_tensor(self.seed, rng.STREAM_XT, self.req_ids[i], [self.shape.d], 1.0,

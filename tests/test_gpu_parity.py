@@ -556,3 +556,77 @@ def test_absorbed_unsupported_configs(hc):
         with pytest.raises(hc.HcError) as e:
             T.make_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN, **kw)   # RoPE / fp32
         assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+
+# ------------------------------------------------------------------ pre-attention LayerNorm (f1 option, R15)
+LN_CASES = [("tiny-f32", None), ("bf16-512", (512, 4, 128, 16)), ("bf16-dh64", (512, 8, 64, 32))]
+# A layer with LayerNorm stores one more bf16 vector (u = LN(x)) on the way to q, k, v than
+# the plain layer; its composed bar is 1.5e-2 (DESIGN reading R16).  fp32 keeps 1e-5.
+TOL_BF16_LN_LAYER = 1.5e-2
+
+
+def _ln_input(t):
+    """Layer inputs with a non-zero mean and a non-unit scale (so LN matters), made on the
+    host and copied to the device (the oracle reads the host copy)."""
+    return (t.float() * 2.5 + 1.0).to(t.dtype)
+
+
+@pytest.mark.parametrize("name,shape", LN_CASES)
+def test_layer_norm_and_decode_layer_with_ln(hc, name, shape):
+    from oracle import hc_oracle as O
+    if shape is None:
+        w, tol = C.tiny(bias=True), TOL_F32
+    else:
+        w, tol = _bf16_workload(*shape, n=[1, 40, 700, 129, 2], bias=True), TOL_BF16_LN_LAYER
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w, ln=True)
+    ln = T.ln_params(w)
+    xs = [_ln_input(w.x_t(i)) for i in range(len(w.n))]
+    x = torch.stack(xs).contiguous().to(dev)
+    # hc_layer_norm alone: every element within the storage precision of the fp64 LN
+    u = pool.layer_norm(x).float().cpu().numpy()
+    ref = O.layer_norm(torch.stack(xs), *ln)
+    assert np.abs(u - ref).max() <= (1e-5 if shape is None else 2e-2) * max(1.0, np.abs(ref).max())
+    T.fill(pool, T.prefix_workload(w))
+    y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
+    y = y.float().cpu().numpy()
+    for i in range(len(w.n)):
+        y_ref, _, _, _ = T.oracle_layer(w, i, ln=ln, x_t=xs[i])
+        assert O.max_rel_err(y[i][None], y_ref[None], w.shape.H) <= tol, (name, i)
+
+
+@pytest.mark.parametrize("name,shape", LN_CASES)
+def test_prefill_with_ln_then_decode(hc, name, shape):
+    """Prefill with LN: outputs against the oracle, then a decode over the written caches —
+    hidden caches hold u = LN(x), KV caches hold W_KV u (+b)."""
+    from oracle import hc_oracle as O
+    if shape is None:
+        w, tol = C.tiny(bias=True), TOL_F32
+    else:
+        w, tol = _bf16_workload(*shape, n=[65, 1, 300, 129], bias=True, seed=17), TOL_BF16_LN_LAYER
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w, ln=True)
+    ln = T.ln_params(w)
+    X = [_ln_input(w.x(i)) for i in range(len(w.n))]
+    yp = pool.prefill_layer(w.req_ids, w.modes, w.n, torch.cat(X).contiguous().to(dev), w.scale)
+    yp = yp.float().cpu().numpy()
+    r = 0
+    for i in range(len(w.n)):
+        Y, _, _ = O.prefill_layer(X[i], w.w_q(), w.w_kv(), w.w_o(), w.shape.H, w.scale, w.b_q(), w.b_kv(),
+                                  w.b_o(), ln=ln)
+        assert O.max_rel_err(yp[r:r + w.n[i]], Y, w.shape.H) <= tol, (name, "prefill", i)
+        r += w.n[i]
+    out, _ = T.decode(pool, w, T.queries(w))
+    for i in range(len(w.n)):
+        K, V = O.hidden_request_kv(O.layer_norm(X[i], *ln), w.w_kv(), w.b_kv())
+        ref, _ = O.attend(w.q(i).double().numpy(), K, V, w.shape.H, w.scale)
+        assert O.max_rel_err(out[i][None], ref[None], w.shape.H) <= tol, (name, "cache", i)
+
+
+def test_layer_norm_unconfigured_is_unsupported(hc):
+    w = _bf16_workload(512, 4, 128, 16, n=[3])
+    pool = T.make_layer_pool(w)
+    with pytest.raises(hc.HcError) as e:
+        pool.layer_norm(torch.zeros(2, 512, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.status == hc.HC_E_UNSUPPORTED

@@ -327,3 +327,47 @@ def test_rope_hidden_equals_rotated_kv_twin():
     oh, lh = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.3, rope_theta=theta)
     ok, lk = O.decode_batch([{"mode": 0, "q": q, "K": Kr, "V": V}], W, H, 0.3)
     assert np.allclose(oh, ok, atol=1e-13) and np.allclose(lh, lk, atol=1e-13)
+
+
+# ---------------------------------------------------------------- pre-attention LayerNorm (f1 option)
+def test_layer_norm_matches_torch_and_is_shift_invariant():
+    """LN against torch.nn.functional.layer_norm in float64 (library routine); exact
+    invariance to adding a constant to a row; gamma = 1, beta = 0 gives mean 0 and
+    variance var / (var + eps) per row."""
+    rs = np.random.default_rng(5)
+    X = rs.normal(size=(7, 48)) * 3.0 + 2.0
+    g, b = 1 + 0.1 * rs.normal(size=48), 0.02 * rs.normal(size=48)
+    ref = torch.nn.functional.layer_norm(torch.from_numpy(X), (48,), torch.from_numpy(g), torch.from_numpy(b), 1e-5)
+    assert np.allclose(O.layer_norm(X, g, b, 1e-5), ref.numpy(), rtol=0, atol=1e-12)
+    assert np.allclose(O.layer_norm(X + 5.0, g, b), O.layer_norm(X, g, b), rtol=0, atol=1e-12)
+    U = O.layer_norm(X, np.ones(48), None, 1e-5)
+    var = X.var(axis=1)
+    assert np.allclose(U.mean(axis=1), 0, atol=1e-12)
+    assert np.allclose(U.var(axis=1), var / (var + 1e-5), rtol=1e-12)
+
+
+def test_layer_with_ln_is_layer_on_normalised_input():
+    """attention_layer / prefill_layer with ln = the same layers fed LN(x) (the hidden cache
+    holds u = LN(x), reading R15), for both cache modes."""
+    rs = np.random.default_rng(6)
+    d, H, n = 32, 2, 9
+    Wq, Wkv, Wo = rs.normal(size=(d, d)) / 6, rs.normal(size=(2 * d, d)) / 6, rs.normal(size=(d, d)) / 6
+    g, b = 1 + 0.1 * rs.normal(size=d), 0.02 * rs.normal(size=d)
+    X = rs.normal(size=(n, d)) * 2 + 1
+    ln = (g, b, 1e-5)
+    U = O.layer_norm(X, *ln)
+    for mode in (0, 1):
+        if mode == 1:
+            cache = {"mode": 1, "X": U[:-1]}
+        else:
+            KV = U[:-1] @ Wkv.T
+            cache = {"mode": 0, "K": KV[:, :d], "V": KV[:, d:]}
+        y1, q1, l1, _ = O.attention_layer(X[-1], cache, Wq, Wkv, Wo, H, 0.25, ln=ln)
+        y2, q2, l2, _ = O.attention_layer(U[-1], cache, Wq, Wkv, Wo, H, 0.25)
+        assert np.array_equal(y1, y2) and np.array_equal(l1, l2)
+    Y1, _, _ = O.prefill_layer(X, Wq, Wkv, Wo, H, 0.25, ln=ln)
+    Y2, _, _ = O.prefill_layer(U, Wq, Wkv, Wo, H, 0.25)
+    assert np.array_equal(Y1, Y2)
+    # and the LN really changes the layer for this input
+    Y3, _, _ = O.prefill_layer(X, Wq, Wkv, Wo, H, 0.25)
+    assert np.abs(Y1 - Y3).max() > 1e-3
