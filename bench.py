@@ -246,6 +246,9 @@ def main():
     ap.add_argument("--absorb", action="store_true",
                     help="NON-PAPER variant (NEXT row f4 (ii)): hidden requests attend through "
                          "q~ = W_K^T q and W_V (sum a x) instead of rebuilding K/V")
+    ap.add_argument("--gather", action="store_true",
+                    help="N>1: all-gather every rank's out + lse over NCCL after each step, inside the "
+                         "timed region (north_star's output gather; not a data-path exchange)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -290,8 +293,21 @@ def main():
     ws = pool.workspace(ids)
     stream = torch.cuda.current_stream()
 
+    gather = args.gather and world > 1
+    if gather:
+        # every rank holds n_req rows in weak scaling; strong scaling pads to the max
+        n_max = torch.tensor([n_req], device="cuda")
+        dist.all_reduce(n_max, op=dist.ReduceOp.MAX)
+        n_max = int(n_max.item())
+        send = torch.zeros((n_max, w.shape.d + 2 * w.shape.H), dtype=torch.float32, device="cuda")
+        recv = torch.empty((world * n_max, send.shape[1]), dtype=torch.float32, device="cuda")
+
     def step():
         hc.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, stream)
+        if gather:
+            send[:n_req, :w.shape.d].copy_(out)
+            send[:n_req, w.shape.d:w.shape.d + w.shape.H].copy_(lse)
+            dist.all_gather_into_tensor(recv, send)
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -382,6 +398,12 @@ def main():
     d, s = w.shape.d, w.elem_bytes
     hbm = peaks["hbm_gbs"]
     tf_burst, tf_sus = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # the sustained (power-capped) peak for a step that ran capped, the burst peak when the
+    # SM clock held its maximum through the timed region (B200_PROFILING: burst vs sustained)
+    capped = not clocks or clocks.get("sm_mhz", 0) < 0.97 * (clocks.get("sm_max_mhz") or 1e9) \
+        or "sw_power_cap" in clocks.get("reasons", [])
+    tf_peak = tf_sus if capped else tf_burst
+    tf_kind = ("bf16 sustained (power-capped run), " if capped else "bf16 burst (clock held max), ") + peak_src
     fused = decode_path == 1
     absorbed = decode_path == 3
     if absorbed:
@@ -418,18 +440,18 @@ def main():
                 "peak": hbm, "unit": "GB/s", "frac": k["achieved"] / hbm, "traffic": None,
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
-        peak = tf_sus
+        peak = tf_peak
         roof = {"bound": "tensor", "kernel": "fused_step_kernel<3,4,2>" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
                 "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get(dom),
                 "ncu_tensor_pipe_pct": TRAFFIC.get(w.name, {}).get(dom + "_tensor_pipe_pct"),
-                "peak_kind": "bf16 sustained, " + peak_src}
+                "peak_kind": tf_kind}
     else:
         peak = hbm
         roof = {"bound": "hbm", "kernel": "attn_pipe_kernel<128,8,3>", "achieved": k["achieved"], "peak": peak,
                 "unit": "GB/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get("attention"),
                 "peak_kind": "HBM copy, " + peak_src}
-    T_roof = max(F_alg / (tf_sus * 1e12), B_alg / (hbm * 1e9))
+    T_roof = max(F_alg / (tf_peak * 1e12), B_alg / (hbm * 1e9))
     line = {
         "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "step_ms_percentiles": pct, "higher_is_better": True,
@@ -438,6 +460,7 @@ def main():
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
+                   "output_gather": "NCCL all-gather of out+lse every step (timed)" if gather else "none",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
                    "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
                    else "paper (hidden K/V rebuilt every step)"},
