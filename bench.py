@@ -259,6 +259,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("HC_BENCH_ONE_GPU"):
+        # test hook: every rank on device 0 (exercises the N>1 control path on a 1-GPU box;
+        # use with HC_BENCH_BACKEND=gloo — NCCL refuses two ranks on one GPU)
+        local = 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.mode != "decode":
@@ -275,7 +279,11 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     w0 = workload_from(args.config)
     if args.strong:
         from synth.partition import strong_shard
@@ -460,7 +468,7 @@ def main():
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
-                   "output_gather": "NCCL all-gather of out+lse every step (timed)" if gather else "none",
+                   "output_gather": f"{dist.get_backend()} all-gather of out+lse every step (timed)" if gather else "none",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
                    "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
                    else "paper (hidden K/V rebuilt every step)"},
