@@ -91,7 +91,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sms, smax, reasons = [], None, set()
+        sms, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -102,13 +102,17 @@ class ClockSampler:
                 smax = float(f[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for nm, val in zip(names, f[5:9]):
                 if val.lower() in ("active", "1", "yes"):
                     reasons.add(nm)
         if not sms:
             return None
         return {"sm_mhz": statistics.median(sms), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms), "power_w": statistics.median(pw) if pw else None}
 
 
 # ============================================================================ reference arm

@@ -166,6 +166,11 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   ap_.gemm_tile_n = PC::TILE_N;
   // 3-stage GEMM ring + 4 attention warps x 2 stages (measured best of {3,4,2}, {3,3,3},
   // {2,6,2}, {2,4,3}: two GEMM stages starve the tensor cores).
+  const char* e = std::getenv("HC_FUSED_CFG");   // A/B knob
+  const int cfg = e ? std::atoi(e) : 342;
+  if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
 }
 
