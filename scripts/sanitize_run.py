@@ -26,5 +26,20 @@ run(w, flags=hc.HC_FLAG_GENERIC_ATTN)
 shape64 = LayerShape("san64", 512, 8, 64)
 w64 = Workload("san-bf16-dh64", shape64, 32, "bf16", 6, n, [0, 1, 0, 1, 1, 0, 1], list(range(len(n))), False)
 run(w64)
+# absorbed hidden attention (f4 ii): tcgen05 score / Z kernels, P rescale, q~ / W_V GEMMs
+run(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+run(w64, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+# decode layer + prefill (tcgen05 prefill attention) with LayerNorm and RoPE
+from oracle import hc_oracle as O
+dev = torch.device("cuda", 0)
+for ln, rope in ((True, 0.0), (False, 10000.0)):
+    wl = Workload("san-layer", shape, 16, "bf16", 7, [1, 40, 130, 300], [0, 1, 0, 1], [0, 1, 2, 3], True)
+    pool = T.make_layer_pool(wl, ln=ln, rope_theta=rope)
+    x = torch.cat([wl.x(i, device=dev) for i in range(len(wl.n))]).contiguous()
+    y = pool.prefill_layer(wl.req_ids, wl.modes, wl.n, x, wl.scale)
+    xt = torch.stack([wl.x_t(i, device=dev) for i in range(len(wl.n))]).contiguous()
+    y2, _ = pool.decode_layer(wl.req_ids, wl.modes, xt, wl.scale)
+    torch.cuda.synchronize()
+    print("layer ln", ln, "rope", rope, "finite", bool(torch.isfinite(y).all() and torch.isfinite(y2).all()), flush=True)
 torch.cuda.synchronize()
 print("done")
