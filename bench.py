@@ -551,18 +551,31 @@ def run_module_mode(args, rank, world, local):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    capped = not clocks or clocks.get("sm_mhz", 0) < 0.97 * (clocks.get("sm_max_mhz") or 1e9) \
+        or "sw_power_cap" in clocks.get("reasons", [])
+    peak = tf if capped else peaks["bf16_tflops"]
+    achieved = flops / (ms / 1e3) / 1e12
     line = {"metric": metric, "mode": args.mode, "value": n_layer / (ms / 1e3), "unit": unit, "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "dtype": w.dtype, "data": "synthetic", "config": {"workload": w.name, "d": d},
-            "tensor_TFLOPs": flops / (ms / 1e3) / 1e12, "frac_of_sustained_bf16": flops / (ms / 1e3) / 1e12 / tf,
-            "gpu_launches_per_step": pool.last_launch_count()}
+            "roofline": {"bound": "tensor", "kernel": "whole layer (projection GEMMs + attention)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "flops_per_step": flops,
+                         "peak_kind": ("bf16 sustained (power-capped run), " if capped
+                                       else "bf16 burst (clock held max), ") + peak_src},
+            "tensor_TFLOPs": achieved, "frac_of_sustained_bf16": achieved / tf,
+            "gpu_launches_per_step": pool.last_launch_count(), "clocks": clocks}
     print(json.dumps(line), flush=True)
     return 0
 
