@@ -159,6 +159,17 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.l2_hint = 0;
   a.sync_w = 8;
   a.sync = (num_sms / 2 <= pg::kMaxSyncPairs) ? rp.sync_counter : nullptr;
+  if (rp.epi_attend) {   // hidden rows become partials in the GEMM epilogue: no hidden tasks
+    a.epi = pg::EPI_ATTEND;
+    a.hblk_req = rp.hblk_req;
+    a.reqs = rp.reqs;
+    a.q = static_cast<const __nv_bfloat16*>(rp.q);
+    a.part_ml = rp.part_ml;
+    a.part_acc = rp.part_acc;
+    a.scale_log2 = rp.scale_log2;
+    a.seg = rp.seg;
+    tile_done = nullptr;
+  }
   a.tile_done = tile_done;
   ap_.tile_done = tile_done;
   ap_.gemm_n_tiles = a.n_tiles;

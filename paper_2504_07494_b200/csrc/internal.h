@@ -69,9 +69,20 @@ struct ReconParams {
   void* scr_v;
   int32_t d, H, dh, B;
   int32_t* sync_counter;  // >= 32*num_sms zeroed ints (pair progress words)
-  const int32_t* hblk_pos;  // RoPE: token position of row 0 of each hidden block (nullable)
+  const int32_t* hblk_pos;  // token position of row 0 of each hidden block (RoPE / attend; nullable)
   const double* rope_inv;   // RoPE: inv_freq table [dh/2] (nullable = no RoPE)
+  // ---- fused reconstruct-and-attend (epi_attend): the GEMM epilogue turns each segment of
+  // `seg` tokens x head into a flash-decoding partial; rebuilt K/V never reach memory
+  bool epi_attend;
+  const int32_t* hblk_req;  // batch index of each hidden block's request
+  const ReqDesc* reqs;      // n, split_begin of every request
+  const void* q;            // [n_req, d]
+  float* part_ml;
+  float* part_acc;
+  float scale_log2;
+  int32_t seg;              // tokens per partial: min(B, 32)
 };
+bool recon_pair_mode(int B);   // the CTA-pair GEMM serves this block size (else the 1-SM kernel)
 
 struct AppendReq {
   int32_t mode;

@@ -53,13 +53,22 @@ struct TcArgs {
   __nv_bfloat16* kvbuf;    // EPI_PROJECT (prefill): also every row's head-interleaved K||V, [M, 2d]
   // RoPE (NEXT row f4): rotate K (and q) columns at each row's token position
   const double* rope_inv;  // nullable: inv_freq[c] = theta^(-2c/dh), c < dh/2
-  const int32_t* row_pos;  // EPI_SCRATCH: position of row 0 of each hidden block (lb * B)
+  const int32_t* row_pos;  // EPI_SCRATCH / EPI_ATTEND: position of row 0 of each hidden block (lb * B)
+  // EPI_ATTEND (fused reconstruct-and-attend)
+  const int32_t* hblk_req;  // batch index of each hidden block's request
+  const ReqDesc* reqs;
+  const __nv_bfloat16* q;   // [n_req, d]
+  float* part_ml;           // [task][2], task = split * H + head
+  float* part_acc;          // [task][dh]
+  float scale_log2;
+  int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
 constexpr int EPI_SCRATCH = 0;   // [K||V] rows -> scratch blocks [hblock][H][B][dh]
 constexpr int EPI_PROJECT = 1;   // cols [0,d): q row; cols [d,3d) (head-interleaved K||V) -> cache slot
 constexpr int EPI_DENSE = 2;     // plain row-major C
+constexpr int EPI_ATTEND = 3;    // [K||V] rows -> per-(segment, head) flash-decoding partials
 
 template <int NSUB, int NSTAGE>
 struct PairCfg {
@@ -180,6 +189,127 @@ __device__ __forceinline__ void store_chunk(const TcArgs& a, int n, const float 
     uint4* d4 = reinterpret_cast<uint4*>(dst2);
 #pragma unroll
     for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+  }
+}
+
+
+// ---- EPI_ATTEND: fused reconstruct-and-attend -------------------------------------------
+constexpr unsigned kFull = 0xffffffffu;
+
+// Butterfly reduce-scatter over the S lanes of a segment: on return lane i (= lane % S)
+// holds in x[0 .. 32/S) the segment sums of columns [i*32/S, (i+1)*32/S) of its chunk.
+template <int OFF, int CNT>
+struct SegReduceScatter {
+  static __device__ __forceinline__ void run(float* x, int lane) {
+    constexpr int HALF = CNT / 2;
+    const bool up = (lane & OFF) != 0;
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) {
+      const float send = up ? x[i] : x[i + HALF];
+      const float keep = up ? x[i + HALF] : x[i];
+      x[i] = keep + __shfl_xor_sync(kFull, send, OFF);
+    }
+    SegReduceScatter<OFF / 2, HALF>::run(x, lane);
+  }
+};
+template <int CNT>
+struct SegReduceScatter<0, CNT> {
+  static __device__ __forceinline__ void run(float*, int) {}
+};
+
+__device__ __forceinline__ float dot32_bf16(const float (&f)[32], const __nv_bfloat16* q) {
+  const uint4* q4 = reinterpret_cast<const uint4*>(q);
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 u = __ldg(q4 + j);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 v = __bfloat1622float2(b[e]);
+      s = fmaf(f[8 * j + 2 * e], v.x, s);
+      s = fmaf(f[8 * j + 2 * e + 1], v.y, s);
+    }
+  }
+  return s;
+}
+
+// One pair tile's rows -> partials.  Thread = GEMM row (a token of a hidden block); the
+// tile's columns are HT = TILE_N / (2 dh) heads of K_h || V_h.  Per head: s = scale *
+// q_h . k (bias and RoPE applied to k in registers), segment max / sum over the S lanes of
+// the segment, and the segment's sum_j p_j v_j by a butterfly reduce-scatter; lane i of the
+// segment writes dims [i*32/S, (i+1)*32/S) of every 32-column chunk.  Rows past M and
+// tokens past n get p = 0; a segment that starts past n writes nothing.
+template <int S, int TILE_N>
+__device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane) {
+  const bool valid = grow < a.M;
+  int req = 0, tok = 0, n = 0;
+  if (valid) {
+    const int g = grow / a.B;
+    req = a.hblk_req[g];
+    tok = a.row_pos[g] + (grow - g * a.B);
+    n = a.reqs[req].n;
+  }
+  const bool live = valid && tok < n;
+  const int tok0 = tok - (lane & (S - 1));   // first token of this lane's segment
+  const bool seg_live = valid && tok0 < n;
+  const int split = valid ? a.reqs[req].split_begin + tok0 / S : 0;
+  const int dh = a.dh, HT = TILE_N / (2 * dh);
+#pragma unroll 1
+  for (int j = 0; j < HT; ++j) {
+    const int h = nt * HT + j;
+    const int nk = nt * TILE_N + j * 2 * dh;      // interleaved column of K_h (bias index)
+    const uint32_t tk = tacc + j * 2 * dh;
+    const __nv_bfloat16* qh = a.q + (size_t)req * a.d + h * dh;
+    float s = 0.f;
+    if (a.rope_inv != nullptr) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < dh / 2; c0 += 32) {
+        float f[32], f2[32];
+        load_chunk(tk + c0, a.bias, nk + c0, f);
+        load_chunk(tk + c0 + dh / 2, a.bias, nk + c0 + dh / 2, f2);
+        rope_rotate(f, f2, tok, a.rope_inv + c0);
+        s += dot32_bf16(f, qh + c0) + dot32_bf16(f2, qh + c0 + dh / 2);
+      }
+    } else {
+#pragma unroll 1
+      for (int c0 = 0; c0 < dh; c0 += 32) {
+        float f[32];
+        load_chunk(tk + c0, a.bias, nk + c0, f);
+        s += dot32_bf16(f, qh + c0);
+      }
+    }
+    s = live ? s * a.scale_log2 : -INFINITY;
+    float m = s;
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    const float p = live ? exp2f(s - m) : 0.f;
+    float l = p;
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
+    const size_t task = (size_t)split * a.H + h;
+#pragma unroll 1
+    for (int c0 = 0; c0 < dh; c0 += 32) {
+      float f[32];
+      load_chunk(tk + dh + c0, a.bias, nk + dh + c0, f);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) f[e] *= p;
+      SegReduceScatter<S / 2, 32>::run(f, lane);
+      if (seg_live) {
+        float* dst = a.part_acc + task * dh + c0 + (lane & (S - 1)) * (32 / S);
+        if constexpr (S == 32) {
+          dst[0] = f[0];
+        } else if constexpr (S == 16) {
+          *reinterpret_cast<float2*>(dst) = make_float2(f[0], f[1]);
+        } else {
+          *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+        }
+      }
+    }
+    if (seg_live && (lane & (S - 1)) == 0) {
+      a.part_ml[2 * task] = m;
+      a.part_ml[2 * task + 1] = l;
+    }
   }
 }
 
@@ -352,6 +482,19 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       ptx::mbar_wait(&s.tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const int grow = mt * P_BM + row_in_tile;
+      if (a.epi == EPI_ATTEND) {
+        const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
+        if (a.seg == 8)
+          attend_tile<8, PC::TILE_N>(a, tacc, nt, grow, lane);
+        else if (a.seg == 16)
+          attend_tile<16, PC::TILE_N>(a, tacc, nt, grow, lane);
+        else
+          attend_tile<32, PC::TILE_N>(a, tacc, nt, grow, lane);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        continue;
+      }
       const bool valid = grow < a.M;
       const int g = grow / a.B, r = grow - g * a.B;
       int4 dst_info = make_int4(-1, -1, 0, 0);

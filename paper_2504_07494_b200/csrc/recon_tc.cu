@@ -254,6 +254,8 @@ static int getenv_int(const char* k) {
 
 bool dense_tc_supported(int d) { return d % 256 == 0; }
 
+bool recon_pair_mode(int B) { return (B <= 128 || B % 256 == 0) && getenv_int("HC_TC_1SM") == 0; }
+
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s) {
   if (p.M <= 0) return cudaSuccess;
   pg::TcArgs a{};
@@ -307,6 +309,16 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   a.bias = p.b_int;
   a.rope_inv = p.rope_inv;
   a.row_pos = p.hblk_pos;
+  if (p.epi_attend) {   // fused reconstruct-and-attend: partials instead of scratch K/V
+    a.epi = pg::EPI_ATTEND;
+    a.hblk_req = p.hblk_req;
+    a.reqs = p.reqs;
+    a.q = static_cast<const __nv_bfloat16*>(p.q);
+    a.part_ml = p.part_ml;
+    a.part_acc = p.part_acc;
+    a.scale_log2 = p.scale_log2;
+    a.seg = p.seg;
+  }
   // Default schedule: n-major raster with 2 n-tiles per group, so pairs p and p^1 of a wave
   // share one A panel and every wave shares the group's W panels; the partner lockstep
   // makes the shared A panel hit in L2 (measured: DRAM reads 190 GB -> ~60 GB at OPT-66B).
@@ -315,7 +327,7 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   const int sw = getenv_int("HC_SYNC_W");
   a.sync_w = sw != 0 ? sw : 8;
   a.sync = (a.sync_w > 0 && a.group_m == -2) ? p.sync_counter : nullptr;
-  const bool pair_mode = (p.B <= 128 || p.B % 256 == 0) && (getenv_int("HC_TC_1SM") == 0 || p.rope_inv);
+  const bool pair_mode = recon_pair_mode(p.B) || p.rope_inv || p.epi_attend;
   if (pair_mode) {
     const int nsub_env = getenv_int("HC_TC_NSUB");
     const bool can2 = (2 * p.d) % 512 == 0;

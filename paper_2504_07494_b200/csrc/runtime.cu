@@ -161,6 +161,9 @@ struct Plan {
   int32_t n_kv_splits = 0, n_hid_splits = 0;
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
   bool absorb = false;                // hidden requests through absorbed.cu (f4 (ii)), no splits
+  bool attend = false;                // fused reconstruct-and-attend epilogue (no K/V scratch)
+  int32_t seg = 0;                    // attend: tokens per hidden partial (min(B, 32))
+  size_t off_hreqblk = 0;             // attend: batch index of each hidden block's request
   int32_t n_h = 0, n_atiles = 0, Hp = 0;
   int32_t gemm_m_tiles = 0, gemm_n_tiles = 0;
   int64_t n_tab = 0;
@@ -261,6 +264,12 @@ struct hc_pool {
     P.n_req = (int32_t)rs.size();
     P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
     P.absorb = (cfg.flags & HC_FLAG_ABSORB_HIDDEN) != 0;
+    {
+      const char* ea = std::getenv("HC_EPI_ATTEND");   // 0: rebuild K/V into scratch instead
+      P.attend = !P.absorb && tc_ok && cfg.dtype == HC_BF16 && !(ea && std::atoi(ea) == 0) &&
+                 recon_pair_mode(B);
+      P.seg = std::min(B, 32);
+    }
     for (auto* r : rs) {
       const int64_t nb = cdiv(r->n, B);
       const int32_t ns = (int32_t)cdiv(nb, P.split_blocks);
@@ -273,6 +282,8 @@ struct hc_pool {
         if (P.absorb) {
           ++P.n_h;
           P.n_atiles += (int32_t)cdiv(r->n, 128);
+        } else if (P.attend) {
+          P.n_splits += (int32_t)cdiv(r->n, P.seg);   // one partial per segment, in the GEMM epilogue
         } else {
           P.n_splits += ns;
           P.n_hid_splits += ns;
@@ -298,7 +309,9 @@ struct hc_pool {
     P.off_gather = o = align_up(o, 64);
     o += sizeof(int32_t) * P.n_hb;
     P.off_hpos = o = align_up(o, 64);
-    o += cfg.rope_theta > 0.f ? sizeof(int32_t) * P.n_hb : 0;
+    o += (cfg.rope_theta > 0.f || P.attend) ? sizeof(int32_t) * P.n_hb : 0;
+    P.off_hreqblk = o = align_up(o, 64);
+    o += P.attend ? sizeof(int32_t) * P.n_hb : 0;
     P.off_kvsplit = o = align_up(o, 64);
     o += P.fused ? sizeof(int32_t) * P.n_kv_splits : 0;
     P.off_hidsplit = o = align_up(o, 64);
@@ -321,7 +334,7 @@ struct hc_pool {
     const size_t n_tasks = (size_t)P.n_splits * H;
     P.off_ml = P.desc_bytes;
     P.off_acc = align_up(P.off_ml + n_tasks * 2 * sizeof(float), kAlign);
-    const size_t scr = P.absorb ? 0 : (size_t)P.n_hb * H * B * dh * elem;
+    const size_t scr = (P.absorb || P.attend) ? 0 : (size_t)P.n_hb * H * B * dh * elem;
     P.off_sk = align_up(P.off_acc + n_tasks * dh * sizeof(float), 1024);
     P.off_sv = align_up(P.off_sk + scr, 1024);
     size_t e = align_up(P.off_sv + scr, kAlign);
@@ -711,7 +724,11 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   int32_t* ahtile0 = reinterpret_cast<int32_t*>(h + P.off_htile0);
   int32_t* atreq = reinterpret_cast<int32_t*>(h + P.off_treq);
   int32_t* att0 = reinterpret_cast<int32_t*>(h + P.off_tt0);
+  int32_t* hreqblk = reinterpret_cast<int32_t*>(h + P.off_hreqblk);
   int32_t n_split = 0, n_tab = 0, n_hb = 0, n_kvs = 0, n_hds = 0, n_ah = 0, n_at = 0;
+  // attend mode: KV splits first (the attention kernels' tasks are exactly those), then one
+  // split per hidden segment (written by the GEMM epilogue, read only by the combine)
+  int32_t next_hid = P.n_kv_splits;
   if (P.fused) std::memset(h + P.off_tiledone, 0, P.desc_bytes - P.off_tiledone);
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = *rs[i];
@@ -719,7 +736,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     ReqDesc d{};
     d.mode = r.mode;
     d.n = (int32_t)r.n;
-    d.split_begin = n_split;
+    d.split_begin = (P.attend && r.mode == HC_MODE_HIDDEN) ? next_hid : n_split;
     if (r.mode == HC_MODE_KV) {
       d.tab_off = n_tab;
       for (int32_t lb = 0; lb < nb; ++lb) {
@@ -740,9 +757,22 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
         ++n_ah;
       }
       for (int32_t lb = 0; lb < nb; ++lb) {
-        if (rope) hpos[n_hb] = lb * B;
+        if (rope || P.attend) hpos[n_hb] = lb * B;
+        if (P.attend) hreqblk[n_hb] = i;
         gat[n_hb++] = r.a[lb];
       }
+    }
+    if (P.attend && r.mode == HC_MODE_HIDDEN) {
+      for (int64_t t0 = 0; t0 < r.n; t0 += P.seg) {
+        SplitDesc s{};
+        s.req = i;
+        s.lb0 = (int32_t)(t0 / B);
+        s.ntok = (int32_t)std::min<int64_t>(P.seg, r.n - t0);
+        sd[next_hid++] = s;
+      }
+      d.split_count = next_hid - d.split_begin;
+      rd[i] = d;
+      continue;
     }
     const bool absorbed = P.absorb && r.mode == HC_MODE_HIDDEN;
     for (int32_t lb = 0; lb < nb && !absorbed; lb += P.split_blocks) {
@@ -787,8 +817,16 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.dh = pool->cfg.head_dim;
   rp.B = B;
   rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
-  rp.hblk_pos = rope ? reinterpret_cast<const int32_t*>(ws + P.off_hpos) : nullptr;
+  rp.hblk_pos = (rope || P.attend) ? reinterpret_cast<const int32_t*>(ws + P.off_hpos) : nullptr;
   rp.rope_inv = rope ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
+  rp.epi_attend = P.attend;
+  rp.hblk_req = reinterpret_cast<const int32_t*>(ws + P.off_hreqblk);
+  rp.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
+  rp.q = q;
+  rp.part_ml = reinterpret_cast<float*>(ws + P.off_ml);
+  rp.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
+  rp.scale_log2 = scale * 1.4426950408889634f;
+  rp.seg = P.seg;
   AttnParams ap{};
   ap.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
   ap.splits = reinterpret_cast<const SplitDesc*>(ws + P.off_splits);
@@ -800,7 +838,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.part_ml = reinterpret_cast<float*>(ws + P.off_ml);
   ap.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
   ap.task_counter = reinterpret_cast<int32_t*>(ws);
-  ap.n_tasks = P.n_splits * H;
+  ap.n_tasks = (P.attend ? P.n_kv_splits : P.n_splits) * H;   // attend: hidden partials come from the GEMM
   ap.H = H;
   ap.dh = pool->cfg.head_dim;
   ap.B = B;

@@ -630,3 +630,36 @@ def test_layer_norm_unconfigured_is_unsupported(hc):
     with pytest.raises(hc.HcError) as e:
         pool.layer_norm(torch.zeros(2, 512, dtype=torch.bfloat16, device="cuda"))
     assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+# ------------------------------------------------------------------ fused reconstruct-and-attend (f1)
+@pytest.mark.parametrize("shape", [(512, 4, 128, 16), (512, 8, 64, 32), (384, 3, 128, 8), (256, 2, 128, 256)])
+def test_attend_epilogue_vs_scratch_path(hc, monkeypatch, shape):
+    """The default bf16 path turns rebuilt K/V into flash-decoding partials inside the GEMM
+    epilogue (segments of min(B, 32) tokens; K/V never stored).  It meets the oracle bar,
+    agrees with the K/V-scratch path (HC_EPI_ATTEND=0) within twice the bar with bit-identical
+    KV-mode rows, and needs far less workspace."""
+    d, H, dh, B = shape
+    w = _bf16_workload(d, H, dh, B, bias=True)
+    pool, a, la = _run(w, split_tokens=64)
+    ids = list(w.req_ids)
+    ws_attend = pool.workspace_size(ids)
+    assert T.compare(w, a, la, range(len(w.n)))[0] <= TOL_BF16
+    monkeypatch.setenv("HC_EPI_ATTEND", "0")
+    pool2, b, lb = _run(w, split_tokens=64)
+    from oracle import hc_oracle as O
+    assert O.max_rel_err(a, b, H) <= 2 * TOL_BF16
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    assert np.array_equal(a[kv], b[kv]) and np.array_equal(la[kv], lb[kv])
+    assert ws_attend < pool2.workspace_size(ids)
+
+
+def test_attend_epilogue_rope_and_long_contexts(hc):
+    """RoPE applied to k in registers before the dot product; contexts spanning many
+    segments and a last segment past n inside the last block."""
+    w = _bf16_workload(512, 4, 128, 16, n=[1, 17, 300, 4000, 129, 64, 2049], bias=True)
+    pool = T.make_pool(w, rope_theta=ROPE_THETA)
+    T.fill(pool, w)
+    out, lse = T.decode(pool, w, T.queries(w))
+    err, lerr = T.compare(w, out, lse, range(len(w.n)), rope_theta=ROPE_THETA)
+    assert err <= TOL_BF16 and lerr <= 5e-2, (err, lerr)
