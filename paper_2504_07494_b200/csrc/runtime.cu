@@ -379,6 +379,7 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   const size_t e = cfg->dtype == HC_BF16 ? 2 : 4;
   if ((cfg->head_dim * e) % 16 != 0)
     return fail(HC_E_UNSUPPORTED, "head_dim * element size must be a multiple of 16 bytes");
+  if (cfg->head_dim > 256) return fail(HC_E_UNSUPPORTED, "head_dim > 256");
   if (cfg->num_blocks > INT32_MAX || (int64_t)cfg->num_blocks * cfg->block_size > INT32_MAX)
     return fail(HC_E_UNSUPPORTED, "num_blocks * block_size must fit in int32");
   const bool accounting = (cfg->flags & HC_FLAG_ACCOUNTING_ONLY) != 0;

@@ -14,3 +14,7 @@ HC_FUSED=0 timeout 900 $NCU --set full --clock-control none --import-source on -
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"attn_pipe" -c 1 \
    -o $OUT/full_attn_cfg5h0 python bench.py --config cfg5:0.0 --profile-steps 1 > /dev/null 2>&1
 ls -la $OUT
+for r in full_fused_cfg4 full_recon_cfg4 full_attn_cfg5h0; do
+  [ -f $OUT/$r.ncu-rep ] && $NCU -i $OUT/$r.ncu-rep --page details --csv > $OUT/$r.csv 2>/dev/null
+done
+ls -la $OUT
