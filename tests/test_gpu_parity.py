@@ -633,7 +633,8 @@ def test_layer_norm_unconfigured_is_unsupported(hc):
 
 
 # ------------------------------------------------------------------ fused reconstruct-and-attend (f1)
-@pytest.mark.parametrize("shape", [(512, 4, 128, 16), (512, 8, 64, 32), (384, 3, 128, 8), (256, 2, 128, 256)])
+@pytest.mark.parametrize("shape", [(512, 4, 128, 16), (512, 8, 64, 32), (384, 3, 128, 8), (256, 2, 128, 256),
+                                   (256, 8, 32, 16)])
 def test_attend_epilogue_vs_scratch_path(hc, monkeypatch, shape):
     """The default bf16 path turns rebuilt K/V into flash-decoding partials inside the GEMM
     epilogue (segments of min(B, 32) tokens; K/V never stored).  It meets the oracle bar,
