@@ -247,6 +247,8 @@ def main():
     ap.add_argument("--prefill-reqs", type=int, default=16)
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: one batch split across ranks by LPT (default: weak)")
+    ap.add_argument("--rope", type=float, default=0.0,
+                    help="RoPE base theta (NEXT row f4 (i)): rebuilt K rotated at its positions")
     ap.add_argument("--absorb", action="store_true",
                     help="NON-PAPER variant (NEXT row f4 (ii)): hidden requests attend through "
                          "q~ = W_K^T q and W_V (sum a x) instead of rebuilding K/V")
@@ -295,7 +297,7 @@ def main():
     else:
         w = C.shard_for_rank(w0, rank, world)
     pool = T.make_pool(w, device=local, split_tokens=args.split_tokens,
-                       flags=hc.HC_FLAG_ABSORB_HIDDEN if args.absorb else 0)
+                       flags=hc.HC_FLAG_ABSORB_HIDDEN if args.absorb else 0, rope_theta=args.rope)
     T.fill(pool, w, device=local)
     q = T.queries(w, device=local)
     ids = list(w.req_ids)
@@ -475,7 +477,8 @@ def main():
                    "output_gather": f"{dist.get_backend()} all-gather of out+lse every step (timed)" if gather else "none",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
                    "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
-                   else "paper (hidden K/V rebuilt every step)"},
+                   else "paper (hidden K/V rebuilt every step)",
+                   "rope_theta": args.rope},
         "roofline": roof,
         "step_roofline": {"T_roof_ms": T_roof * 1e3, "frac": T_roof * 1e3 / ms, "alg_bytes": B_alg,
                           "alg_flops": F_alg, "alg_GBps": B_alg / (ms / 1e3) / 1e9,
