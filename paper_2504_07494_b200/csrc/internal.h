@@ -164,6 +164,7 @@ bool prefill_attn_mma_supported(int dtype, int dh);
 // tmap_kv over kv [R, 2d], both {64 x 128} boxes.  HC_PREFILL_TC=0 selects the mma.sync kernel.
 bool prefill_attn_tc_enabled();
 int prefill_attn_tc_keys();   // keys per tile (tmap_kv box rows)
+int prefill_attn_tc_rows();   // query rows per CTA (tile_q0 step): 128 or 256
 cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_q, const void* tmap_kv,
                                    cudaStream_t s);
 

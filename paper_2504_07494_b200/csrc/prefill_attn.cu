@@ -245,16 +245,21 @@ __global__ void __launch_bounds__(128) prefill_attn_mma_kernel(const PrefillAttn
 //              more than 2^8): O rows are rescaled in TMEM (ld / scale / st) only then;
 //              P <= 2^8 in bf16 is exact enough and l is fp32.  Epilogue: O / l -> bf16.
 // TMEM: S0 cols [0,128), S1 [128,256), O [256, 256+dh).
-template <int DH, int BK>
-__global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
+// NQ = query tiles of 128 rows per CTA sharing every K/V tile (NQ = 2: FlashAttention-4
+// style pair of softmax warpgroups that ping-pong on the tensor core); ST = K/V stages.
+template <int DH, int BK, int NQ, int ST>
+__global__ void __launch_bounds__(64 + 128 * NQ, (BK == 64 && NQ == 1) ? 2 : 1)
     prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_kv,
                            const PrefillAttnParams p) {
-  constexpr int BM = 128, NCH = DH / 64, ST = 2, NPC = BK / 64;
+  constexpr int BM = 128, NCH = DH / 64, NPC = BK / 64;
   constexpr int QCH = 128 * 128;                   // Q / P chunk: 128 rows x 64 columns (16 KiB)
   constexpr int KCH = BK * 128;                    // K / V chunk: BK rows x 64 columns
-  constexpr int Q_OFF = 0, K_OFF = NCH * QCH, V_OFF = K_OFF + ST * NCH * KCH;
-  constexpr int P_OFF = V_OFF + ST * NCH * KCH, BAR_OFF = P_OFF + NPC * QCH;
-  constexpr uint32_t O_COL = 2 * BK;               // TMEM: S buffers [0, 2 BK), O [2 BK, 2 BK + DH)
+  constexpr int Q_OFF = 0, K_OFF = NQ * NCH * QCH, V_OFF = K_OFF + ST * NCH * KCH;
+  constexpr int P_OFF = V_OFF + ST * NCH * KCH, BAR_OFF = P_OFF + NQ * NPC * QCH;
+  // TMEM per query tile: S buffers [0, 2 BK), O [2 BK, 2 BK + DH); tiles TCOLS apart
+  constexpr uint32_t O_COL = 2 * BK, TCOLS = (2 * BK + DH <= 256) ? 256 : 512;
+  constexpr uint32_t TMEM_ALLOC = NQ * TCOLS;
+  static_assert(TMEM_ALLOC <= 512, "TMEM");
   constexpr float kRescale = 8.f;                  // log2 headroom before O is rescaled
   // no alignment slack (two CTAs per SM need every KiB): the dynamic window is 1024-aligned
   // when the kernel has no static shared memory; trap otherwise rather than overflow
@@ -263,19 +268,24 @@ __global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
   if (ptx::smem_u32(smem) & 1023) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;        // [ST]
-  uint64_t* kv_empty = bars + 3;       // [ST]
-  uint64_t* s_full = bars + 5;         // [2]
-  uint64_t* s_free = bars + 7;         // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_done = bars + 10;
-  uint64_t* o_final = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* kv_full = bars + 1;                    // [ST]
+  uint64_t* kv_empty = kv_full + ST;               // [ST]
+  uint64_t* s_full = kv_empty + ST;                // [NQ][2]
+  uint64_t* s_free = s_full + 2 * NQ;              // [NQ][2]
+  uint64_t* p_full = s_free + 2 * NQ;              // [NQ]
+  uint64_t* o_done = p_full + NQ;                  // [NQ]
+  uint64_t* o_final = o_done + NQ;                 // [NQ]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + NQ);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y;
   const int req = p.tile_req[blockIdx.x], q0 = p.tile_q0[blockIdx.x];
   const int row0 = p.row0[req], L = p.row0[req + 1] - row0;
-  const int nt = (min(q0 + BM, L) + BK - 1) / BK;
+  // key tiles each query tile needs (causal: up to its last query); 0 = tile past L
+  int ntq[NQ];
+#pragma unroll
+  for (int qt = 0; qt < NQ; ++qt)
+    ntq[qt] = q0 + qt * BM < L ? (min(q0 + (qt + 1) * BM, L) + BK - 1) / BK : 0;
+  const int nt = ntq[0] > ntq[NQ - 1] ? ntq[0] : ntq[NQ - 1];
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_q);
     ptx::prefetch_tmap(&tmap_kv);
@@ -284,26 +294,29 @@ __global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
       ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2 * NQ; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_free[i], 128);
     }
-    ptx::mbar_init(p_full, 128);
-    ptx::mbar_init(o_done, 1);
-    ptx::mbar_init(o_final, 1);
+    for (int i = 0; i < NQ; ++i) {
+      ptx::mbar_init(&p_full[i], 128);
+      ptx::mbar_init(&o_done[i], 1);
+      ptx::mbar_init(&o_final[i], 1);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<(2 * BK + DH <= 256 ? 256 : 512)>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<TMEM_ALLOC>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_o = tmem + O_COL;
 
   if (warp == 0) {
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(q_full, NCH * QCH);
-      for (int c = 0; c < NCH; ++c) ptx::tma_load_2d(smem + Q_OFF + c * QCH, &tmap_q, h * DH + c * 64, row0 + q0, q_full);
+      ptx::mbar_arrive_expect_tx(q_full, NQ * NCH * QCH);
+      for (int qt = 0; qt < NQ; ++qt)
+        for (int c = 0; c < NCH; ++c)
+          ptx::tma_load_2d(smem + Q_OFF + (qt * NCH + c) * QCH, &tmap_q, h * DH + c * 64, row0 + q0 + qt * BM, q_full);
       for (int t = 0; t < nt; ++t) {
         const int st = t % ST;
         ptx::mbar_wait(&kv_empty[st], ((t / ST) & 1) ^ 1);
@@ -320,53 +333,62 @@ __global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = ptx::umma_idesc_bf16_f32(BM, BK);
       constexpr uint32_t idesc_o = ptx::umma_idesc_bf16_f32(BM, DH) | (1u << 16);   // B (V) MN-major
-      const uint32_t sq = ptx::smem_u32(smem + Q_OFF), sp = ptx::smem_u32(smem + P_OFF);
-      auto issue_s = [&](int t) {
+      auto issue_s = [&](int qt, int t) {
         const int st = t % ST, b = t & 1;
         ptx::mbar_wait(&kv_full[st], (t / ST) & 1);
-        ptx::mbar_wait(&s_free[b], ((t >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&s_free[2 * qt + b], ((t >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
+        const uint32_t sq = ptx::smem_u32(smem + Q_OFF + qt * NCH * QCH);
         const uint32_t sk = ptx::smem_u32(smem + K_OFF + st * NCH * KCH);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          ptx::umma_f16_ss(tmem + b * BK, ptx::umma_desc_k_sw128(sq + (kk >> 2) * QCH + (kk & 3) * 32),
+          ptx::umma_f16_ss(tmem + qt * TCOLS + b * BK, ptx::umma_desc_k_sw128(sq + (kk >> 2) * QCH + (kk & 3) * 32),
                            ptx::umma_desc_k_sw128(sk + (kk >> 2) * KCH + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
-        ptx::umma_commit(&s_full[b]);
+        ptx::umma_commit(&s_full[2 * qt + b]);
       };
       ptx::mbar_wait(q_full, 0);
-      issue_s(0);
+      for (int qt = 0; qt < NQ; ++qt)
+        if (ntq[qt] > 0) issue_s(qt, 0);
       for (int t = 0; t < nt; ++t) {
-        if (t + 1 < nt) issue_s(t + 1);
-        ptx::mbar_wait(p_full, t & 1);
-        ptx::tc_fence_after();
+        for (int qt = 0; qt < NQ; ++qt)
+          if (t + 1 < ntq[qt]) issue_s(qt, t + 1);
         const uint32_t sv = ptx::smem_u32(smem + V_OFF + (t % ST) * NCH * KCH);
+        for (int qt = 0; qt < NQ; ++qt) {
+          if (t >= ntq[qt]) continue;
+          ptx::mbar_wait(&p_full[qt], t & 1);
+          ptx::tc_fence_after();
+          const uint32_t sp = ptx::smem_u32(smem + P_OFF + qt * NPC * QCH);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
-          ptx::umma_f16_ss(tmem_o, ptx::umma_desc_k_sw128(sp + (kk >> 2) * QCH + (kk & 3) * 32),
-                           ptx::umma_desc_mn_sw128(sv + kk * 2048, KCH), idesc_o, (t | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk)
+            ptx::umma_f16_ss(tmem + qt * TCOLS + O_COL, ptx::umma_desc_k_sw128(sp + (kk >> 2) * QCH + (kk & 3) * 32),
+                             ptx::umma_desc_mn_sw128(sv + kk * 2048, KCH), idesc_o, (t | kk) != 0 ? 1u : 0u);
+          ptx::umma_commit(&o_done[qt]);
+        }
         ptx::umma_commit(&kv_empty[t % ST]);
-        ptx::umma_commit(o_done);
       }
-      ptx::umma_commit(o_final);
+      for (int qt = 0; qt < NQ; ++qt) ptx::umma_commit(&o_final[qt]);
     }
     __syncwarp();
   } else {
+    const int qt = (warp - 2) >> 2;                // query tile of this softmax warpgroup
     const int quad = warp & 3, row = quad * 32 + lane;
-    const int qi = q0 + row;                       // query token index (>= L: padding row)
+    const int qi = q0 + qt * BM + row;             // query token index (>= L: padding row)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tq = tmem + qt * TCOLS, tmem_o = tq + O_COL;
     const float sl = p.scale_log2;
     float m_ref = -INFINITY, l = 0.f;
-    uint8_t* sP = smem + P_OFF;
-    for (int t = 0; t < nt; ++t) {
+    uint8_t* sP = smem + P_OFF + qt * NPC * QCH;
+    const int my_nt = ntq[qt];
+    for (int t = 0; t < my_nt; ++t) {
       const int b = t & 1;
-      ptx::mbar_wait(&s_full[b], (t >> 1) & 1);
+      ptx::mbar_wait(&s_full[2 * qt + b], (t >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t v[BK / 32][32];
 #pragma unroll
-      for (int c = 0; c < BK / 32; ++c) ptx::tmem_ld_32x32b_x32(tmem + lane_off + b * BK + c * 32, v[c]);
+      for (int c = 0; c < BK / 32; ++c) ptx::tmem_ld_32x32b_x32(tq + lane_off + b * BK + c * 32, v[c]);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_free[b]);
+      ptx::mbar_arrive(&s_free[2 * qt + b]);
       // keys k0 + j valid iff k0 + j <= qi and < L
       const int lim = min(qi, L - 1) - t * BK;     // last valid j (may be >= BK-1 or < 0)
       float sv[BK];
@@ -401,7 +423,7 @@ __global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
       }
       l += (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
       if (t > 0) {
-        ptx::mbar_wait(o_done, (t - 1) & 1);       // PV_{t-1} retired: P buffer free, O stable
+        ptx::mbar_wait(&o_done[qt], (t - 1) & 1);  // PV_{t-1} retired: P buffer free, O stable
         ptx::tc_fence_after();
         if (scale_o != 1.f) {
 #pragma unroll 1
@@ -425,31 +447,33 @@ __global__ void __launch_bounds__(192, BK == 64 ? 2 : 1)
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full);
+      ptx::mbar_arrive(&p_full[qt]);
     }
-    ptx::mbar_wait(o_final, 0);
-    ptx::tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.o);
+    if (my_nt > 0) {
+      ptx::mbar_wait(&o_final[qt], 0);
+      ptx::tc_fence_after();
+      const float inv = 1.f / l;
+      __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.o);
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t o[32];
-      ptx::tmem_ld_32x32b_x32(tmem_o + lane_off + c * 32, o);
-      ptx::tmem_ld_wait();
-      if (qi < L) {
-        uint4* dst = reinterpret_cast<uint4*>(O + (size_t)(row0 + qi) * p.d + h * DH + c * 32);
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t o[32];
+        ptx::tmem_ld_32x32b_x32(tmem_o + lane_off + c * 32, o);
+        ptx::tmem_ld_wait();
+        if (qi < L) {
+          uint4* dst = reinterpret_cast<uint4*>(O + (size_t)(row0 + qi) * p.d + h * DH + c * 32);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(pack2(__uint_as_float(o[8 * j]) * inv, __uint_as_float(o[8 * j + 1]) * inv),
-                              pack2(__uint_as_float(o[8 * j + 2]) * inv, __uint_as_float(o[8 * j + 3]) * inv),
-                              pack2(__uint_as_float(o[8 * j + 4]) * inv, __uint_as_float(o[8 * j + 5]) * inv),
-                              pack2(__uint_as_float(o[8 * j + 6]) * inv, __uint_as_float(o[8 * j + 7]) * inv));
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(pack2(__uint_as_float(o[8 * j]) * inv, __uint_as_float(o[8 * j + 1]) * inv),
+                                pack2(__uint_as_float(o[8 * j + 2]) * inv, __uint_as_float(o[8 * j + 3]) * inv),
+                                pack2(__uint_as_float(o[8 * j + 4]) * inv, __uint_as_float(o[8 * j + 5]) * inv),
+                                pack2(__uint_as_float(o[8 * j + 6]) * inv, __uint_as_float(o[8 * j + 7]) * inv));
+        }
       }
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc<(2 * BK + DH <= 256 ? 256 : 512)>(tmem);
+  if (warp == 1) ptx::tmem_dealloc<TMEM_ALLOC>(tmem);
 }
 
 // ------------------------------------------------------------------ SIMT fallback
@@ -535,20 +559,27 @@ bool prefill_attn_tc_enabled() {   // read per call so tests can switch paths
   return !e || std::atoi(e) != 0;
 }
 
-int prefill_attn_tc_keys() {   // keys per tile of the tcgen05 kernel (A/B knob HC_PREFILL_BK)
-  const char* e = std::getenv("HC_PREFILL_BK");
-  return e && std::atoi(e) == 128 ? 128 : 64;
+// Configuration of the tcgen05 prefill kernel (A/B knob HC_PREFILL_CFG): 1 = one query tile
+// per CTA, 64-key tiles, 2 K/V stages, two CTAs per SM (default, fastest measured);
+// 2 = two query tiles per CTA sharing 3 K/V stages (FA4-style pair of softmax warpgroups);
+// 128 = one query tile, 128-key tiles.
+int prefill_attn_tc_cfg() {
+  const char* e = std::getenv("HC_PREFILL_CFG");
+  const int v = e ? std::atoi(e) : 1;
+  return (v == 2 || v == 128) ? v : 1;
 }
+int prefill_attn_tc_keys() { return prefill_attn_tc_cfg() == 128 ? 128 : 64; }
+int prefill_attn_tc_rows() { return prefill_attn_tc_cfg() == 2 ? 256 : 128; }
 
-template <int DH, int BK>
+template <int DH, int BK, int NQ, int ST>
 static cudaError_t launch_tc(const PrefillAttnParams& p, const CUtensorMap& tq, const CUtensorMap& tkv,
                              cudaStream_t s) {
   constexpr int NCH = DH / 64;
-  constexpr int smem = NCH * 128 * 128 + 4 * NCH * BK * 128 + (BK / 64) * 128 * 128 + 128;
+  constexpr int smem = NQ * NCH * 128 * 128 + 2 * ST * NCH * BK * 128 + NQ * (BK / 64) * 128 * 128 + 256;
   static const cudaError_t a =
-      cudaFuncSetAttribute(prefill_attn_tc_kernel<DH, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(prefill_attn_tc_kernel<DH, BK, NQ, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (a != cudaSuccess) return a;
-  prefill_attn_tc_kernel<DH, BK><<<dim3(p.n_qtiles, p.H), 192, smem, s>>>(tq, tkv, p);
+  prefill_attn_tc_kernel<DH, BK, NQ, ST><<<dim3(p.n_qtiles, p.H), 64 + 128 * NQ, smem, s>>>(tq, tkv, p);
   return cudaGetLastError();
 }
 
@@ -557,9 +588,17 @@ cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_
   if (p.n_qtiles <= 0) return cudaSuccess;
   const CUtensorMap& tq = *static_cast<const CUtensorMap*>(tmap_q);
   const CUtensorMap& tkv = *static_cast<const CUtensorMap*>(tmap_kv);
-  const int bk = prefill_attn_tc_keys();
-  if (p.dh == 128) return bk == 128 ? launch_tc<128, 128>(p, tq, tkv, s) : launch_tc<128, 64>(p, tq, tkv, s);
-  if (p.dh == 64) return bk == 128 ? launch_tc<64, 128>(p, tq, tkv, s) : launch_tc<64, 64>(p, tq, tkv, s);
+  const int cfg = prefill_attn_tc_cfg();
+  if (p.dh == 128) {
+    if (cfg == 128) return launch_tc<128, 128, 1, 2>(p, tq, tkv, s);
+    if (cfg == 1) return launch_tc<128, 64, 1, 2>(p, tq, tkv, s);
+    return launch_tc<128, 64, 2, 3>(p, tq, tkv, s);
+  }
+  if (p.dh == 64) {
+    if (cfg == 128) return launch_tc<64, 128, 1, 2>(p, tq, tkv, s);
+    if (cfg == 1) return launch_tc<64, 64, 1, 2>(p, tq, tkv, s);
+    return launch_tc<64, 64, 2, 3>(p, tq, tkv, s);
+  }
   return cudaErrorInvalidValue;
 }
 

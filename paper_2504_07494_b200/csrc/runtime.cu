@@ -1149,7 +1149,7 @@ bool prefill_uses_tc(const hc_pool* pool) {
   return prefill_attn_tc_enabled() && prefill_attn_mma_supported(pool->cfg.dtype, pool->cfg.head_dim) &&
          !(pool->cfg.flags & HC_FLAG_FORCE_SIMT);
 }
-int prefill_tile_rows(const hc_pool* pool) { return prefill_uses_tc(pool) ? 128 : 64; }
+int prefill_tile_rows(const hc_pool* pool) { return prefill_uses_tc(pool) ? prefill_attn_tc_rows() : 64; }
 
 PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens) {
   PrefillPlan P;
