@@ -97,14 +97,15 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(const AttnParams p) {
       }
       m = m_new;
     }
+    const size_t pidx = (size_t)(task % p.H) * p.n_splits_all + task / p.H;   // head-major
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
       const int c = lane + 32 * i;
-      if (c < DH) p.part_acc[(size_t)task * DH + c] = acc[i];
+      if (c < DH) p.part_acc[pidx * DH + c] = acc[i];
     }
     if (lane == 0) {
-      p.part_ml[2 * (size_t)task] = m;
-      p.part_ml[2 * (size_t)task + 1] = l;
+      p.part_ml[2 * pidx] = m;
+      p.part_ml[2 * pidx + 1] = l;
     }
     __syncwarp();
   }

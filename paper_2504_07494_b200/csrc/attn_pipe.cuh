@@ -275,15 +275,16 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
 #pragma unroll
         for (int c = 0; c < 8; ++c) a[c] += __shfl_xor_sync(FULL, a[c], o);
       const float l_tot = warp_sum(l_lane);
-      const int task = mt.x;
+      const int task = mt.x;   // split * H + head -> head-major partial index
+      const size_t pidx = (size_t)(task % p.H) * p.n_splits_all + task / p.H;
       if (lane < LPR) {
-        float4* dst = reinterpret_cast<float4*>(p.part_acc + (size_t)task * DH) + 2 * lane;
+        float4* dst = reinterpret_cast<float4*>(p.part_acc + pidx * DH) + 2 * lane;
         dst[0] = make_float4(a[0], a[1], a[2], a[3]);
         dst[1] = make_float4(a[4], a[5], a[6], a[7]);
       }
       if (lane == 0) {
-        p.part_ml[2 * (size_t)task] = m_run;
-        p.part_ml[2 * (size_t)task + 1] = l_tot;
+        p.part_ml[2 * pidx] = m_run;
+        p.part_ml[2 * pidx + 1] = l_tot;
       }
     }
     __syncwarp();

@@ -166,6 +166,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     a.q = static_cast<const __nv_bfloat16*>(rp.q);
     a.part_ml = rp.part_ml;
     a.part_acc = rp.part_acc;
+    a.n_splits_all = rp.n_splits_all;
     a.scale_log2 = rp.scale_log2;
     a.seg = rp.seg;
     tile_done = nullptr;

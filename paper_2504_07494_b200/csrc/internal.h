@@ -35,8 +35,10 @@ struct AttnParams {
   const void* scr_k;      // rebuilt K of hidden requests, [hblock][H][B][dh]
   const void* scr_v;
   const void* q;          // [n_req, d]
-  float* part_ml;         // [n_tasks][2]: running max (log2 domain), sum
-  float* part_acc;        // [n_tasks][dh]: unnormalised sum_j p_j v_j
+  float* part_ml;         // [H][n_splits_all][2]: running max (log2 domain), sum
+  float* part_acc;        // [H][n_splits_all][dh]: unnormalised sum_j p_j v_j (head-major, so a
+                          // (request, head)'s splits are contiguous for the combine)
+  int32_t n_splits_all;   // splits in the call (partial index = head * n_splits_all + split)
   int32_t* task_counter;  // zero on entry (part of the uploaded descriptor)
   int32_t n_tasks;        // n_splits * H; task = split * H + head
   int32_t H, dh, B, d;
@@ -52,8 +54,9 @@ struct AttnParams {
 
 struct CombineParams {
   const ReqDesc* reqs;
-  const float* part_ml;
-  const float* part_acc;
+  const float* part_ml;   // [H][n_splits][2]
+  const float* part_acc;  // [H][n_splits][dh]
+  int32_t n_splits;
   void* out;   // [n_req, d]
   float* lse;  // nullable [n_req, H]
   int32_t n_req, H, dh, d;
@@ -79,6 +82,7 @@ struct ReconParams {
   const void* q;            // [n_req, d]
   float* part_ml;
   float* part_acc;
+  int32_t n_splits_all;     // partial index = head * n_splits_all + split
   float scale_log2;
   int32_t seg;              // tokens per partial: min(B, 32)
 };

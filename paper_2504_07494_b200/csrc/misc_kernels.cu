@@ -71,69 +71,67 @@ __device__ __forceinline__ void st_out<__nv_bfloat16>(__nv_bfloat16* p, float v)
 }
 
 // Split combine: M = max_s m_s, L = sum_s 2^(m_s-M) l_s, out = sum_s 2^(m_s-M) acc_s / L,
-// lse = (M + log2 L) ln 2 (scores were kept in log2 units).  One CTA (128 threads) per
+// lse = (M + log2 L) ln 2 (scores were kept in log2 units).  One CTA (256 threads) per
 // (request, head): block reductions for M and L, the split weights 2^(m_s - M) staged in
-// shared memory chunk by chunk, then every thread accumulates one output dimension (or, for
-// dh < 128, one dimension over an interleaved subset of the splits, reduced at the end).
+// shared memory chunk by chunk, then 256/dh groups of threads each accumulate every output
+// dimension over an interleaved subset of the splits (partials are head-major, so the
+// splits of one (request, head) are contiguous), reduced through shared memory.
 template <typename T>
-__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
-  constexpr int kChunk = 512;
+__global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
+  constexpr int NT = 256, kChunk = 512;
   __shared__ float w_s[kChunk];
-  __shared__ float red[4];
-  __shared__ float part[128];
+  __shared__ float red[NT / 32];
+  __shared__ float part[NT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = blockIdx.x / p.H, h = blockIdx.x - r * p.H;
   const ReqDesc rq = p.reqs[r];
   if (rq.split_count == 0) return;   // absorbed hidden request: written by wv_kernel
   const int H = p.H, dh = p.dh, cnt = rq.split_count;
-  const float* ml = p.part_ml + 2 * ((size_t)rq.split_begin * H + h);   // split s at ml[2 s H]
+  const size_t base_idx = (size_t)h * p.n_splits + rq.split_begin;   // head-major: splits contiguous
+  const float* ml = p.part_ml + 2 * base_idx;                         // split s at ml[2 s]
+  auto block_reduce = [&](float v, bool is_max) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, u) : v + u;
+    }
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) t = is_max ? fmaxf(t, red[w]) : t + red[w];
+    __syncthreads();
+    return t;
+  };
   float M = -INFINITY;
-  for (int s = tid; s < cnt; s += 128) M = fmaxf(M, ml[2 * (size_t)s * H]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  if (lane == 0) red[warp] = M;
-  __syncthreads();
-  M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-  __syncthreads();
+  for (int s = tid; s < cnt; s += NT) M = fmaxf(M, ml[2 * s]);
+  M = block_reduce(M, true);
   float L = 0.f;
-  for (int s = tid; s < cnt; s += 128) L += exp2f(ml[2 * (size_t)s * H] - M) * ml[2 * (size_t)s * H + 1];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-  if (lane == 0) red[warp] = L;
-  __syncthreads();
-  L = (red[0] + red[1]) + (red[2] + red[3]);
+  for (int s = tid; s < cnt; s += NT) L += exp2f(ml[2 * s] - M) * ml[2 * s + 1];
+  L = block_reduce(L, false);
   const float inv = 1.f / L;
-  const int G = dh >= 128 ? 1 : 128 / dh;          // split interleave groups
-  const int grp = dh >= 128 ? 0 : tid / dh, c0 = dh >= 128 ? tid : tid - grp * dh;
-  const float* acc = p.part_acc + (size_t)rq.split_begin * H * dh + (size_t)h * dh;   // split s at s H dh
-  float o[2] = {0.f, 0.f};                          // dims c0 and c0 + 128 (dh <= 256)
+  // thread -> (split group, dimension): G = NT / dh groups take interleaved splits
+  const int G = NT / dh, grp = tid / dh, c = tid - grp * dh;
+  const float* acc = p.part_acc + base_idx * dh;   // split s at s dh
+  float o = 0.f;
   for (int base = 0; base < cnt; base += kChunk) {
     const int n = min(kChunk, cnt - base);
     __syncthreads();
-    for (int s = tid; s < n; s += 128) w_s[s] = exp2f(ml[2 * (size_t)(base + s) * H] - M);
+    for (int s = tid; s < n; s += NT) w_s[s] = exp2f(ml[2 * (base + s)] - M);
     __syncthreads();
-    if (c0 < dh) {
-      const float* a0 = acc + (size_t)base * H * dh;
+    if (grp < G) {
+      const float* a0 = acc + (size_t)base * dh + c;
 #pragma unroll 4
-      for (int s = grp; s < n; s += G) {
-        const float ws = w_s[s];
-        o[0] = fmaf(ws, a0[(size_t)s * H * dh + c0], o[0]);
-        if (c0 + 128 < dh) o[1] = fmaf(ws, a0[(size_t)s * H * dh + c0 + 128], o[1]);
-      }
+      for (int s = grp; s < n; s += G) o = fmaf(w_s[s], a0[(size_t)s * dh], o);
     }
   }
+  part[tid] = o;
+  __syncthreads();
   T* out = static_cast<T*>(p.out) + (size_t)r * p.d + h * dh;
-  if (G == 1) {
-    if (c0 < dh) st_out<T>(out + c0, o[0] * inv);
-    if (c0 + 128 < dh) st_out<T>(out + c0 + 128, o[1] * inv);
-  } else {
-    part[tid] = o[0];
-    __syncthreads();
-    if (tid < dh) {
-      float t = 0.f;
-      for (int g = 0; g < G; ++g) t += part[g * dh + tid];
-      st_out<T>(out + tid, t * inv);
-    }
+  for (int cc = tid; cc < dh; cc += NT) {
+    float t = 0.f;
+    for (int g = 0; g < G; ++g) t += part[g * dh + cc];
+    st_out<T>(out + cc, t * inv);
   }
   if (tid == 0 && p.lse) p.lse[(size_t)r * H + h] = (M + log2f(L)) * 0.69314718055994531f;
 }
@@ -167,9 +165,9 @@ cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s) {
   if (blocks <= 0) return cudaSuccess;
   if (p.dh > 256) return cudaErrorInvalidValue;
   if (dtype == 1)
-    combine_kernel<float><<<blocks, 128, 0, s>>>(p);
+    combine_kernel<float><<<blocks, 256, 0, s>>>(p);
   else
-    combine_kernel<__nv_bfloat16><<<blocks, 128, 0, s>>>(p);
+    combine_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

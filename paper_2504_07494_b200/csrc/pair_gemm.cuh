@@ -58,8 +58,9 @@ struct TcArgs {
   const int32_t* hblk_req;  // batch index of each hidden block's request
   const ReqDesc* reqs;
   const __nv_bfloat16* q;   // [n_req, d]
-  float* part_ml;           // [task][2], task = split * H + head
-  float* part_acc;          // [task][dh]
+  float* part_ml;           // [H][n_splits_all][2]
+  float* part_acc;          // [H][n_splits_all][dh]
+  int32_t n_splits_all;
   float scale_log2;
   int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
 };
@@ -287,7 +288,7 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
     float l = p;
 #pragma unroll
     for (int o = S / 2; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
-    const size_t task = (size_t)split * a.H + h;
+    const size_t task = (size_t)h * a.n_splits_all + split;   // head-major partial index
 #pragma unroll 1
     for (int c0 = 0; c0 < dh; c0 += 32) {
       float f[32];

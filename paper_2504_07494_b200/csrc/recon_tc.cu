@@ -316,6 +316,7 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
     a.q = static_cast<const __nv_bfloat16*>(p.q);
     a.part_ml = p.part_ml;
     a.part_acc = p.part_acc;
+    a.n_splits_all = p.n_splits_all;
     a.scale_log2 = p.scale_log2;
     a.seg = p.seg;
   }

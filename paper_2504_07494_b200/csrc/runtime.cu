@@ -826,6 +826,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.q = q;
   rp.part_ml = reinterpret_cast<float*>(ws + P.off_ml);
   rp.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
+  rp.n_splits_all = P.n_splits;
   rp.scale_log2 = scale * 1.4426950408889634f;
   rp.seg = P.seg;
   AttnParams ap{};
@@ -838,6 +839,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.q = q;
   ap.part_ml = reinterpret_cast<float*>(ws + P.off_ml);
   ap.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
+  ap.n_splits_all = P.n_splits;
   ap.task_counter = reinterpret_cast<int32_t*>(ws);
   ap.n_tasks = (P.attend ? P.n_kv_splits : P.n_splits) * H;   // attend: hidden partials come from the GEMM
   ap.H = H;
@@ -926,6 +928,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   cp.reqs = ap.reqs;
   cp.part_ml = ap.part_ml;
   cp.part_acc = ap.part_acc;
+  cp.n_splits = P.n_splits;
   cp.out = out;
   cp.lse = lse;
   cp.n_req = n_req;
