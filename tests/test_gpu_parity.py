@@ -238,7 +238,7 @@ def _sample(w, n_kv=4, n_hid=2):
     return [int(i) for i in pick]
 
 
-@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4"])
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4", "cfg5:0.03125", "cfg5:1.0"])
 def test_opt_shaped_sampled_parity(hc, cfg):
     """Full batch on the GPU in the bench's launch configuration (auto split, tcgen05
     GEMM, pipelined attention); the oracle checks a seeded sample of requests (KV: all
