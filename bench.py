@@ -444,13 +444,13 @@ def main():
         kernels["absorbed_hidden"] = {
             "ms": t_rec, "bound": "hbm", "unit": "GB/s", "bytes_per_launch": ab_bytes,
             "achieved": (ab_bytes / (t_rec / 1e3) / 1e9) if t_rec > 0 else None,
-            "note": "5 kernels: q~ (warp MMA), scores (tcgen05), P rescale, Z (tcgen05), W_V (warp MMA); bytes = x read twice + W_K + W_V + q~/Z round trips"}
+            "note": "5 kernels: q~, scores, Z and W_V GEMMs on tcgen05, P rescale; bytes = x read twice + W_K + W_V + q~/Z round trips"}
         dom = "absorbed_hidden" if t_rec >= t_att else "attention"
     else:
         dom = ("fused_step" if fused else "recon_gemm") if t_rec >= t_att else "attention"
     k = kernels[dom]
     if dom == "absorbed_hidden":
-        roof = {"bound": "hbm", "kernel": "absorbed qt/score/stats/z/wv kernels", "achieved": k["achieved"],
+        roof = {"bound": "hbm", "kernel": "absorbed qt/score/rescale/z/wv kernels", "achieved": k["achieved"],
                 "peak": hbm, "unit": "GB/s", "frac": k["achieved"] / hbm, "traffic": None,
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":

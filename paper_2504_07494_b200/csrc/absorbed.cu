@@ -9,13 +9,13 @@
 // so a hidden token costs two reads of x (4d bytes, like the K and V rows of a KV token)
 // plus 4 Hp d FLOPs, and the per-call work is two weight reads (W_K, W_V) — the path is
 // HBM-bound instead of tensor-bound.  Five kernels, bf16 in / fp32 accumulate:
-//   K1 qt_kernel       q~[r][h][:] = W_K,h^T q_{r,h} (per head [n_h x dh][dh x d], warp MMA);
-//                      q_h . b_K,h
+//   K1 qt_tc_kernel    q~[r][h][:] = W_K,h^T q_{r,h} (per head [n_h x dh][dh x d], tcgen05,
+//                      W_K,h as an MN-major operand); q_h . b_K,h
 //   K2 score_tc_kernel per 128-token tile of request r (tcgen05): s = x . q~[r][h]; tile max
 //                      m_t[h], P[row][h] = 2^(scaled s - m_t) (bf16), l_t[h] = sum P
 //   K3 rescale_kernel  m[h] = max_t m_t, P *= 2^(m_t - m), l = sum_t 2^(m_t - m) l_t
 //   K4 z_tc_kernel     Z[r][h][:] = sum_rows P[row][h] x_row (tcgen05, MN-major operands)
-//   K5 wv_kernel       out[r][h*dh:] = W_V,h Z[r][h] / l + b_V,h;  lse (warp MMA)
+//   K5 wv_tc_kernel    out[r][h*dh:] = W_V,h Z[h][r] / l + b_V,h;  lse (tcgen05)
 // x is read exactly twice (K2, K4), straight from the pool blocks through TMA.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -43,103 +43,12 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ void ldsm4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(a));
-}
-__device__ __forceinline__ void ldsm4t(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(a));
-}
-__device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                    uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
 __device__ __forceinline__ uint32_t pk(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 // 64-element (128 B) swizzled rows: 16-byte chunk c (0..7) of row r at chunk c ^ (r & 7)
 __device__ __forceinline__ uint32_t sw64(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
-
-// ------------------------------------------------------------------ K1: q~ = W_K,h^T q_h
-// CTA: 64 hidden requests x 128 columns of d, one head; K = dh (<= 128, multiple of 16).
-// A = q rows [64 x dh] (row-major, K contiguous), B = W_K,h [dh x 128] (row-major K x N ->
-// ldmatrix.trans).  4 warps x 16 rows.
-__global__ void __launch_bounds__(128) qt_kernel(const AbsorbParams p) {
-  __shared__ __align__(128) uint8_t sA[64 * 256];      // 64 rows x dh(<=128) bf16, as 2 x 64-wide halves
-  __shared__ __align__(128) uint8_t sB[128 * 256];     // dh rows x 128 cols bf16, as 2 x 64-wide halves
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n0 = blockIdx.x * 128, h = blockIdx.y, r0 = blockIdx.z * 64;
-  const int dh = p.dh, d = p.d, Hp = p.Hp;
-  if (h >= p.H) {   // padding heads of q~ (rows H..Hp-1 of each request) are zero
-    for (int i = threadIdx.x; i < 64 * 16; i += 128) {
-      const int rr = r0 + (i >> 4);
-      if (rr < p.n_h) reinterpret_cast<uint4*>(p.qt + ((size_t)rr * Hp + h) * d + n0)[i & 15] = make_uint4(0, 0, 0, 0);
-    }
-    return;
-  }
-  const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.q);
-  const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w_int);
-  // A: rows r0.., columns [h*dh, h*dh+dh) of q; half k of 64 columns each
-  for (int i = tid; i < 64 * (dh / 8); i += 128) {
-    const int r = i / (dh / 8), c = i % (dh / 8);
-    const int rr = r0 + r;
-    const bool ok = rr < p.n_h;
-    const int req = ok ? p.hreq[rr] : 0;
-    cp16_zfill(sA + (c >> 3) * (64 * 128) + sw64(r, c & 7), q + (size_t)req * d + h * dh + c * 8, ok);
-  }
-  // B: W_K,h rows k = 0..dh-1 (W_int row h*2dh + k), columns n0..n0+127
-  for (int i = tid; i < dh * 16; i += 128) {
-    const int k = i >> 4, c = i & 15;
-    cp16(sB + (c >> 3) * (128 * 128) + sw64(k, c & 7), w + (size_t)(h * 2 * dh + k) * d + n0 + c * 8);
-  }
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  float acc[16][4];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const int mat = lane >> 3, rr = lane & 7;
-  for (int ks = 0; ks < dh / 16; ++ks) {
-    uint32_t a0, a1, a2, a3;
-    {
-      const int row = warp * 16 + ((mat & 1) << 3) + rr, chunk = 2 * ks + (mat >> 1);
-      ldsm4(saddr(sA) + (chunk >> 3) * (64 * 128) + sw64(row, chunk & 7), a0, a1, a2, a3);
-    }
-#pragma unroll
-    for (int nj = 0; nj < 8; ++nj) {   // 16 columns per ldmatrix.x4.trans
-      const int krow = ks * 16 + ((mat & 1) << 3) + rr, chunk = 2 * nj + (mat >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm4t(saddr(sB) + (chunk >> 3) * (128 * 128) + sw64(krow, chunk & 7), b0, b1, b2, b3);
-      mma(acc[2 * nj], a0, a1, a2, a3, b0, b1);
-      mma(acc[2 * nj + 1], a0, a1, a2, a3, b2, b3);
-    }
-  }
-  if (blockIdx.x == 0 && tid < 64 && r0 + tid < p.n_h) {   // c = q_h . b_K,h (shifts lse only)
-    float c = 0.f;
-    if (p.b_int) {
-      const __nv_bfloat16* qr = q + (size_t)p.hreq[r0 + tid] * d + h * dh;
-      for (int e = 0; e < dh; ++e) c += __bfloat162float(qr[e]) * p.b_int[h * 2 * dh + e];
-    }
-    p.ml[3 * ((size_t)(r0 + tid) * p.H + h) + 2] = c;
-  }
-  const int g = lane >> 2, t4 = lane & 3;
-  __nv_bfloat16* qt = p.qt;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int col = n0 + j * 8 + 2 * t4;
-    const int ra = r0 + warp * 16 + g, rb = ra + 8;
-    if (ra < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)ra * Hp + h) * d + col) = pk(acc[j][0], acc[j][1]);
-    if (rb < p.n_h) *reinterpret_cast<uint32_t*>(qt + ((size_t)rb * Hp + h) * d + col) = pk(acc[j][2], acc[j][3]);
-  }
-}
 
 // ------------------------------------------------------------------ K2: scores on tcgen05
 // CTA: one 128-token tile of one hidden request.  S[128 x Hp] = X_tile q~[r]^T with
@@ -433,7 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN * ST <= 256 ? 3 : (BN == 128 ? 
       ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
       ptx::tmem_ld_wait();
       if (h < H) {
-        uint4* dst = reinterpret_cast<uint4*>(p.z + ((size_t)r * H + h) * d + n0 + c);
+        uint4* dst = reinterpret_cast<uint4*>(p.z + ((size_t)h * p.n_h + r) * d + n0 + c);   // [H][n_h][d]
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           dst[j] = make_uint4(pk(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
@@ -448,86 +357,206 @@ __global__ void __launch_bounds__(TC_THREADS, BN * ST <= 256 ? 3 : (BN == 128 ? 
   if (warp == 1) ptx::tmem_dealloc<BN>(tmem);
 }
 
-// ------------------------------------------------------------------ K5: o = W_V,h z / l + b_V
-constexpr int kST = 4;   // cp.async pipeline depth of K5
-// CTA: 64 hidden requests x dh outputs of one head, K loop over d in 64s.  A = Z[r][h]
-// rows (K contiguous), B = W_V,h [dh x d] rows (N x K, K contiguous -> non-trans).
-__global__ void __launch_bounds__(128) wv_kernel(const AbsorbParams p) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int dh = p.dh, d = p.d, H = p.H;
-  const int stage_bytes = 64 * 128 + dh * 128;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = blockIdx.x, r0 = blockIdx.y * 64;
-  const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(p.w_int);
-  auto load = [&](int kc, int st) {
-    uint8_t* a = sm + st * stage_bytes;
-    uint8_t* b = a + 64 * 128;
-    for (int i = tid; i < 64 * 8; i += 128) {
-      const int row = i >> 3, c = i & 7;
-      const bool ok = r0 + row < p.n_h;
-      cp16_zfill(a + sw64(row, c), p.z + ((size_t)(ok ? r0 + row : 0) * H + h) * d + kc * 64 + c * 8, ok);
-    }
-    for (int i = tid; i < dh * 8; i += 128) {
-      const int e = i >> 3, c = i & 7;
-      cp16(b + sw64(e, c), w + (size_t)(h * 2 * dh + dh + e) * d + kc * 64 + c * 8);
-    }
-  };
-  const int NT = dh / 8;
-  float acc[16][4];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const int KC = d / 64;
-#pragma unroll
-  for (int st = 0; st < kST - 1; ++st) {
-    if (st < KC) load(st, st);
-    cp_commit();
+// ------------------------------------------------------------------ K1: q~ = W_K,h^T q_h on tcgen05
+// CTA: 128 hidden requests x 256 columns of d, one head.  D[128 x 256] = A[128 x dh] B[dh x 256]:
+// A = the requests' q_h rows, gathered by the 4 epilogue warps with cp.async straight into
+// the K-major SWIZZLE_128B layout; B = W_K,h rows (dh x 256 columns, MN-major) by TMA.
+// The blockIdx.x == 0 CTAs also store c = q_h . b_K,h (the score shift that only moves lse).
+template <int DH, int BN>
+__global__ void __launch_bounds__(TC_THREADS, BN == 128 ? 3 : 2)
+    qt_tc_kernel(const __grid_constant__ CUtensorMap tmap_wk, const AbsorbParams p) {
+  constexpr int NCH = DH / 64, A_BYTES = NCH * 128 * 128, B_BYTES = DH * BN * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + B_BYTES);
+  uint64_t* a_full = bars;      // 128 gather threads
+  uint64_t* b_full = bars + 1;  // TMA
+  uint64_t* tfull = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, h = blockIdx.y, r0 = blockIdx.z * 128;
+  const int d = p.d, Hp = p.Hp;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_wk);
+    ptx::mbar_init(a_full, 128);
+    ptx::mbar_init(b_full, 1);
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
   }
-  const int mat = lane >> 3, rr = lane & 7;
-  for (int kc = 0; kc < KC; ++kc) {
-    cp_wait<kST - 2>();
-    __syncthreads();
-    const uint32_t a_s = saddr(sm + (kc % kST) * stage_bytes), b_s = a_s + 64 * 128;
+  if (warp == 1) ptx::tmem_alloc<BN>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.q);
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(b_full, B_BYTES);
+      for (int j = 0; j < BN / 64; ++j)   // W_K,h rows h*2dh .. +dh, 64-column boxes
+        ptx::tma_load_2d(sB + j * DH * 128, &tmap_wk, n0 + 64 * j, h * 2 * DH, b_full);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // A K-major; B MN-major (bit 16), 64-column chunks DH*128 bytes apart
+      const uint32_t idesc = ptx::umma_idesc_bf16_f32(128, BN) | (1u << 16);
+      ptx::mbar_wait(a_full, 0);
+      ptx::mbar_wait(b_full, 0);
+      ptx::tc_fence_after();
+      const uint32_t aa = ptx::smem_u32(sA), bb = ptx::smem_u32(sB);
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      uint32_t a0, a1, a2, a3;
-      ldsm4(a_s + sw64(warp * 16 + ((mat & 1) << 3) + rr, 2 * ks + (mat >> 1)), a0, a1, a2, a3);
+      for (int kk = 0; kk < DH / 16; ++kk)
+        ptx::umma_f16_ss(tmem, ptx::umma_desc_k_sw128(aa + (kk >> 2) * (128 * 128) + (kk & 3) * 32),
+                         ptx::umma_desc_mn_sw128(bb + kk * 2048, DH * 128), idesc, kk != 0 ? 1u : 0u);
+      ptx::umma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3, row = q4 * 32 + lane, r = r0 + row;
+    const bool ok = r < p.n_h;
+    const int req = ok ? p.hreq[r] : 0;
+    // gather: this thread's request row, DH/8 16-byte chunks, swizzled
 #pragma unroll
-      for (int nj = 0; nj < 8; ++nj) {
-        if (2 * nj < NT) {
-          uint32_t b0, b1, b2, b3;
-          ldsm4(b_s + sw64(nj * 16 + ((mat >> 1) << 3) + rr, 2 * ks + (mat & 1)), b0, b1, b2, b3);
-          mma(acc[2 * nj], a0, a1, a2, a3, b0, b1);
-          mma(acc[2 * nj + 1], a0, a1, a2, a3, b2, b3);
+    for (int c = 0; c < DH / 8; ++c)
+      cp16_zfill(sA + (c >> 3) * (128 * 128) + sw64(row, c & 7), q + (size_t)req * d + h * DH + c * 8, ok);
+    cp_commit();
+    cp_wait<0>();
+    ptx::fence_proxy_async_smem();
+    ptx::mbar_arrive(a_full);
+    if (blockIdx.x == 0 && ok) {   // c = q_h . b_K,h
+      float cb = 0.f;
+      if (p.b_int) {
+        const __nv_bfloat16* qr = q + (size_t)req * d + h * DH;
+        for (int e = 0; e < DH; ++e) cb += __bfloat162float(qr[e]) * p.b_int[h * 2 * DH + e];
+      }
+      p.ml[3 * ((size_t)r * p.H + h) + 2] = cb;
+    }
+    ptx::mbar_wait(tfull, 0);
+    ptx::tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q4 * 32) << 16) + c, v);
+      ptx::tmem_ld_wait();
+      if (ok) {
+        uint4* dst = reinterpret_cast<uint4*>(p.qt + ((size_t)r * Hp + h) * d + n0 + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pk(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
+                              pk(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                              pk(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                              pk(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<BN>(tmem);
+}
+
+// ------------------------------------------------------------------ K5: o = W_V,h z / l + b_V on tcgen05
+// CTA: one head x 128 hidden requests.  D[128 x dh] = Z_h [128 x d] W_V,h^T, both operands
+// K-major by TMA (Z is head-major [H][n_h][d], so a head's rows are one block), 6-stage
+// ring over d.  Epilogue: thread = request row: o = D / l + b_V, and lse.
+template <int DH>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    wv_tc_kernel(const __grid_constant__ CUtensorMap tmap_z, const __grid_constant__ CUtensorMap tmap_wv,
+                 const AbsorbParams p) {
+  constexpr int ST = 6, A_BYTES = 128 * 128, STAGE = A_BYTES + DH * 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x, r0 = blockIdx.y * 128, H = p.H, d = p.d;
+  const int KC = d / 64;
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_z);
+    ptx::prefetch_tmap(&tmap_wv);
+    for (int i = 0; i < ST; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<(DH < 32 ? 32 : DH)>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
+        uint8_t* a = smem + stage * STAGE;
+        ptx::tma_load_2d(a, &tmap_z, kc * 64, h * p.n_h + r0, &full[stage]);
+        ptx::tma_load_2d(a + A_BYTES, &tmap_wv, kc * 64, h * 2 * DH + DH, &full[stage]);
+        if (++stage == ST) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
-    const int nk = kc + kST - 1;
-    if (nk < KC) load(nk, nk % kST);
-    cp_commit();
-  }
-  cp_wait<0>();
-  const int g = lane >> 2, t4 = lane & 3;
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::umma_idesc_bf16_f32(128, DH);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t a = ptx::smem_u32(smem + stage * STAGE), b = a + A_BYTES;
 #pragma unroll
-  for (int hr = 0; hr < 2; ++hr) {
-    const int r = r0 + warp * 16 + g + 8 * hr;
-    if (r >= p.n_h) continue;
-    const float* ml = p.ml + 3 * ((size_t)r * H + h);
-    const float inv = 1.f / ml[1];
-    const int req = p.hreq[r];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j >= NT) break;
-      const int e = j * 8 + 2 * t4;
-      float v0 = acc[j][2 * hr] * inv, v1 = acc[j][2 * hr + 1] * inv;
-      if (p.b_int) {
-        v0 += p.b_int[h * 2 * dh + dh + e];
-        v1 += p.b_int[h * 2 * dh + dh + e + 1];
+        for (int k = 0; k < 4; ++k)
+          ptx::umma_f16_ss(tmem, ptx::umma_desc_k_sw128(a + k * 32), ptx::umma_desc_k_sw128(b + k * 32), idesc,
+                           (kc | k) != 0 ? 1u : 0u);
+        ptx::umma_commit(&empty[stage]);
+        if (++stage == ST) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
-      *reinterpret_cast<uint32_t*>(out + (size_t)req * d + h * dh + e) = pk(v0, v1);
+      ptx::umma_commit(tfull);
     }
-    if (t4 == 0 && p.lse) p.lse[(size_t)req * H + h] = (ml[0] + log2f(ml[1])) * 0.69314718055994531f + p.scale * ml[2];
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3, r = r0 + q4 * 32 + lane;
+    ptx::mbar_wait(tfull, 0);
+    ptx::tc_fence_after();
+    const bool ok = r < p.n_h;
+    const float* ml = p.ml + 3 * ((size_t)(ok ? r : 0) * H + h);
+    const float inv = ok ? 1.f / ml[1] : 0.f;
+    const int req = ok ? p.hreq[r] : 0;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + (size_t)req * d + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH; c += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q4 * 32) << 16) + c, v);
+      ptx::tmem_ld_wait();
+      if (ok) {
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          f[j] = __uint_as_float(v[j]) * inv + (p.b_int ? p.b_int[h * 2 * DH + DH + c + j] : 0.f);
+        uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pk(f[8 * j], f[8 * j + 1]), pk(f[8 * j + 2], f[8 * j + 3]), pk(f[8 * j + 4], f[8 * j + 5]),
+                              pk(f[8 * j + 6], f[8 * j + 7]));
+      }
+    }
+    if (ok && p.lse) p.lse[(size_t)req * H + h] = (ml[0] + log2f(ml[1])) * 0.69314718055994531f + p.scale * ml[2];
   }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<(DH < 32 ? 32 : DH)>(tmem);
 }
 
 }  // namespace
@@ -549,8 +578,33 @@ static cudaError_t launch_z(const AbsorbParams& p, const CUtensorMap& tx, const 
   return cudaGetLastError();
 }
 
+template <int DH, int BN>
+static cudaError_t launch_qt(const AbsorbParams& p, const CUtensorMap& twk, cudaStream_t s) {
+  constexpr int smem = 1024 + (DH / 64) * 128 * 128 + DH * BN * 2 + 256;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(qt_tc_kernel<DH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return attr;
+  qt_tc_kernel<DH, BN><<<dim3(p.d / BN, p.H, (p.n_h + 127) / 128), TC_THREADS, smem, s>>>(twk, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || p.Hp == p.H) return e;
+  // padding heads H..Hp-1 of q~ are zero rows (the score GEMM's B operand is Hp rows wide)
+  const size_t row = (size_t)p.d * 2;
+  return cudaMemset2DAsync(p.qt + (size_t)p.H * p.d, p.Hp * row, 0, (size_t)(p.Hp - p.H) * row, p.n_h, s);
+}
+
+template <int DH>
+static cudaError_t launch_wv(const AbsorbParams& p, const CUtensorMap& tz, const CUtensorMap& twv, cudaStream_t s) {
+  constexpr int smem = 1024 + 6 * (128 * 128 + DH * 128) + 256;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(wv_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return attr;
+  wv_tc_kernel<DH><<<dim3(p.H, (p.n_h + 127) / 128), TC_THREADS, smem, s>>>(tz, twv, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
-                            const void* tmap_p, cudaStream_t s) {
+                            const void* tmap_p, const void* tmap_wk, const void* tmap_z, const void* tmap_wv,
+                            cudaStream_t s) {
   if (p.n_h <= 0) return cudaSuccess;
   constexpr int smem_tc = 1024 + 3 * 32768 + 256 + 512;
   static const int zcfg = [] {   // Z GEMM tile width x pipeline depth (A/B knob; default 128x2: 3 CTAs per SM)
@@ -566,14 +620,20 @@ cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const voi
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(score_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s2);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(wv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kST * (64 * 128 + 128 * 128));
     return e;
   }();
   if (attr != cudaSuccess) return attr;
   cudaError_t e;
-  qt_kernel<<<dim3(p.d / 128, p.Hp, (p.n_h + 63) / 64), 128, 0, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const CUtensorMap& twk = *static_cast<const CUtensorMap*>(tmap_wk);
+  static const int qbn = [] {   // q~ GEMM tile width (A/B knob HC_QT_BN; 128 also serves d % 256 != 0)
+    const char* v = std::getenv("HC_QT_BN");
+    return v && std::atoi(v) == 256 ? 256 : 128;
+  }();
+  if (qbn == 256 && p.d % 256 == 0)
+    e = p.dh == 128 ? launch_qt<128, 256>(p, twk, s) : launch_qt<64, 256>(p, twk, s);
+  else
+    e = p.dh == 128 ? launch_qt<128, 128>(p, twk, s) : launch_qt<64, 128>(p, twk, s);
+  if (e != cudaSuccess) return e;
   if (sst == 2)
     score_tc_kernel<2><<<p.n_tiles, TC_THREADS, smem_s2, s>>>(*static_cast<const CUtensorMap*>(tmap_x),
                                                               *static_cast<const CUtensorMap*>(tmap_qt), p);
@@ -593,9 +653,9 @@ cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const voi
     e = launch_z<128, 2>(p, tx, tp, s);
   if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int smem5 = kST * (64 * 128 + p.dh * 128);
-  wv_kernel<<<dim3(p.H, (p.n_h + 63) / 64), 128, smem5, s>>>(p);
-  return cudaGetLastError();
+  const CUtensorMap& tz = *static_cast<const CUtensorMap*>(tmap_z);
+  const CUtensorMap& twv = *static_cast<const CUtensorMap*>(tmap_wv);
+  return p.dh == 128 ? launch_wv<128>(p, tz, twv, s) : launch_wv<64>(p, tz, twv, s);
 }
 
 }  // namespace hc

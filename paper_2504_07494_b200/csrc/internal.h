@@ -191,7 +191,7 @@ struct AbsorbParams {
   __nv_bfloat16* pm;       // [rows][Hp]    2^(scaled score - m_t), m_t = its tile's max
   float* tml;              // [n_tiles][Hp][2] tile max m_t (log2 domain), tile sum l_t
   float* ml;               // [n_h][H][3]   m (log2 domain), l, q_h . b_K,h
-  __nv_bfloat16* z;        // [n_h][H][d]   sum_j 2^(s_j - m) x_j
+  __nv_bfloat16* z;        // [H][n_h][d]   sum_j 2^(s_j - m) x_j (head-major: K5's A operand)
   void* out;               // [n_req, d]
   float* lse;              // nullable [n_req, H]
   int32_t n_h, n_tiles, H, Hp, dh, d, B;
@@ -202,8 +202,11 @@ struct AbsorbParams {
 bool absorb_supported(int dtype, int d, int dh, int H, int B);
 int absorb_launches();
 // tmap_x / tmap_x64: pool rows with {64 x min(B,128)} / {64 x min(B,64)} boxes; tmap_qt:
-// q~ [n_h*Hp, d] with {64 x Hp} boxes; tmap_p: P [rows, Hp] with {64 x 64} boxes.
+// q~ [n_h*Hp, d] with {64 x Hp} boxes; tmap_p: P [rows, Hp] with {64 x 64} boxes; tmap_wk:
+// W_int [2d, d] with {64 x dh} boxes (W_K,h rows, MN-major use) ; tmap_z: Z [H*n_h, d]
+// with {64 x 128} boxes; tmap_wv: W_int with {64 x dh} boxes (W_V,h rows).
 cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
-                            const void* tmap_p, cudaStream_t s);
+                            const void* tmap_p, const void* tmap_wk, const void* tmap_z, const void* tmap_wv,
+                            cudaStream_t s);
 
 }  // namespace hc

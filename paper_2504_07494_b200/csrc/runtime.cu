@@ -882,11 +882,14 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       bp.n_hb = P.n_hb;
       bp.rpb = std::min(B, 128);
       bp.rpb64 = std::min(B, 64);
-      CUtensorMap tm_qt, tm_p;
-      if (!make_tmap_2d(&tm_qt, ws + P.off_qt, (uint64_t)bp.d, (uint64_t)P.n_h * P.Hp, 64, (uint32_t)P.Hp) ||
-          !make_tmap_2d(&tm_p, ws + P.off_pm, (uint64_t)P.Hp, (uint64_t)P.n_hb * B, 64, 64))
+      CUtensorMap tm_qt, tm_p, tm_w, tm_z;
+      const uint64_t dd = (uint64_t)bp.d;
+      if (!make_tmap_2d(&tm_qt, ws + P.off_qt, dd, (uint64_t)P.n_h * P.Hp, 64, (uint32_t)P.Hp) ||
+          !make_tmap_2d(&tm_p, ws + P.off_pm, (uint64_t)P.Hp, (uint64_t)P.n_hb * B, 64, 64) ||
+          !make_tmap_2d(&tm_w, pool->storage + pool->L.w_off, dd, 2 * dd, 64, (uint32_t)bp.dh) ||
+          !make_tmap_2d(&tm_z, ws + P.off_z, dd, (uint64_t)H * P.n_h, 64, 128))
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (absorbed path)");
-      err = launch_absorbed(bp, &pool->tmap_x, &pool->tmap_x64, &tm_qt, &tm_p, s);
+      err = launch_absorbed(bp, &pool->tmap_x, &pool->tmap_x64, &tm_qt, &tm_p, &tm_w, &tm_z, &tm_w, s);
       if (err != cudaSuccess) return cuda_fail(err, "absorbed hidden attention");
       launches += absorb_launches();
     }
