@@ -143,7 +143,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.n_hblocks = rp.n_hblocks;
   a.B = rp.B;
   a.M = rp.n_hblocks * rp.B;
-  a.rows_per_box = rp.B < 128 ? rp.B : 128;
+  a.rows_per_box = (rp.B < 128 && !std::getenv("HC_DIAG_BOX")) ? rp.B : 128;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
   a.n_tiles = 2 * rp.d / PC::TILE_N;
   a.k_iters = rp.d / pg::BK;
@@ -157,8 +157,16 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.row_pos = rp.hblk_pos;
   a.group_m = -2;
   a.l2_hint = 0;
-  a.sync_w = 8;
-  a.sync = (num_sms / 2 <= pg::kMaxSyncPairs) ? rp.sync_counter : nullptr;
+  // Partner lockstep off by default in the fused kernel: with the attend epilogue, tiles of
+  // partner pairs finish at different times and the spin costs more than the L2 reuse buys
+  // (same-box A/B: cfg4 -2.5%, cfg3 -2%, cfg2 -1%, crossover neutral).
+  // HC_SYNC_W=<w> re-enables it with window w (the stand-alone GEMM keeps w = 8).
+  a.sync_w = 0;
+  a.sync = nullptr;
+  if (const char* sw = std::getenv("HC_SYNC_W")) {
+    a.sync_w = std::atoi(sw);
+    if (a.sync_w > 0 && num_sms / 2 <= pg::kMaxSyncPairs) a.sync = rp.sync_counter;
+  }
   if (rp.epi_attend) {   // hidden rows become partials in the GEMM epilogue: no hidden tasks
     a.epi = pg::EPI_ATTEND;
     a.hblk_req = rp.hblk_req;
@@ -170,6 +178,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     a.scale_log2 = rp.scale_log2;
     a.seg = rp.seg;
     tile_done = nullptr;
+    const char* de = std::getenv("HC_DIAG_EPI");
+    a.diag = de ? std::atoi(de) : 0;
   }
   a.tile_done = tile_done;
   ap_.tile_done = tile_done;

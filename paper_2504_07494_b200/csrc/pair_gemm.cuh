@@ -63,6 +63,7 @@ struct TcArgs {
   int32_t n_splits_all;
   float scale_log2;
   int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
+  int32_t diag;             // timing diagnostic only (HC_DIAG_EPI=1): skip the EPI_ATTEND math
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -484,6 +485,12 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       ptx::tc_fence_after();
       const int grow = mt * P_BM + row_in_tile;
       if (a.epi == EPI_ATTEND) {
+        if (a.diag == 1) {   // timing diagnostic (wrong outputs): release the accumulator untouched
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          continue;
+        }
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
         if (a.seg == 8)
           attend_tile<8, PC::TILE_N>(a, tacc, nt, grow, lane);

@@ -467,7 +467,8 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     }
     if (cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) &&
         recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)) {
-      const uint32_t rpb = (uint32_t)std::min(cfg->block_size, 128);
+      // HC_DIAG_BOX=1 (timing diagnostic only, wrong results): 128-row A boxes as if dense
+      const uint32_t rpb = std::getenv("HC_DIAG_BOX") ? 128u : (uint32_t)std::min(cfg->block_size, 128);
       const bool ok1 = make_tmap_2d(&p->tmap_x, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
                                     (uint64_t)cfg->num_blocks * cfg->block_size, 64, rpb);
       const bool ok2 = make_tmap_2d(&p->tmap_w, p->storage + L.w_off, (uint64_t)cfg->d_model,
