@@ -219,21 +219,26 @@ struct SegReduceScatter<0, CNT> {
   static __device__ __forceinline__ void run(float*, int) {}
 };
 
-__device__ __forceinline__ float dot32_bf16(const float (&f)[32], const __nv_bfloat16* q) {
+// q chunk (32 bf16) for a dot with a TMEM chunk: loaded BEFORE the tcgen05.ld so the L1/L2
+// latency overlaps the TMEM load; four independent FMA chains (chain length 8, not 32).
+__device__ __forceinline__ void load_q32(const __nv_bfloat16* q, uint4 (&u)[4]) {
   const uint4* q4 = reinterpret_cast<const uint4*>(q);
-  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) u[j] = __ldg(q4 + j);
+}
+__device__ __forceinline__ float dot32_q(const float (&f)[32], const uint4 (&u)[4]) {
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint4 u = __ldg(q4 + j);
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 v = __bfloat1622float2(b[e]);
-      s = fmaf(f[8 * j + 2 * e], v.x, s);
-      s = fmaf(f[8 * j + 2 * e + 1], v.y, s);
+      s[e] = fmaf(f[8 * j + 2 * e], v.x, s[e]);
+      s[e] = fmaf(f[8 * j + 2 * e + 1], v.y, s[e]);
     }
   }
-  return s;
+  return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 // One pair tile's rows -> partials.  Thread = GEMM row (a token of a hidden block); the
@@ -267,18 +272,23 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
     if (a.rope_inv != nullptr) {
 #pragma unroll 1
       for (int c0 = 0; c0 < dh / 2; c0 += 32) {
+        uint4 qa[4], qb[4];
+        load_q32(qh + c0, qa);
+        load_q32(qh + c0 + dh / 2, qb);
         float f[32], f2[32];
         load_chunk(tk + c0, a.bias, nk + c0, f);
         load_chunk(tk + c0 + dh / 2, a.bias, nk + c0 + dh / 2, f2);
         rope_rotate(f, f2, tok, a.rope_inv + c0);
-        s += dot32_bf16(f, qh + c0) + dot32_bf16(f2, qh + c0 + dh / 2);
+        s += dot32_q(f, qa) + dot32_q(f2, qb);
       }
     } else {
 #pragma unroll 1
       for (int c0 = 0; c0 < dh; c0 += 32) {
+        uint4 qa[4];
+        load_q32(qh + c0, qa);
         float f[32];
         load_chunk(tk + c0, a.bias, nk + c0, f);
-        s += dot32_bf16(f, qh + c0);
+        s += dot32_q(f, qa);
       }
     }
     s = live ? s * a.scale_log2 : -INFINITY;
@@ -392,6 +402,7 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
           } else {
             const int g = grow / a.B;
             s.prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
+            if (a.diag == 3 && i > 0) s.prow[i] = s.prow[0] + i * a.rows_per_box;   // timing diagnostic
           }
         }
         const int wrow = nt * PC::TILE_N + (int)rank * 128;
