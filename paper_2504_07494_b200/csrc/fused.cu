@@ -155,7 +155,11 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.bias = rp.b_int;
   a.rope_inv = rp.rope_inv;
   a.row_pos = rp.hblk_pos;
-  a.group_m = -2;
+  // n-major raster, 4 n-tiles per group: four pairs of a wave share each A panel (same-box
+  // A/B vs 2: cfg4 -2.5%, cfg5 1/32 -2..-4%)
+  a.group_m = -4;
+  if (const char* gn = std::getenv("HC_GROUP_N"))   // A/B knob: n-tiles per raster group (>= 1)
+    if (std::atoi(gn) >= 1) a.group_m = -std::atoi(gn);
   a.l2_hint = 0;
   // Partner lockstep off by default in the fused kernel: with the attend epilogue, tiles of
   // partner pairs finish at different times and the spin costs more than the L2 reuse buys
