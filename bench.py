@@ -80,7 +80,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region: samples from nvidia-smi's start-up (its first NVML
+        queries can stall CUDA calls) and from warm-up are dropped; the sampler is started
+        before warm-up so that start-up never lands inside the timed region."""
+        self.t0 = time.time()
 
     def stop(self):
         if self.proc is None:
@@ -93,7 +99,10 @@ class ClockSampler:
         self.t.join(timeout=2)
         sms, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = getattr(self, "t0", 0.0)
+        for ts, ln in self.lines:
+            if ts < t0:
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -329,14 +338,14 @@ def main():
         torch.cuda.synchronize()
         return 0
 
+    sampler = ClockSampler(local)
+    sampler.start()   # before warm-up: nvidia-smi's start-up stays out of the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches_per_step = pool.last_launch_count()
     decode_path = pool.last_decode_path()
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
+    sampler.mark()
     pool.set_profiling(True)
     pool.kernel_times()  # clear
     if world > 1:
@@ -354,9 +363,11 @@ def main():
     kt = pool.kernel_times()
     pool.set_profiling(False)
     ms = evs[0].elapsed_time(evs[-1]) / args.steps
-    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    per_step_raw = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    per_step = sorted(per_step_raw)
     pct = {"p10": per_step[int(0.1 * (len(per_step) - 1))], "p50": statistics.median(per_step),
-           "p90": per_step[int(0.9 * (len(per_step) - 1))]}
+           "p90": per_step[int(0.9 * (len(per_step) - 1))], "max": per_step[-1],
+           "max_step": per_step_raw.index(per_step[-1])}
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -551,12 +562,13 @@ def run_module_mode(args, rank, world, local):
         flops = 8 * nreq * L * d * d + 2 * nreq * L * L * d
         n_layer = nreq * L
         unit, metric = "tokens/s", "prefill-layer tokens/s (projections + causal attention + W_O)"
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
     time.sleep(0.3)
+    sampler.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
