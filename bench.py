@@ -91,6 +91,8 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return None
+        t1 = time.time()
+        time.sleep(0.12)   # one more sample period, for timed regions shorter than 100 ms
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -100,9 +102,12 @@ class ClockSampler:
         sms, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         t0 = getattr(self, "t0", 0.0)
-        for ts, ln in self.lines:
-            if ts < t0:
-                continue
+        window = "timed region"
+        lines = [(ts, ln) for ts, ln in self.lines if t0 <= ts <= t1 + 0.01]
+        if not lines:   # timed region shorter than the 100 ms sample period
+            lines = [(ts, ln) for ts, ln in self.lines if t0 - 0.15 <= ts <= t1 + 0.15]
+            window = "timed region +-150 ms (region shorter than the 100 ms sample period)"
+        for ts, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -121,7 +126,7 @@ class ClockSampler:
         if not sms:
             return None
         return {"sm_mhz": statistics.median(sms), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sms), "power_w": statistics.median(pw) if pw else None}
+                "samples": len(sms), "power_w": statistics.median(pw) if pw else None, "window": window}
 
 
 # ============================================================================ reference arm
