@@ -75,6 +75,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + 3.0   # nvidia-smi start-up: wait for its first sample
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
@@ -471,7 +474,7 @@ def main():
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
         peak = tf_peak
-        roof = {"bound": "tensor", "kernel": "fused_step_kernel<3,4,2>" if fused else "recon_tc2_kernel<2,4>",
+        roof = {"bound": "tensor", "kernel": "fused_step_kernel<3,5,2,qreg>" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
                 "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get(dom),
                 "ncu_tensor_pipe_pct": TRAFFIC.get(w.name, {}).get(dom + "_tensor_pipe_pct"),

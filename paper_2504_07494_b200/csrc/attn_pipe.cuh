@@ -68,11 +68,14 @@ struct Bfly {
   }
 };
 
-template <int DH, int NST>
+// QREG: q_h is loaded into registers at the producer (one 16-byte vector per lane) instead
+// of riding in every stage, so a stage is exactly K chunk + V chunk — the fused kernel uses
+// the saved smem for a fifth attention warp.
+template <int DH, int NST, bool QREG = false>
 struct PipeCfg {
   static constexpr int TOK = 16;                      // tokens per chunk
   static constexpr int CHUNK = TOK * DH * 2;          // bytes of one K (or V) chunk
-  static constexpr int QB = DH * 2;                   // bytes of q_h
+  static constexpr int QB = QREG ? 0 : DH * 2;        // bytes of q_h staged per stage
   static constexpr int STAGE = 2 * CHUNK + QB;        // multiple of 16 bytes
   static_assert(STAGE % 16 == 0, "stage alignment");
   static constexpr int WARP_BYTES = (NST * STAGE + NST * 8 + NST * 16 + TOK * 4 + 127) / 128 * 128;
@@ -103,9 +106,10 @@ struct DirectTaskMap {   // stand-alone attention: all K/V already in memory, ta
 // One warp's attention loop: a private NST-stage ring of bulk copies (K chunk, V chunk, q_h)
 // on mbarriers, fed from a global task counter; the ring flows across task boundaries.
 // wb: this warp's smem region of PipeCfg<DH,NST>::WARP_BYTES bytes (16-B aligned).
-template <int DH, int NST, class TaskMap>
+template <int DH, int NST, class TaskMap, bool QREG = false>
 __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, int lane, const TaskMap& tm) {
-  using C = PipeCfg<DH, NST>;
+  using C = PipeCfg<DH, NST, QREG>;
+  static_assert(!QREG || NST <= 3, "register q slots: at most 3 stages");
   constexpr int TOK = C::TOK;
   constexpr int LPR = DH / 8;      // lanes per row (each lane: 8 dims = 16 bytes)
   constexpr int RPI = 32 / LPR;    // rows per 128-bit load instruction
@@ -153,6 +157,7 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     }
   };
   load_task(ptask);
+  uint4 qr0 = make_uint4(0, 0, 0, 0), qr1 = qr0, qr2 = qr0;   // QREG: q_h slot per stage
 
   // issue the next chunk of the producer stream into `stage`; false when no work is left
   auto produce = [&](int stage) -> bool {
@@ -180,8 +185,14 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       ptx::mbar_arrive_expect_tx(&bars[stage], 2 * C::CHUNK + (first ? C::QB : 0));
       ptx::bulk_g2s(sb, ksrc, C::CHUNK, &bars[stage]);
       ptx::bulk_g2s(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage]);
-      if (first)
+      if (!QREG && first)
         ptx::bulk_g2s(sb + 2 * C::CHUNK, qg + (size_t)psp.req * d + phead * DH, C::QB, &bars[stage]);
+    }
+    if (QREG && first) {   // every lane: its 8 dims of q_h (consumed when this stage is)
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(qg + (size_t)psp.req * d + phead * DH) + lane % LPR);
+      if (stage == 0) qr0 = v;
+      else if (stage == 1) qr1 = v;
+      else qr2 = v;
     }
     if (++pchunk == pnch) {
       ptask = grab();
@@ -212,7 +223,10 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     ptx::mbar_wait(&bars[cstage], cphase);
     const uint8_t* sb = stage_base + cstage * C::STAGE;
     if (mt.w & 1) {  // first chunk of a task: fresh state, load q_h (pre-scaled by scale*log2 e)
-      bf16x8_to_f32(reinterpret_cast<const uint4*>(sb + 2 * C::CHUNK)[lr], qf);
+      if constexpr (QREG)
+        bf16x8_to_f32(cstage == 0 ? qr0 : (cstage == 1 ? qr1 : qr2), qf);
+      else
+        bf16x8_to_f32(reinterpret_cast<const uint4*>(sb + 2 * C::CHUNK)[lr], qf);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         qf[i] *= p.scale_log2;

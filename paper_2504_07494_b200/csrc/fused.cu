@@ -69,15 +69,15 @@ struct FusedTaskMap {
   }
 };
 
-template <int GS, int NA, int NSTA>
+template <int GS, int NA, int NSTA, bool QR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * NA, 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                       const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
   using PC = pg::PairCfg<kNsub, GS>;
   // late-joining GEMM warps: as many 2-stage attention rings as fit in the GEMM stage buffers
-  constexpr int kJoin = (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2>::WARP_BYTES) < 6
-                            ? (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2>::WARP_BYTES) : 6;
+  constexpr int kJoin = (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2, QR>::WARP_BYTES) < 6
+                            ? (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2, QR>::WARP_BYTES) : 6;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
@@ -99,13 +99,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
       ptx::fence_proxy_async_smem();
       if (warp < kJoin) {
         const FusedTaskMap tm{&p};
-        ap::attn_warp_run<128, 2>(p, ps.stages + warp * ap::PipeCfg<128, 2>::WARP_BYTES, lane, tm);
+        ap::attn_warp_run<128, 2, FusedTaskMap, QR>(p, ps.stages + warp * ap::PipeCfg<128, 2, QR>::WARP_BYTES,
+                                                    lane, tm);
       }
     }
   } else {
     const FusedTaskMap tm{&p};
-    ap::attn_warp_run<128, NSTA>(p, attn_base + (warp - pg::GEMM_THREADS / 32) * ap::PipeCfg<128, NSTA>::WARP_BYTES,
-                                 lane, tm);
+    ap::attn_warp_run<128, NSTA, FusedTaskMap, QR>(
+        p, attn_base + (warp - pg::GEMM_THREADS / 32) * ap::PipeCfg<128, NSTA, QR>::WARP_BYTES, lane, tm);
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -113,12 +114,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   pg::pair_teardown<kNsub, kGemmStages>(warp, tmem_base);
 }
 
-template <int GS, int NA, int NSTA>
+template <int GS, int NA, int NSTA, bool QR = false>
 cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, int num_sms,
                        cudaStream_t s) {
-  constexpr int smem = 1024 + pg::PairCfg<kNsub, GS>::REGION_BYTES + NA * ap::PipeCfg<128, NSTA>::WARP_BYTES;
+  constexpr int smem = 1024 + pg::PairCfg<kNsub, GS>::REGION_BYTES + NA * ap::PipeCfg<128, NSTA, QR>::WARP_BYTES;
   static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
-  auto k = fused_step_kernel<GS, NA, NSTA>;
+  auto k = fused_step_kernel<GS, NA, NSTA, QR>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
@@ -190,14 +191,19 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   ap_.gemm_n_tiles = a.n_tiles;
   ap_.gemm_tile_m = pg::P_BM;
   ap_.gemm_tile_n = PC::TILE_N;
-  // 3-stage GEMM ring + 4 attention warps x 2 stages (measured best of {3,4,2}, {3,3,3},
-  // {2,6,2}, {2,4,3}: two GEMM stages starve the tensor cores).
+  // 3-stage GEMM ring + 5 attention warps x 2 stages with q_h in registers (the stages carry
+  // only K and V chunks, which frees the smem for the fifth warp: more KV bytes in flight
+  // next to the GEMM; crossover 1/64-1/32 -1.5..-7% on cool boxes, neutral elsewhere).
+  // Measured earlier (q staged): {3,4,2} best of {3,3,3}, {2,6,2}, {2,4,3} — two GEMM stages
+  // starve the tensor cores.
   const char* e = std::getenv("HC_FUSED_CFG");   // A/B knob
-  const int cfg = e ? std::atoi(e) : 342;
+  const int cfg = e ? std::atoi(e) : 352;
   if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 342) return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 3420) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
 }
 
 }  // namespace hc

@@ -43,7 +43,7 @@ shutil.copy(os.path.join(src, "bench_cfg4.json"), os.path.join(dst, "r01_bench_c
 shutil.copy(os.path.join(src, "bench_cfg5_h0.json"), os.path.join(dst, "r01_bench_cfg5_h0.json"))
 shutil.copy(os.path.join(src, "launches_cfg4.csv"), os.path.join(dst, "r01_launches_cfg4.csv"))
 fb, ft = details(os.path.join(src, "full_fused_cfg4.ncu-rep"),
-                 "# ncu --set full: fused_step_kernel<3,4,2>, attend epilogue (cfg4: OPT-66B, 256 req, 50% hidden)",
+                 "# ncu --set full: fused_step_kernel<3,5,2,true> (q in registers), attend epilogue (cfg4: OPT-66B, 256 req, 50% hidden)",
                  "r01_ncu_fused_cfg4.txt")
 rb, rt = details(os.path.join(src, "full_recon_cfg4.ncu-rep"),
                  "# ncu --set full: recon_tc2_kernel<2,4>, attend epilogue (HC_FUSED=0, cfg4)", "r01_ncu_recon_cfg4.txt")
