@@ -598,7 +598,8 @@ def run_module_mode(args, rank, world, local):
                          "peak_kind": ("bf16 sustained (power-capped run), " if capped
                                        else "bf16 burst (clock held max), ") + peak_src},
             "tensor_TFLOPs": achieved, "frac_of_sustained_bf16": achieved / tf,
-            "gpu_launches_per_step": pool.last_launch_count(), "clocks": clocks}
+            "gpu_launches_per_step": pool.last_launch_count(),
+            "gpu_launches": pool.last_launch_count() * args.steps, "clocks": clocks}
     print(json.dumps(line), flush=True)
     return 0
 
