@@ -496,7 +496,16 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       ptx::tc_fence_after();
       const int grow = mt * P_BM + row_in_tile;
       if (a.epi == EPI_ATTEND) {
-        if (a.diag == 1) {   // timing diagnostic (wrong outputs): release the accumulator untouched
+        if (a.diag == 1 || a.diag == 2) {   // timing diagnostics (wrong outputs)
+          if (a.diag == 2) {   // read the whole accumulator from TMEM, skip the math
+            float f[32], sum = 0.f;
+            for (int c = 0; c < PC::TILE_N / 32; ++c) {
+              load_chunk(tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N + c * 32, nullptr, 0, f);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sum += f[j];
+            }
+            if (sum == 12345.f) a.part_ml[0] = sum;
+          }
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
