@@ -274,6 +274,7 @@ def main():
                          "timed region (north_star's output gather; not a data-path exchange)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay variant")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run only N untimed steps (for ncu); prints nothing")
     args = ap.parse_args()
@@ -382,6 +383,33 @@ def main():
         ms = float(t.item())
     n_total = len(w0.n) if args.strong else world * n_req
     value = n_total / (ms / 1e3)
+
+    # ---- CUDA-graph variant: one hc_decode_attention call (descriptor H2D
+    # copy from the runtime's pinned staging buffer + kernels) captured once and replayed —
+    # valid while the batch (ids, cache contents) is fixed, as in this loop; kernel-side
+    # work is identical, only host launch overhead goes away.
+    graph = None
+    if world == 1 and not args.no_graph:
+        try:
+            gr = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gr, capture_error_mode="relaxed"):
+                hc.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, torch.cuda.current_stream())
+            for _ in range(2):
+                gr.replay()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            for _ in range(args.steps):
+                gr.replay()
+            g1.record()
+            torch.cuda.synchronize()
+            ms_g = g0.elapsed_time(g1) / args.steps
+            graph = {"value": n_total / (ms_g / 1e3), "unit": "req-layers/s", "ms_per_step": ms_g,
+                     "note": "one decode call captured as a CUDA graph and replayed (fixed batch)"}
+            del gr
+        except Exception as ex:   # report, never fall back silently
+            graph = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # ---- end to end through the public API: pinned host q -> device, decode, out -> host
     e2e = None
@@ -505,6 +533,7 @@ def main():
         "kernels": kernels,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,
+        "cuda_graph": graph,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

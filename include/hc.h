@@ -156,7 +156,12 @@ size_t hc_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_
  * Hidden-mode K/V are rebuilt by a tcgen05 GEMM (bf16 in, fp32 accumulate, bf16 out),
  * then one split-K flash-decoding pass covers KV- and hidden-mode requests, then a
  * split combine.  n_req = 0 is HC_OK and launches nothing.  Errors: HC_E_INVALID,
- * HC_E_UNKNOWN_REQ, HC_E_WORKSPACE, HC_E_UNSUPPORTED, HC_E_CUDA. */
+ * HC_E_UNKNOWN_REQ, HC_E_WORKSPACE, HC_E_UNSUPPORTED, HC_E_CUDA.
+ * CUDA graphs: the call may be stream-captured (relaxed capture mode).  The descriptor is
+ * built on the host at capture time and its pinned staging buffer is retired from the
+ * runtime's 16-slot ring, so every replay recomputes exactly the captured batch (same
+ * ids, tables, q/out/lse/workspace pointers) until hc_pool_destroy; appends after the
+ * capture are not seen by replays.  HC_E_CUDA once all 16 slots are held by captures. */
 hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
                               const void* q, float scale, void* out, float* lse,
                               void* workspace, size_t ws_bytes, void* stream);

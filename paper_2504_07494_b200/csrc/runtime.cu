@@ -154,6 +154,8 @@ struct Pinned {
   size_t cap = 0;
   cudaEvent_t ev = nullptr;
   bool pending = false;
+  bool captured = false;   // used by a call captured into a CUDA graph: the graph's memcpy node
+                           // reads this buffer at every replay, so it leaves the rotation
 };
 
 // Decode-call plan: sizes and offsets inside the caller's workspace.
@@ -202,7 +204,7 @@ struct hc_pool {
   ~hc_pool() {
     for (auto& p : ring) {
       if (p.ev) {
-        cudaEventSynchronize(p.ev);
+        if (p.pending) cudaEventSynchronize(p.ev);
         cudaEventDestroy(p.ev);
       }
       if (p.ptr) cudaFreeHost(p.ptr);
@@ -214,8 +216,13 @@ struct hc_pool {
 
   // pinned staging buffer of >= bytes; waits only if its previous copy is still queued
   Pinned* pinned(size_t bytes) {
-    Pinned* p = &ring[ring_next];
-    ring_next = (ring_next + 1) % kRing;
+    Pinned* p = nullptr;
+    for (int i = 0; i < kRing && p == nullptr; ++i) {   // skip slots owned by captured graphs
+      Pinned* c = &ring[ring_next];
+      ring_next = (ring_next + 1) % kRing;
+      if (!c->captured) p = c;
+    }
+    if (p == nullptr) return nullptr;
     if (p->pending) {
       cudaEventSynchronize(p->ev);
       p->pending = false;
@@ -227,6 +234,7 @@ struct hc_pool {
       size_t cap = std::max<size_t>(bytes, 1 << 16);
       cap = align_up(cap + cap / 2, 4096);
       for (auto& r : ring) {
+        if (r.captured) continue;
         if (r.pending) {
           cudaEventSynchronize(r.ev);
           r.pending = false;
@@ -244,6 +252,20 @@ struct hc_pool {
     }
     if (!p->ev && cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
     return p;
+  }
+
+  // After the H2D copy from `p` is enqueued on `s`: remember when the buffer is free again.
+  // Under stream capture the copy becomes a graph node that re-reads the buffer at every
+  // replay, so the slot is retired from the ring instead (kept until the pool is destroyed).
+  void staged(Pinned* p, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      p->captured = true;
+      p->pending = false;
+      return;
+    }
+    cudaEventRecord(p->ev, s);
+    p->pending = true;
   }
 
   cudaEvent_t get_event() {
@@ -568,7 +590,7 @@ static hc_status scatter_rows(hc_pool* pool, const std::vector<AppendReq>& ar, c
     }
     if (bytes_req + bytes_tab > kStagingBytes / 2) return fail(HC_E_UNSUPPORTED, "append descriptor too large");
     Pinned* pin = pool->pinned(bytes_req + bytes_tab);
-    if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+    if (!pin) return fail(HC_E_CUDA, "pinned staging unavailable (cudaMallocHost failed, or all slots held by captured graphs)");
     AppendReq* hr = static_cast<AppendReq*>(pin->ptr);
     for (size_t i = i0; i < i1; ++i) {
       hr[i - i0] = ar[i];
@@ -577,8 +599,7 @@ static hc_status scatter_rows(hc_pool* pool, const std::vector<AppendReq>& ar, c
     std::memcpy(static_cast<char*>(pin->ptr) + bytes_req, tabs.data() + tab_lo, bytes_tab);
     cudaError_t err = cudaMemcpyAsync(staging, pin->ptr, bytes_req + bytes_tab, cudaMemcpyHostToDevice, s);
     if (err != cudaSuccess) return cuda_fail(err, "append descriptor upload");
-    cudaEventRecord(pin->ev, s);
-    pin->pending = true;
+    pool->staged(pin, s);
     AppendParams ap;
     ap.reqs = reinterpret_cast<const AppendReq*>(staging);
     ap.tabs = reinterpret_cast<const int32_t*>(staging + bytes_req);
@@ -721,7 +742,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
 
   // ---- descriptor (a3): requests, split-K work list, KV block tables, hidden gather list
   Pinned* pin = pool->pinned(P.desc_bytes);
-  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  if (!pin) return fail(HC_E_CUDA, "pinned staging unavailable (cudaMallocHost failed, or all slots held by captured graphs)");
   char* h = static_cast<char*>(pin->ptr);
   std::memset(h, 0, kHeaderBytes);  // attention task counter and GEMM progress words = 0
   ReqDesc* rd = reinterpret_cast<ReqDesc*>(h + P.off_reqs);
@@ -811,8 +832,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   char* ws = static_cast<char*>(workspace);
   cudaError_t err = cudaMemcpyAsync(ws, h, P.desc_bytes, cudaMemcpyHostToDevice, s);
   if (err != cudaSuccess) return cuda_fail(err, "descriptor upload");
-  cudaEventRecord(pin->ev, s);
-  pin->pending = true;
+  pool->staged(pin, s);
   if (pool->profiling) cudaEventRecord(ev[1], s);
 
   char* blocks = pool->storage + pool->L.blocks_off;
@@ -1014,12 +1034,11 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   if (rd_bytes > kStagingBytes / 2) return fail(HC_E_UNSUPPORTED, "batch too large for the staging area");
   char* rd_dev = pool->storage + pool->L.stage_off + kStagingBytes / 2;
   Pinned* pin = pool->pinned(rd_bytes);
-  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  if (!pin) return fail(HC_E_CUDA, "pinned staging unavailable (cudaMallocHost failed, or all slots held by captured graphs)");
   std::memcpy(pin->ptr, row_dst.data(), rd_bytes);
   cudaError_t err = cudaMemcpyAsync(rd_dev, pin->ptr, rd_bytes, cudaMemcpyHostToDevice, s);
   if (err != cudaSuccess) return cuda_fail(err, "projection descriptor upload");
-  cudaEventRecord(pin->ev, s);
-  pin->pending = true;
+  pool->staged(pin, s);
   DenseParams dp{};
   dp.a = x;
   dp.w = pool->storage + pool->L.wq_off;
@@ -1240,7 +1259,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   // host descriptor: per-row cache targets (KV rows), request row offsets, query tiles
   const size_t desc_bytes = P.total - P.off_rowdst;
   Pinned* pin = pool->pinned(desc_bytes);
-  if (!pin) return fail(HC_E_CUDA, "pinned staging allocation failed");
+  if (!pin) return fail(HC_E_CUDA, "pinned staging unavailable (cudaMallocHost failed, or all slots held by captured graphs)");
   char* hbase = static_cast<char*>(pin->ptr);
   std::memset(hbase, 0, desc_bytes);
   int32_t* rowdst = reinterpret_cast<int32_t*>(hbase);
@@ -1289,8 +1308,7 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   char* ws = static_cast<char*>(workspace);
   cudaError_t err = cudaMemcpyAsync(ws + P.off_rowdst, hbase, desc_bytes, cudaMemcpyHostToDevice, s);
   if (err != cudaSuccess) return cuda_fail(err, "prefill descriptor upload");
-  cudaEventRecord(pin->ev, s);
-  pin->pending = true;
+  pool->staged(pin, s);
   int launches = 0;
   if (pool->L.has_ln) {   // u = LN(x): the projections' input and what the hidden cache holds (R15)
     const float* gb = reinterpret_cast<const float*>(pool->storage + pool->L.ln_off);

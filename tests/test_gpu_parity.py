@@ -308,6 +308,36 @@ def test_fused_schedules_agree_bitwise(hc, monkeypatch, env):
     assert np.array_equal(a, b) and np.array_equal(la, lb)
 
 
+def test_cuda_graph_replay_bitwise(hc):
+    """One decode call (descriptor upload from the runtime's pinned staging buffer + the
+    fused kernel + combine) captured as a CUDA graph: replays equal the eager call bit for
+    bit while the batch is fixed (bench.py's `cuda_graph` variant)."""
+    from paper_2504_07494_b200 import hc as H
+    n = [700, 33, 511, 1, 257, 96, 129, 64]
+    modes = [MODE_HIDDEN if i % 3 != 1 else MODE_KV for i in range(len(n))]
+    w = _bf16_workload(1024, 8, 128, 16, n=n, modes=modes, bias=True)
+    pool = T.make_pool(w)
+    T.fill(pool, w)
+    q = T.queries(w)
+    ids = list(w.req_ids)
+    ws = pool.workspace(ids)
+    out = torch.empty((len(n), w.shape.d), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((len(n), w.shape.H), dtype=torch.float32, device="cuda")
+    H.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    ref_out, ref_lse = out.clone(), lse.clone()
+    out.zero_()
+    lse.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="relaxed"):
+        H.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, torch.cuda.current_stream())
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_out) and torch.equal(lse, ref_lse)
+
+
 # ------------------------------------------------------------------ attention layer (NEXT row f1)
 LAYER_CASES = [
     ("tiny-f32", None),
