@@ -1,4 +1,39 @@
-# Round 1 profile summary (B200, sm_100a) — end of round
+"""Regenerate profiles/r01_summary.md from the committed profile files."""
+import json
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+
+
+def line(f):
+    return json.loads(open(os.path.join(P, f)).read().strip().splitlines()[-1])
+
+
+def ncu(f):
+    d = {}
+    for ln in open(os.path.join(P, f)):
+        p = ln.rstrip("\n").split("\t")
+        if len(p) == 3:
+            d[p[1]] = p[2]
+    return d
+
+
+def row(name, d):
+    r, c = d["roofline"], d["clocks"]
+    kind = "sustained" if "sustained" in r.get("peak_kind", "") else ("burst" if r["unit"] == "TFLOP/s" else "copy BW")
+    return (f"| {name} | {d['ms_per_step']:.3f} | {d['step_ms_percentiles']['p50']:.3f} | {d['value']:.0f} | "
+            f"{(d.get('cuda_graph') or {}).get('ms_per_step', float('nan')):.3f} | {r['kernel']} | "
+            f"{r['achieved']:.0f} {r['unit']} | {r['frac']:.3f} ({kind}) | {d['step_roofline']['frac']:.3f} | "
+            f"{c['sm_mhz']:.0f} MHz, {','.join(c['reasons']) or 'none'} |")
+
+
+c4, c3, c2, h0 = (line(f"r01_bench_{x}.json") for x in ("cfg4", "cfg3", "cfg2", "cfg5_h0"))
+sw = json.load(open(os.path.join(P, "r01_cfg5_sweep.json")))
+cub = json.load(open(os.path.join(P, "r01_cublas_same_shapes.json")))
+l2 = [json.loads(x) for x in open(os.path.join(P, "r01_l2_fabric_bw.jsonl"))]
+cb = c4["cpu_baseline"]
+txt = f"""# Round 1 profile summary (B200, sm_100a) — end of round
 
 Peaks: MEASURED_PEAKS.json (re-measured this round) — HBM copy 6543 GB/s; bf16 cuBLAS
 1658.7 TF/s burst, 1375.6 TF/s sustained. All timings: CUDA events inside `bench.py`'s
@@ -14,13 +49,13 @@ Regenerate with `python scripts/make_summary.py`.
 
 | workload | ms/step | p50 | req-layers/s | CUDA-graph ms | dominant kernel | achieved | frac of measured peak | step T_roof/T | clocks |
 |---|---|---|---|---|---|---|---|---|---|
-| cfg4 OPT-66B, 256 req, 50% hidden | 41.201 | 41.038 | 6213 | 41.075 | fused_step_kernel<3,5,2,qreg> | 1322 TFLOP/s | 0.961 (sustained) | 0.955 | 1387 MHz, sw_power_cap |
-| cfg3 OPT-30B, 128 req, planner modes | 3.761 | 3.845 | 33772 | 3.700 | fused_step_kernel<3,5,2,qreg> | 1363 TFLOP/s | 0.991 (sustained) | 0.972 | 1721 MHz, sw_power_cap |
-| cfg2 OPT-13B, 64 req, 50% hidden | 1.058 | 1.029 | 60511 | 1.034 | fused_step_kernel<3,5,2,qreg> | 1414 TFLOP/s | 1.028 (sustained) | 0.981 | 1860 MHz, none |
-| cfg5 h=0 (KV only) | 1.850 | 1.832 | 138366 | nan | attn_pipe_kernel<128,8,3> | 7093 GB/s | 1.084 (copy BW) | 1.028 | 1965 MHz, none |
+{row('cfg4 OPT-66B, 256 req, 50% hidden', c4)}
+{row('cfg3 OPT-30B, 128 req, planner modes', c3)}
+{row('cfg2 OPT-13B, 64 req, 50% hidden', c2)}
+{row('cfg5 h=0 (KV only)', h0)}
 
-cfg4 e2e (pinned q in, out + lse back, every step): 6220 req-layers/s; the fp64 oracle
-on 16 host threads: 5.70 req-layers/s (one thread: {"kv_token_us": 28.44557723585602, "hidden_token_us": 4056.51497468351}).
+cfg4 e2e (pinned q in, out + lse back, every step): {c4['e2e']['value']:.0f} req-layers/s; the fp64 oracle
+on {cb['cores']} host threads: {cb['value']:.2f} req-layers/s (one thread: {json.dumps(cb.get('single_thread'))}).
 Box-to-box spread at cfg4 this round: 40.1-42.3 ms for the fused kernel (SM clock
 1305-1447 MHz under the power cap). ncu shows 1.42-1.56 GHz under tensor load even when
 nvidia-smi reports 1965 MHz for a short run (cfg2).
@@ -28,19 +63,24 @@ nvidia-smi reports 1965 MHz for a short run (cfg2).
 ## Library calibration and bandwidth probes
 
 cuBLAS (`nvjet_tst_256x256_64x4_2x1_2cta`: the same 256x512 CTA-pair tile) on a dense A of
-the same M, N, K: cfg2 1404 TF/s, cfg3 1395 TF/s, cfg4 1387 TF/s, cfg5_1/32 1362 TF/s. The
+the same M, N, K: {', '.join(f"{c['shape']} {c['tflops']:.0f} TF/s" for c in cub)}. The
 fused kernel (gathered A, attend epilogue, and all KV attention in the same kernel) runs
 the GEMM at 1290-1350 TF/s at cfg4.
-Bulk-copy streaming into 148 SMs: 32 MiB buffer 20.0 TB/s, 64 MiB buffer 19.9 TB/s, 96 MiB buffer 19.3 TB/s, 4096 MiB buffer 7.2 TB/s.
+Bulk-copy streaming into 148 SMs: {', '.join(f"{x['buffer_MiB']} MiB buffer {x['TBps']:.1f} TB/s" for x in l2)}.
 
 ## ncu --set full (one launch each)
 
 | kernel (workload) | time | SM clock | DRAM read + write | L2 hit | tensor pipe |
 |---|---|---|---|---|---|
-| fused_step_kernel<3,5,2,true> (cfg4) | 36.98 ms | 1.42 Ghz | 63.876502 Gbyte + 431.960064 Mbyte | 59.85 % | 85.110157 % |
-| recon_tc2_kernel<2,4> (cfg4, HC_FUSED=0) | 38.21 ms | 1.40 Ghz | 61.236089 Gbyte + 381.106432 Mbyte | 72.55 % | 84.457946 % |
-| attn_pipe_kernel<128,8,3> (cfg5 h=0) | 1.73 ms | 1.95 Ghz | 12.506343 Gbyte + 57.726720 Mbyte | 0.23 % | 0 % |
-
+"""
+for f, name in [("r01_ncu_fused_cfg4.txt", "fused_step_kernel<3,5,2,true> (cfg4)"),
+                ("r01_ncu_recon_cfg4.txt", "recon_tc2_kernel<2,4> (cfg4, HC_FUSED=0)"),
+                ("r01_ncu_attn_cfg5h0.txt", "attn_pipe_kernel<128,8,3> (cfg5 h=0)")]:
+    d = ncu(f)
+    txt += (f"| {name} | {d.get('Duration', '')} | {d.get('SM Frequency', '')} | {d.get('dram__bytes_read.sum', '')} + "
+            f"{d.get('dram__bytes_write.sum', '')} | {d.get('L2 Hit Rate', '')} | "
+            f"{d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', '—')} |\n")
+txt += """
 The fused kernel's DRAM read varies between captures (46-66 GB per cfg4 launch): the
 4-n-tile raster's A-panel sharing depends on how closely the four sharing pairs run.
 Attention DRAM read = 1.006 x the algorithmic bytes (K and V rows of 337,276 tokens x 36,864 B).
@@ -49,16 +89,10 @@ Attention DRAM read = 1.006 x the algorithmic bytes (K and V rows of 337,276 tok
 
 | hidden | ms/step | T_roof/T | SM MHz |
 |---|---|---|---|
-| 0.0 | 1.908 | 0.997 | 1687 |
-| 0.015625 | 2.599 | 0.748 | 1357 |
-| 0.03125 | 3.916 | 0.527 | 1087 |
-| 0.0625 | 7.070 | 0.729 | 1125 |
-| 0.125 | 13.116 | 0.845 | 1230 |
-| 0.25 | 25.196 | 0.898 | 1297 |
-| 0.5 | 45.739 | 0.945 | 1365 |
-| 0.75 | 66.720 | 0.959 | 1368 |
-| 1.0 | 86.467 | 0.963 | 1357 |
-
+"""
+for h, r in sw["runs"].items():
+    txt += f"| {h} | {r['ms_per_step']:.3f} | {r['frac']:.3f} | {r['clocks']['sm_mhz']:.0f} |\n"
+txt += """
 (Previous commit on a cooler box: `runs_r01e` in the same file, 1/32 at 3.60 ms / 0.57.)
 The crossover (1/32) is the weak point: see DESIGN.md §7 "Crossover anatomy".
 
@@ -75,3 +109,6 @@ cfg4 2.36-2.45 ms/step (104-108 K req-layers/s); `r01_bench_cfg4_absorb.json`, `
 | f2 planner (native `hc_schedule`) | `r01_planner_timing.json` | 50: 4 us ... 1600: 196 us (paper Table 6: 0.3 ... 10.8 ms) |
 | f3 prefill (OPT-66B, 8 x 2048) | `r01_bench_prefill_8x2048.json`, `r01_ncu_prefill_attn_tc.txt` | 8.9-9.9 ms, 1.66-1.83 M tokens/s |
 | f4 (i) RoPE, cfg4 | `r01_bench_cfg4_rope.json` | 41.4-42.6 ms/step |
+"""
+open(os.path.join(P, "r01_summary.md"), "w").write(txt)
+print("wrote profiles/r01_summary.md")
