@@ -481,8 +481,12 @@ def main():
     tf_burst, tf_sus = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     # the sustained (power-capped) peak for a step that ran capped, the burst peak when the
     # SM clock held its maximum through the timed region (B200_PROFILING: burst vs sustained)
+    # A power-cap flag counts only when the timed region lasted long enough (>= 1 s) to
+    # reach the capped steady state the sustained figure was measured in (4 s back to
+    # back); a short region at a held clock is a burst.
+    timed_s = ms * args.steps / 1e3
     capped = not clocks or clocks.get("sm_mhz", 0) < 0.90 * (clocks.get("sm_max_mhz") or 1e9) \
-        or "sw_power_cap" in clocks.get("reasons", [])
+        or ("sw_power_cap" in clocks.get("reasons", []) and timed_s >= 1.0)
     tf_peak = tf_sus if capped else tf_burst
     tf_kind = ("bf16 sustained (power-capped run), " if capped else "bf16 burst (clock held max), ") + peak_src
     fused = decode_path == 1
@@ -634,8 +638,12 @@ def run_module_mode(args, rank, world, local):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    # A power-cap flag counts only when the timed region lasted long enough (>= 1 s) to
+    # reach the capped steady state the sustained figure was measured in (4 s back to
+    # back); a short region at a held clock is a burst.
+    timed_s = ms * args.steps / 1e3
     capped = not clocks or clocks.get("sm_mhz", 0) < 0.90 * (clocks.get("sm_max_mhz") or 1e9) \
-        or "sw_power_cap" in clocks.get("reasons", [])
+        or ("sw_power_cap" in clocks.get("reasons", []) and timed_s >= 1.0)
     peak = tf if capped else peaks["bf16_tflops"]
     achieved = flops / (ms / 1e3) / 1e12
     line = {"metric": metric, "mode": args.mode, "value": n_layer / (ms / 1e3), "unit": unit, "n_gpus": 1,
