@@ -526,7 +526,7 @@ def main():
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
         peak = tf_peak
-        roof = {"bound": "tensor", "kernel": "fused_step_kernel<3,5,2,qreg>" if fused else "recon_tc2_kernel<2,4>",
+        roof = {"bound": "tensor", "kernel": "fused_step_kernel (<3,5,2> or, KV-dominated, <2,8,2>)" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
                 "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get(dom),
                 "ncu_tensor_pipe_pct": TRAFFIC.get(w.name, {}).get(dom + "_tensor_pipe_pct"),

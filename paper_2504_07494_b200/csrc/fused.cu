@@ -196,13 +196,20 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // next to the GEMM; crossover 1/64-1/32 -1.5..-7% on cool boxes, neutral elsewhere).
   // Measured earlier (q staged): {3,4,2} best of {3,3,3}, {2,6,2}, {2,4,3} — two GEMM stages
   // starve the tensor cores.
+  // When the rebuild is small next to the KV stream (est. GEMM time < half the KV time,
+  // e.g. 1/64 of OPT-66B requests hidden), a 2-stage GEMM ring and 8 attention warps
+  // stream KV faster (-4% at 1/64); from 1/32 up the 2-stage ring starves the tensor cores
+  // (+15..+25%), so the default stays <3,5,2>.
+  const double t_gemm = 4.0 * rp.d * (double)rp.d * a.M / 1.3e15;
+  const double t_kv = (double)rp.kv_tokens * 4.0 * rp.d / 6.5e12;
   const char* e = std::getenv("HC_FUSED_CFG");   // A/B knob
-  const int cfg = e ? std::atoi(e) : 352;
+  const int cfg = e ? std::atoi(e) : (t_gemm < 0.5 * t_kv ? 282 : 352);
   if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 342) return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 3420) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
 }
 

@@ -85,6 +85,7 @@ struct ReconParams {
   int32_t n_splits_all;     // partial index = head * n_splits_all + split
   float scale_log2;
   int32_t seg;              // tokens per partial: min(B, 32)
+  int64_t kv_tokens;        // KV-mode tokens attended in this call (fused-kernel configuration choice)
 };
 bool recon_pair_mode(int B);   // the CTA-pair GEMM serves this block size (else the 1-SM kernel)
 

@@ -162,6 +162,7 @@ struct Pinned {
 struct Plan {
   int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1;
   int32_t n_kv_splits = 0, n_hid_splits = 0;
+  int64_t kv_tokens = 0;
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
   bool absorb = false;                // hidden requests through absorbed.cu (f4 (ii)), no splits
   bool attend = false;                // fused reconstruct-and-attend epilogue (no K/V scratch)
@@ -311,6 +312,7 @@ struct hc_pool {
         P.n_splits += ns;
         P.n_tab += 2 * nb;
         P.n_kv_splits += ns;
+        P.kv_tokens += r->n;
       } else {
         P.n_hb += (int32_t)nb;
         if (P.absorb) {
@@ -862,6 +864,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.n_splits_all = P.n_splits;
   rp.scale_log2 = scale * 1.4426950408889634f;
   rp.seg = P.seg;
+  rp.kv_tokens = P.kv_tokens;
   AttnParams ap{};
   ap.reqs = reinterpret_cast<const ReqDesc*>(ws + P.off_reqs);
   ap.splits = reinterpret_cast<const SplitDesc*>(ws + P.off_splits);
