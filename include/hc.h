@@ -153,9 +153,10 @@ size_t hc_workspace_size(const hc_pool* pool, int32_t n_req, const int64_t* req_
  *   out      device [n_req, d] pool dtype: concat_h sum_j a_j v_{j,h} (pre-W_o).
  *   lse      nullable device [n_req, H] fp32: log sum_j exp(scale q_h.k_j) (natural log).
  *   workspace device, >= hc_workspace_size() bytes, 256-B aligned.
- * Hidden-mode K/V are rebuilt by a tcgen05 GEMM (bf16 in, fp32 accumulate, bf16 out),
- * then one split-K flash-decoding pass covers KV- and hidden-mode requests, then a
- * split combine.  n_req = 0 is HC_OK and launches nothing.  Errors: HC_E_INVALID,
+ * Hidden-mode K/V are rebuilt by a tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM) whose
+ * epilogue attends them straight from TMEM (fp32, never stored; HC_EPI_ATTEND=0 restores
+ * the bf16 scratch path), while KV-mode requests stream through the same persistent
+ * kernel's split-K flash-decoding warps; a split combine then writes out and lse.  n_req = 0 is HC_OK and launches nothing.  Errors: HC_E_INVALID,
  * HC_E_UNKNOWN_REQ, HC_E_WORKSPACE, HC_E_UNSUPPORTED, HC_E_CUDA.
  * CUDA graphs: the call may be stream-captured (relaxed capture mode).  The descriptor is
  * built on the host at capture time and its pinned staging buffer is retired from the
