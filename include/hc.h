@@ -183,6 +183,19 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
  * fp32 statistics): x, u device [n_rows, d] pool dtype (may alias).  HC_E_UNSUPPORTED if
  * the pool has no LayerNorm.  hc_project_append takes the normalised input. */
 hc_status hc_layer_norm(hc_pool* pool, int32_t n_rows, const void* x, void* u, void* stream);
+/* Cross-partition merge (SURVEY §8(e) phase 2; Eq. 2-3 over a union of token ranges).
+ * A request whose tokens are split over n_parts partitions (e.g. ranks that each hold part
+ * of a long request's blocks and each ran hc_decode_attention on their part) has per-part
+ * results out_p (normalised within the part) and lse_p (natural log).  This writes
+ *   lse = log sum_p e^{lse_p},  out = sum_p e^{lse_p - lse} out_p.
+ *   outs  device [n_parts][n_rows][n_heads * head_dim], dtype (the gathered part outputs)
+ *   lses  device [n_parts][n_rows][n_heads] fp32; -inf marks an empty part (weight 0)
+ *   out   device [n_rows][n_heads * head_dim] dtype;  lse nullable device [n_rows][n_heads]
+ * A row whose parts are all empty gets out = 0, lse = -inf.  No pool: buffers are the
+ * caller's.  Errors: HC_E_INVALID (sizes, dtype, null pointers), HC_E_CUDA.  Asynchronous
+ * on `stream`. */
+hc_status hc_merge_partials(int32_t n_parts, int32_t n_rows, int32_t n_heads, int32_t head_dim, hc_dtype dtype,
+                            const void* outs, const float* lses, void* out, float* lse, void* stream);
 /* y = W_O o (+ b_O): the output map of Eq. 3.  o, y device [n_req, d]. */
 hc_status hc_output_projection(hc_pool* pool, int32_t n_req, const void* o, void* y, void* stream);
 /* One attention layer for one decode step: [hc_layer_norm,] hc_project_append,

@@ -148,6 +148,8 @@ int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
+cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
+                         void* out, float* lse, cudaStream_t s);
 // u = (x - mean) / sqrt(var + eps) * gamma + beta per row of d (pre-attention LayerNorm, R15)
 cudaError_t launch_layer_norm(const void* x, void* u, const float* gamma, const float* beta, float eps, int rows,
                               int d, int dtype, cudaStream_t s);

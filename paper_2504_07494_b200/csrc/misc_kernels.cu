@@ -187,6 +187,52 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
   return __float2bfloat16_rn(v);
 }
 
+// ------------------------------------------------------------------ cross-partition merge
+// SURVEY §8(e) phase 2: a request whose token range is split over P partitions (e.g. ranks
+// that each hold part of a long hidden request's blocks) has P partial results, out_p
+// normalised over its own range and lse_p = log sum over that range.  Over the union
+// (Eq. 2-3): LSE = log sum_p e^{lse_p}, out = sum_p e^{lse_p - LSE} out_p.  A part with
+// lse_p = -inf (empty range) weighs 0; a row with no token anywhere gets out = 0,
+// lse = -inf.  One CTA per (row, head), threads over dh.
+template <typename T>
+__global__ void __launch_bounds__(128) merge_kernel(int n_parts, int n_rows, int H, int dh, const T* outs,
+                                                    const float* lses, T* out, float* lse) {
+  const int r = blockIdx.x / H, h = blockIdx.x - r * H;
+  float M = -INFINITY;
+  for (int q = 0; q < n_parts; ++q) M = fmaxf(M, lses[((size_t)q * n_rows + r) * H + h]);
+  float L = 0.f;
+  if (M != -INFINITY)
+    for (int q = 0; q < n_parts; ++q) L += expf(lses[((size_t)q * n_rows + r) * H + h] - M);
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  for (int c = threadIdx.x; c < dh; c += blockDim.x) {
+    float acc = 0.f;
+    if (M != -INFINITY) {
+      for (int q = 0; q < n_parts; ++q) {
+        const float lq = lses[((size_t)q * n_rows + r) * H + h];
+        if (lq == -INFINITY) continue;   // empty part: its out is never read (0 * NaN = NaN)
+        acc = fmaf(expf(lq - M), to_f(outs[(((size_t)q * n_rows + r) * H + h) * dh + c]), acc);
+      }
+    }
+    out[((size_t)r * H + h) * dh + c] = from_f<T>(acc * inv);
+  }
+  if (lse != nullptr && threadIdx.x == 0) lse[(size_t)r * H + h] = M == -INFINITY ? M : M + logf(L);
+}
+
+cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
+                         void* out, float* lse, cudaStream_t s) {
+  if (n_rows == 0) return cudaSuccess;
+  const int blocks = n_rows * H;
+  if (dtype == 1)
+    merge_kernel<float><<<blocks, 128, 0, s>>>(n_parts, n_rows, H, dh, static_cast<const float*>(outs), lses,
+                                               static_cast<float*>(out), lse);
+  else
+    merge_kernel<__nv_bfloat16><<<blocks, 128, 0, s>>>(n_parts, n_rows, H, dh,
+                                                       static_cast<const __nv_bfloat16*>(outs), lses,
+                                                       static_cast<__nv_bfloat16*>(out), lse);
+  return cudaGetLastError();
+}
+
+
 // x and u may alias (each element is read before it is overwritten by the same thread)
 template <typename T>
 __global__ void __launch_bounds__(256) layer_norm_kernel(const T* x, T* u,

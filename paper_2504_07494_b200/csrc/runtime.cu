@@ -1070,6 +1070,19 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   return HC_OK;
 }
 
+hc_status hc_merge_partials(int32_t n_parts, int32_t n_rows, int32_t n_heads, int32_t head_dim, hc_dtype dtype,
+                            const void* outs, const float* lses, void* out, float* lse, void* stream) {
+  if (n_parts < 1 || n_rows < 0 || n_heads < 1 || head_dim < 1)
+    return fail(HC_E_INVALID, "merge: n_parts >= 1, n_rows >= 0, n_heads >= 1, head_dim >= 1 required");
+  if (dtype != HC_BF16 && dtype != HC_F32) return fail(HC_E_INVALID, "merge: unknown dtype");
+  if (n_rows == 0) return HC_OK;
+  if (!outs || !lses || !out) return fail(HC_E_INVALID, "merge: outs / lses / out is null");
+  cudaError_t err = launch_merge(n_parts, n_rows, n_heads, head_dim, dtype == HC_F32 ? 1 : 0, outs, lses, out, lse,
+                                 static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "merge kernel");
+  return HC_OK;
+}
+
 hc_status hc_layer_norm(hc_pool* pool, int32_t n_rows, const void* x, void* u, void* stream) {
   if (!pool) return fail(HC_E_INVALID, "pool is null");
   pool->last_launches = 0;

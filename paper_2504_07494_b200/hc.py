@@ -78,6 +78,7 @@ def _load() -> ctypes.CDLL:
         "hc_project_append": (I32, [P, I32, pI64, pI32, VP, VP, VP]),
         "hc_output_projection": (I32, [P, I32, VP, VP, VP]),
         "hc_layer_norm": (I32, [P, I32, VP, VP, VP]),
+        "hc_merge_partials": (I32, [I32, I32, I32, I32, I32, VP, VP, VP, VP, VP]),
         "hc_layer_workspace_size": (SZ, [P, I32, pI64, pI32]),
         "hc_decode_layer": (I32, [P, I32, pI64, pI32, VP, ctypes.c_float, VP, VP, VP, SZ, VP]),
         "hc_prefill_workspace_size": (SZ, [P, I32, pI32]),
@@ -176,6 +177,14 @@ def hc_project_append(h, req_ids, modes, x, q_out, stream=None) -> None:
 
 def hc_layer_norm(h, n_rows, x, u, stream=None) -> None:
     _check(lib.hc_layer_norm(h, int(n_rows), _ptr(x), _ptr(u), _stream(stream)))
+
+
+def hc_merge_partials(outs, lses, out, lse=None, stream=None) -> None:
+    """outs [P, rows, H*dh] (bf16/fp32), lses [P, rows, H] fp32 -> out [rows, H*dh], lse [rows, H]."""
+    n_parts, n_rows, n_heads = lses.shape
+    dt = HC_F32 if outs.dtype.is_floating_point and outs.element_size() == 4 else HC_BF16
+    _check(lib.hc_merge_partials(int(n_parts), int(n_rows), int(n_heads), int(outs.shape[2] // n_heads), dt,
+                                 _ptr(outs), _ptr(lses), _ptr(out), _ptr(lse), _stream(stream)))
 
 
 def hc_output_projection(h, n_req, o, y, stream=None) -> None:

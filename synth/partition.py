@@ -35,3 +35,45 @@ def strong_shard(w, rank: int, world: int):
     costs = [request_cost(n, m, w.shape.d, w.elem_bytes) for n, m in zip(w.n, w.modes)]
     idx = lpt(costs, world)[rank]
     return w.subset(idx, name=w.name)
+
+
+def lpt_split(ns: Sequence[int], modes: Sequence[int], d: int, world: int, block: int = 16, s: int = 2):
+    """LPT with token-range splitting (SURVEY §8(e) phase 2).  A request whose cost exceeds
+    the ideal per-rank load (total / world) is cut into k = ceil(cost / ideal) (<= world)
+    block-aligned token ranges on k distinct ranks; their (out, lse) partials are merged
+    by hc_merge_partials.  Everything else is plain LPT.  Returns, per rank, a list of
+    (request index, token begin, token end); every rank derives the same plan."""
+    costs = [request_cost(n, m, d, s) for n, m in zip(ns, modes)]
+    ideal = sum(costs) / world
+    items = []   # (cost, request, begin, end)
+    for i, (n, c) in enumerate(zip(ns, costs)):
+        k = min(world, max(1, int(-(-c // ideal)) if ideal > 0 else 1))
+        nb = -(-n // block)
+        k = min(k, nb)
+        if k == 1:
+            items.append((c, i, 0, n))
+            continue
+        # k block-aligned ranges with (almost) equal block counts
+        b0 = 0
+        for p in range(k):
+            b1 = b0 + nb // k + (1 if p < nb % k else 0)
+            t0, t1 = b0 * block, min(n, b1 * block)
+            items.append((c * (t1 - t0) / n, i, t0, t1))
+            b0 = b1
+    order = sorted(range(len(items)), key=lambda j: (-items[j][0], items[j][1], items[j][2]))
+    heap = [(0.0, p) for p in range(world)]
+    plan: List[list] = [[] for _ in range(world)]
+    for j in order:
+        c, i, t0, t1 = items[j]
+        # parts of one request go to distinct ranks: take the lightest rank not holding it
+        popped = []
+        while True:
+            load, p = heapq.heappop(heap)
+            if all(r != i for r, _, _ in plan[p]) or not heap:
+                break
+            popped.append((load, p))
+        plan[p].append((i, t0, t1))
+        heapq.heappush(heap, (load + c, p))
+        for x in popped:
+            heapq.heappush(heap, x)
+    return [sorted(p) for p in plan]

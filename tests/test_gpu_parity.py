@@ -340,6 +340,54 @@ def test_cuda_graph_replay_bitwise(hc):
         assert torch.equal(out, ref_out) and torch.equal(lse, ref_lse)
 
 
+def test_cross_partition_merge_vs_oracle(hc):
+    """SURVEY §8(e) phase 2: each request's tokens split into 3 partitions (stored as
+    separate requests, as ranks holding part of a long request would), decoded
+    separately, merged by hc_merge_partials == the oracle on the whole request.  A 4th
+    partition that holds nothing (lse = -inf, out = NaN) must not change a bit."""
+    from paper_2504_07494_b200 import hc as H
+    n = [700, 300, 129, 1000, 40]
+    modes = [MODE_HIDDEN, MODE_KV, MODE_HIDDEN, MODE_KV, MODE_HIDDEN]
+    w = _bf16_workload(512, 4, 128, 16, n=n, modes=modes, bias=True)
+    dev = torch.device("cuda", 0)
+    data = {i: (w.kv(i, device=dev) if w.modes[i] == MODE_KV else w.x(i, device=dev)) for i in range(len(n))}
+    cuts = {i: [0, 17, n[i] // 2, n[i]] for i in range(len(n))}
+    pool = T.make_pool(w, num_blocks=T.pool_blocks(w) + 8 * len(n))
+    q = T.queries(w)
+    P, d, Hh = 3, w.shape.d, w.shape.H
+    outs = torch.empty((P + 1, len(n), d), dtype=torch.bfloat16, device=dev)
+    lses = torch.empty((P + 1, len(n), Hh), dtype=torch.float32, device=dev)
+    for p in range(P):
+        ids, toks, ks, vs, xs = [], [], [], [], []
+        for i in range(len(n)):
+            a, b = cuts[i][p], cuts[i][p + 1]
+            ids.append(1000 * (p + 1) + i)
+            toks.append(b - a)
+            if w.modes[i] == MODE_KV:
+                ks.append(data[i][0][a:b])
+                vs.append(data[i][1][a:b])
+            else:
+                xs.append(data[i][a:b])
+        pool.append(ids, list(w.modes), toks, torch.cat(ks).contiguous(), torch.cat(vs).contiguous(),
+                    torch.cat(xs).contiguous())
+        o, l = pool.decode(ids, q, w.scale)
+        outs[p].copy_(o)
+        lses[p].copy_(l)
+    out = torch.empty((len(n), d), dtype=torch.bfloat16, device=dev)
+    lse = torch.empty((len(n), Hh), dtype=torch.float32, device=dev)
+    H.hc_merge_partials(outs[:P], lses[:P], out, lse)
+    torch.cuda.synchronize()
+    err, lerr = T.compare(w, out.float().cpu().numpy(), lse.cpu().numpy(), range(len(n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= 5e-2, lerr
+    outs[P].fill_(float("nan"))
+    lses[P].fill_(float("-inf"))
+    out2, lse2 = torch.empty_like(out), torch.empty_like(lse)
+    H.hc_merge_partials(outs, lses, out2, lse2)
+    torch.cuda.synchronize()
+    assert torch.equal(out2, out) and torch.equal(lse2, lse)
+
+
 # ------------------------------------------------------------------ attention layer (NEXT row f1)
 LAYER_CASES = [
     ("tiny-f32", None),

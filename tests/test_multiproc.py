@@ -75,3 +75,30 @@ def test_strong_shard_subsets_partition_the_batch():
     subs = [P.strong_shard(w, r, 4) for r in range(4)]
     ids = sorted(i for s in subs for i in s.req_ids)
     assert ids == sorted(w.req_ids)
+
+
+def test_lpt_split_covers_every_token_once_and_balances():
+    """Phase-2 plan: every request's tokens are covered exactly once, split parts sit on
+    distinct ranks, ranges are block-aligned, and one dominant hidden request no longer
+    bounds the makespan (cfg5 at 1/64 hidden on 8 ranks)."""
+    w = C.cfg5(1 / 64)
+    d, B = w.shape.d, w.block_size
+    costs = [P.request_cost(n, m, d) for n, m in zip(w.n, w.modes)]
+    for G in (2, 4, 8):
+        plan = P.lpt_split(w.n, w.modes, d, G, B)
+        cover = {}
+        for r, items in enumerate(plan):
+            held = [i for i, _, _ in items]
+            assert len(held) == len(set(held))           # parts of one request on distinct ranks
+            for i, t0, t1 in items:
+                assert t0 % B == 0 and t0 < t1 <= w.n[i]
+                cover.setdefault(i, []).append((t0, t1))
+        for i, n in enumerate(w.n):
+            rs = sorted(cover[i])
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        load = [sum(costs[i] * (t1 - t0) / w.n[i] for i, t0, t1 in items) for items in plan]
+        ideal = sum(costs) / G
+        unsplit = [sum(costs[i] for i in p) for p in P.lpt(costs, G)]
+        assert max(load) <= max(unsplit) + 1e-12
+        assert max(load) / ideal < 1.15
