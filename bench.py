@@ -268,6 +268,113 @@ def cpu_baseline(w, budget_s: float = 20.0):
                       f"{t_used:.1f} s; value = 1 / (mix-weighted mean time per request)"}
 
 
+# ============================================================================ phase-2 strong scaling
+def run_split(args, rank: int, world: int, local: int, w0):
+    """Strong scaling with token-range splitting (SURVEY §8(e) phase 2): every rank holds
+    its parts of the batch (synth.partition.lpt_split), decodes them, all-gathers (out,
+    lse) and merges every request's parts with hc_merge_partials.  All of it is timed."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_07494_b200 import hc
+    from synth.configs import MODE_KV
+    from synth.partition import lpt_split
+    from tests import hc_testlib as T
+
+    d, Hh, B = w0.shape.d, w0.shape.H, w0.block_size
+    plans = lpt_split(w0.n, w0.modes, d, world, B)
+    mine = plans[rank]
+    wr = w0.subset(sorted({i for i, _, _ in mine}) or [0])
+    nblk = sum((2 if w0.modes[i] == MODE_KV else 1) * -(-(t1 - t0) // B) for i, t0, t1 in mine)
+    pool = T.make_pool(wr, device=local, num_blocks=int(nblk * 1.05) + 8)
+    dev = torch.device("cuda", local)
+    pid = [10_000_000 + 100_000 * rank + j for j in range(len(mine))]
+    for j, (i, t0, t1) in enumerate(mine):   # one part at a time (cache fill, untimed)
+        if w0.modes[i] == MODE_KV:
+            k, v = w0.kv(i, device=dev, rows=(t0, t1))
+            pool.append([pid[j]], [MODE_KV], [t1 - t0], k=k.contiguous(), v=v.contiguous())
+        else:
+            pool.append([pid[j]], [1], [t1 - t0], x=w0.x(i, device=dev, rows=(t0, t1)).contiguous())
+    q = torch.stack([w0.q(i, device=dev) for i, _, _ in mine]).contiguous() if mine else None
+    n_mine = len(mine)
+    out_p = torch.empty((max(n_mine, 1), d), dtype=w0.torch_dtype, device=dev)
+    lse_p = torch.empty((max(n_mine, 1), Hh), dtype=torch.float32, device=dev)
+    ws = pool.workspace(pid) if mine else None
+    n_max = max(len(p) for p in plans)
+    send = torch.zeros((n_max, d + Hh), dtype=torch.float32, device=dev)
+    send[:, d:] = float("-inf")
+    recv = torch.empty((world * n_max + 1, d + Hh), dtype=torch.float32, device=dev)
+    recv[-1, :d] = 0.0
+    recv[-1, d:] = float("-inf")   # the "empty part" row
+    # merge index: part p of request i lives in recv row rank * n_max + slot
+    parts_of = [[] for _ in w0.n]
+    for r, items in enumerate(plans):
+        for j, (i, _, _) in enumerate(items):
+            parts_of[i].append(r * n_max + j)
+    P = max(len(x) for x in parts_of)
+    idx = torch.full((P, len(w0.n)), world * n_max, dtype=torch.int64)
+    for i, rows in enumerate(parts_of):
+        for p, row in enumerate(rows):
+            idx[p, i] = row
+    idx = idx.to(dev)
+    out_all = torch.empty((len(w0.n), d), dtype=torch.float32, device=dev)
+    lse_all = torch.empty((len(w0.n), Hh), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if mine:
+            hc.hc_decode_attention(pool.handle, pid, q, w0.scale, out_p, lse_p, ws, stream)
+            send[:n_mine, :d].copy_(out_p[:n_mine])
+            send[:n_mine, d:].copy_(lse_p[:n_mine])
+        if world > 1:
+            dist.all_gather_into_tensor(recv[:world * n_max], send)
+        else:
+            recv[:n_max].copy_(send)
+        outs = recv[:, :d].index_select(0, idx.view(-1)).view(P, len(w0.n), d)
+        lses = recv[:, d:].index_select(0, idx.view(-1)).view(P, len(w0.n), Hh)
+        hc.hc_merge_partials(outs, lses, out_all, lse_all, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    n_split = sum(1 for x in parts_of if len(x) > 1)
+    check = None
+    if rank == 0 and os.environ.get("HC_BENCH_CHECK"):
+        # oracle on the longest split request (or the longest request): a few heads
+        cand = [i for i, x in enumerate(parts_of) if len(x) > 1] or [int(np.argmax(w0.n))]
+        i = max(cand, key=lambda j: w0.n[j])
+        heads = [0, Hh // 2, Hh - 1]
+        err, lerr = T.compare(w0, out_all[[i]].cpu().numpy(), lse_all[[i]].cpu().numpy(), [i], {i: heads})
+        check = {"request": i, "n": w0.n[i], "parts": len(parts_of[i]), "max_rel_err": err, "lse_err": lerr}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "decode-attention req-layers/s (hybrid KV/hidden cache, one layer)",
+            "value": len(w0.n) / (ms / 1e3), "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": w0.dtype, "data": "synthetic",
+            "config": {"workload": w0.name, "parallelism": f"request-sharded x{world} (strong, LPT + token-range split)",
+                       "split_requests": n_split, "max_parts": P,
+                       "output": "all-gather of (out, lse) parts + hc_merge_partials, every step (timed)"},
+            "gpu_launches": (pool.last_launch_count() + 1) * args.steps, "check": check}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ============================================================================ main arm
 def main():
     ap = argparse.ArgumentParser()
@@ -289,6 +396,9 @@ def main():
     ap.add_argument("--absorb", action="store_true",
                     help="NON-PAPER variant (NEXT row f4 (ii)): hidden requests attend through "
                          "q~ = W_K^T q and W_V (sum a x) instead of rebuilding K/V")
+    ap.add_argument("--split", action="store_true",
+                    help="with --strong: split requests costlier than total/world across ranks "
+                         "(SURVEY §8(e) phase 2) and merge their (out, lse) parts after an all-gather")
     ap.add_argument("--gather", action="store_true",
                     help="N>1: all-gather every rank's out + lse over NCCL after each step, inside the "
                          "timed region (north_star's output gather; not a data-path exchange)")
@@ -329,6 +439,8 @@ def main():
         else:
             dist.init_process_group(backend)
     w0 = workload_from(args.config)
+    if args.split:
+        return run_split(args, rank, world, local, w0)
     if args.strong:
         from synth.partition import strong_shard
         w = strong_shard(w0, rank, world)
