@@ -258,7 +258,7 @@ typedef struct {
  * iteration type by the larger cumulative pending time (ties -> decode), the candidate set
  * U^e and budget M^e, values g_i = p_i - beta_i (|W|+|R|) rho m_i (Eq. 5-6) with the
  * SLO fallback applied to p_i, then the marginal-gain greedy (hidden / upgrade /
- * direct-KV stages, refinement when p/m < 2 N rho; ties theta desc, delta-m asc, index asc)
+ * direct-KV stages, refinement when p/m < 2 N rho; ties theta desc, delta-m asc, request id asc)
  * compared against the best single feasible assignment (KV or hidden; R14).
  * alpha[i], beta[i] (n each, host) receive the decision for every input request (0 for
  * requests outside U^e); g (nullable) receives each candidate's value at its decided beta.

@@ -80,7 +80,8 @@ def schedule(cfg: dict, reqs: Sequence[dict], now: float):
             ups.append((2 * N * rho, m[i] / 2, pos, 1))                       # upgrade to KV
         else:
             ups.append((pc[i] / m[i], m[i], pos, 2))                          # refined: direct KV
-    ups.sort(key=lambda s: (-s[0], s[1], s[2], s[3]))
+    # ties: theta desc, delta-m asc, lower request id, stage order
+    ups.sort(key=lambda s: (-s[0], s[1], reqs[U[s[2]]]["id"], s[2], s[3]))
     a = {i: 0 for i in U}
     b = {i: 0 for i in U}
     used = 0.0

@@ -604,17 +604,11 @@ static cudaError_t launch_wv(const AbsorbParams& p, const CUtensorMap& tz, const
 
 cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
                             const void* tmap_p, const void* tmap_wk, const void* tmap_z, const void* tmap_wv,
-                            cudaStream_t s) {
+                            const Tuning& t, cudaStream_t s) {
   if (p.n_h <= 0) return cudaSuccess;
   constexpr int smem_tc = 1024 + 3 * 32768 + 256 + 512;
-  static const int zcfg = [] {   // Z GEMM tile width x pipeline depth (A/B knob; default 128x2: 3 CTAs per SM)
-    const char* e = std::getenv("HC_Z_CFG");
-    return e ? std::atoi(e) : 1282;
-  }();
-  static const int sst = [] {
-    const char* e = std::getenv("HC_SCORE_ST");   // A/B knob: 2 stages (3 CTAs/SM, default) or 3
-    return e ? std::atoi(e) : 2;
-  }();
+  const int zcfg = t.z_cfg;     // Z GEMM tile width x pipeline depth (default 128x2: 3 CTAs per SM)
+  const int sst = t.score_st;   // score GEMM stages: 2 (3 CTAs/SM, default) or 3
   constexpr int smem_s2 = 1024 + 128 * 129 * 4 + 256 + 512;
   static const cudaError_t attr = [] {
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
@@ -625,10 +619,7 @@ cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const voi
   if (attr != cudaSuccess) return attr;
   cudaError_t e;
   const CUtensorMap& twk = *static_cast<const CUtensorMap*>(tmap_wk);
-  static const int qbn = [] {   // q~ GEMM tile width (A/B knob HC_QT_BN; 128 also serves d % 256 != 0)
-    const char* v = std::getenv("HC_QT_BN");
-    return v && std::atoi(v) == 256 ? 256 : 128;
-  }();
+  const int qbn = t.qt_bn == 256 ? 256 : 128;   // q~ GEMM tile width (128 also serves d % 256 != 0)
   if (qbn == 256 && p.d % 256 == 0)
     e = p.dh == 128 ? launch_qt<128, 256>(p, twk, s) : launch_qt<64, 256>(p, twk, s);
   else

@@ -129,10 +129,10 @@ bool attn_pipe_supported(int dtype, int dh, int B) {
   return dtype == 0 && (dh == 128 || dh == 64) && B % 16 == 0;
 }
 
-cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s) {
+cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s) {
   if (p.n_tasks <= 0) return cudaSuccess;
   if (!generic && attn_pipe_supported(dtype, p.dh, p.B)) {
-    static const int cfg = [] { const char* v = std::getenv("HC_ATTN_CFG"); return v ? std::atoi(v) : 0; }();
+    const int cfg = t.attn_cfg;
     if (p.dh == 128) {
       if (cfg == 1) return launch_pipe<128, 6, 4>(p, num_sms, s);
       if (cfg == 2) return launch_pipe<128, 4, 6>(p, num_sms, s);

@@ -138,13 +138,13 @@ int fused_tile_m() { return pg::P_BM; }
 int fused_tile_n() { return PC::TILE_N; }
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
-                         int32_t* tile_done, int num_sms, cudaStream_t s) {
+                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s) {
   pg::TcArgs a{};
   a.gather = rp.gather;
   a.n_hblocks = rp.n_hblocks;
   a.B = rp.B;
   a.M = rp.n_hblocks * rp.B;
-  a.rows_per_box = (rp.B < 128 && !std::getenv("HC_DIAG_BOX")) ? rp.B : 128;
+  a.rows_per_box = (rp.B < 128 && !t.diag_box) ? rp.B : 128;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
   a.n_tiles = 2 * rp.d / PC::TILE_N;
   a.k_iters = rp.d / pg::BK;
@@ -158,20 +158,14 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.row_pos = rp.hblk_pos;
   // n-major raster, 4 n-tiles per group: four pairs of a wave share each A panel (same-box
   // A/B vs 2: cfg4 -2.5%, cfg5 1/32 -2..-4%)
-  a.group_m = -4;
-  if (const char* gn = std::getenv("HC_GROUP_N"))   // A/B knob: n-tiles per raster group (>= 1)
-    if (std::atoi(gn) >= 1) a.group_m = -std::atoi(gn);
+  a.group_m = -(t.group_n >= 1 ? t.group_n : 4);
   a.l2_hint = 0;
   // Partner lockstep off by default in the fused kernel: with the attend epilogue, tiles of
   // partner pairs finish at different times and the spin costs more than the L2 reuse buys
   // (same-box A/B: cfg4 -2.5%, cfg3 -2%, cfg2 -1%, crossover neutral).
   // HC_SYNC_W=<w> re-enables it with window w (the stand-alone GEMM keeps w = 8).
-  a.sync_w = 0;
-  a.sync = nullptr;
-  if (const char* sw = std::getenv("HC_SYNC_W")) {
-    a.sync_w = std::atoi(sw);
-    if (a.sync_w > 0 && num_sms / 2 <= pg::kMaxSyncPairs) a.sync = rp.sync_counter;
-  }
+  a.sync_w = t.sync_w > 0 ? t.sync_w : 0;
+  a.sync = (a.sync_w > 0 && num_sms / 2 <= pg::kMaxSyncPairs) ? rp.sync_counter : nullptr;
   if (rp.epi_attend) {   // hidden rows become partials in the GEMM epilogue: no hidden tasks
     a.epi = pg::EPI_ATTEND;
     a.hblk_req = rp.hblk_req;
@@ -183,8 +177,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     a.scale_log2 = rp.scale_log2;
     a.seg = rp.seg;
     tile_done = nullptr;
-    const char* de = std::getenv("HC_DIAG_EPI");
-    a.diag = de ? std::atoi(de) : 0;
+    a.diag = t.diag_epi;
   }
   a.tile_done = tile_done;
   ap_.tile_done = tile_done;
@@ -202,8 +195,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // (+15..+25%), so the default stays <3,5,2>.
   const double t_gemm = 4.0 * rp.d * (double)rp.d * a.M / 1.3e15;
   const double t_kv = (double)rp.kv_tokens * 4.0 * rp.d / 6.5e12;
-  const char* e = std::getenv("HC_FUSED_CFG");   // A/B knob
-  const int cfg = e ? std::atoi(e) : (t_gemm < 0.5 * t_kv ? 282 : 352);
+  const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 282 : 352);
   if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);

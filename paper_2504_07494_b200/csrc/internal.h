@@ -8,6 +8,32 @@
 
 namespace hc {
 
+// Schedule / A-B knobs of the kernels.  Read ONCE from the environment when a pool is created
+// (runtime.cu tuning_from_env, the library's only getenv site) and fixed for the pool's life;
+// the defaults are the measured-best configuration.  None of them changes
+// what is computed — only tile order, pipeline depth or which equivalent kernel runs.  The
+// timing diagnostics that DO change results (HC_DIAG_*) exist only in a -DHC_DIAG build.
+struct Tuning {
+  int fused = -1;        // HC_FUSED: 0 = two-kernel path, else the fused step kernel when supported
+  int epi_attend = 1;    // HC_EPI_ATTEND: 0 = rebuilt K/V into scratch + attention kernel
+  int fused_cfg = 0;     // HC_FUSED_CFG: {GEMM stages, attention warps, stages} of the fused kernel; 0 = auto
+  int group_n = 4;       // HC_GROUP_N: n-tiles per raster group of the fused kernel
+  int sync_w = -1;       // HC_SYNC_W: partner k-lockstep window (-1: kernel default, 0 off)
+  int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM
+  int l2_hint = 0;       // HC_L2HINT
+  int tc_1sm = 0;        // HC_TC_1SM: 1-SM tcgen05 reconstruction kernel instead of CTA pairs
+  int tc_nsub = 0;       // HC_TC_NSUB: 1 = 256-wide pair tiles
+  int tc_stages = 4;     // HC_TC_STAGES (3 or 4)
+  int attn_cfg = 0;      // HC_ATTN_CFG: warps x stages of the stand-alone attention kernel
+  int prefill_tc = 1;    // HC_PREFILL_TC: 0 = mma.sync prefill attention
+  int prefill_cfg = 1;   // HC_PREFILL_CFG: 1, 2 or 128 (prefill_attn.cu)
+  int z_cfg = 1282;      // HC_Z_CFG (absorbed variant)
+  int score_st = 2;      // HC_SCORE_ST (absorbed variant)
+  int qt_bn = 128;       // HC_QT_BN (absorbed variant)
+  int diag_epi = 0;      // -DHC_DIAG builds only: HC_DIAG_EPI (wrong outputs, timing only)
+  int diag_box = 0;      // -DHC_DIAG builds only: HC_DIAG_BOX (wrong outputs, timing only)
+};
+
 // Per-request entry of the decode-call descriptor (uploaded once per call).
 struct ReqDesc {
   int32_t mode;          // 0 KV, 1 hidden (beta_i)
@@ -87,7 +113,7 @@ struct ReconParams {
   int32_t seg;              // tokens per partial: min(B, 32)
   int64_t kv_tokens;        // KV-mode tokens attended in this call (fused-kernel configuration choice)
 };
-bool recon_pair_mode(int B);   // the CTA-pair GEMM serves this block size (else the 1-SM kernel)
+bool recon_pair_mode(int B, const Tuning& t);   // the CTA-pair GEMM serves this block size (else the 1-SM kernel)
 
 struct AppendReq {
   int32_t mode;
@@ -132,13 +158,13 @@ cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float*
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
 // tmap_w: W_int with 256-row boxes (1-SM kernel); tmap_w_half: 128-row boxes (CTA-pair kernel)
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
-                            const void* tmap_w_half, int num_sms, cudaStream_t s);
+                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s);
 bool recon_tc_supported(int d, int H, int dh, int B);
 bool dense_tc_supported(int d);
 // tmap_a: A with {64 x 128} boxes; tmap_w: W with {64 x 128} boxes
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s);
 cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s);
-cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, cudaStream_t s);
+cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s);
 bool attn_pipe_supported(int dtype, int dh, int B);
 // Fused step: reconstruction GEMM (CTA pairs, 256x512 tiles) and split-K attention warps in
 // one persistent kernel; hidden tasks wait on per-tile completion counters.
@@ -146,7 +172,7 @@ bool fused_supported(int d, int H, int dh, int B);
 int fused_tile_m();
 int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
-                         int32_t* tile_done, int num_sms, cudaStream_t s);
+                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
                          void* out, float* lse, cudaStream_t s);
@@ -169,11 +195,10 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStrea
 bool prefill_attn_mma_supported(int dtype, int dh);
 // tcgen05 version (128-query tiles; tile_q0 multiples of 128): tmap_q over q [R, d] and
 // tmap_kv over kv [R, 2d], both {64 x 128} boxes.  HC_PREFILL_TC=0 selects the mma.sync kernel.
-bool prefill_attn_tc_enabled();
-int prefill_attn_tc_keys();   // keys per tile (tmap_kv box rows)
-int prefill_attn_tc_rows();   // query rows per CTA (tile_q0 step): 128 or 256
+int prefill_attn_tc_keys(const Tuning& t);   // keys per tile (tmap_kv box rows)
+int prefill_attn_tc_rows(const Tuning& t);   // query rows per CTA (tile_q0 step): 128 or 256
 cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_q, const void* tmap_kv,
-                                   cudaStream_t s);
+                                   const Tuning& t, cudaStream_t s);
 
 // Absorbed hidden-cache attention (NEXT row f4 (ii), opt-in, absorbed.cu).  Hidden request
 // r (0..n_h-1) owns gathered rows [hrow0[r], hrow0[r] + hntok[r]) (row g*B + t = slot t of
@@ -210,6 +235,6 @@ int absorb_launches();
 // with {64 x 128} boxes; tmap_wv: W_int with {64 x dh} boxes (W_V,h rows).
 cudaError_t launch_absorbed(const AbsorbParams& p, const void* tmap_x, const void* tmap_x64, const void* tmap_qt,
                             const void* tmap_p, const void* tmap_wk, const void* tmap_z, const void* tmap_wv,
-                            cudaStream_t s);
+                            const Tuning& t, cudaStream_t s);
 
 }  // namespace hc

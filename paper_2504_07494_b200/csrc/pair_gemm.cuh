@@ -63,7 +63,7 @@ struct TcArgs {
   int32_t n_splits_all;
   float scale_log2;
   int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
-  int32_t diag;             // timing diagnostic only (HC_DIAG_EPI=1): skip the EPI_ATTEND math
+  int32_t diag;             // -DHC_DIAG builds only (HC_DIAG_EPI): timing diagnostics with wrong outputs
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -402,7 +402,9 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
           } else {
             const int g = grow / a.B;
             s.prow[i] = g < a.n_hblocks ? a.gather[g] * a.B + (grow - g * a.B) : 0;
+#ifdef HC_DIAG
             if (a.diag == 3 && i > 0) s.prow[i] = s.prow[0] + i * a.rows_per_box;   // timing diagnostic
+#endif
           }
         }
         const int wrow = nt * PC::TILE_N + (int)rank * 128;
@@ -496,7 +498,8 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       ptx::tc_fence_after();
       const int grow = mt * P_BM + row_in_tile;
       if (a.epi == EPI_ATTEND) {
-        if (a.diag == 1 || a.diag == 2) {   // timing diagnostics (wrong outputs)
+#ifdef HC_DIAG
+        if (a.diag == 1 || a.diag == 2) {   // timing diagnostics (wrong outputs; -DHC_DIAG builds only)
           if (a.diag == 2) {   // read the whole accumulator from TMEM, skip the math
             float f[32], sum = 0.f;
             for (int c = 0; c < PC::TILE_N / 32; ++c) {
@@ -511,6 +514,7 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
           if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
           continue;
         }
+#endif
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
         if (a.seg == 8)
           attend_tile<8, PC::TILE_N>(a, tacc, nt, grow, lane);

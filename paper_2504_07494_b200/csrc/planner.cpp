@@ -98,9 +98,12 @@ hc_status hc_schedule(const hc_sched_config* cfg, int32_t n, const hc_sched_requ
       ups.push_back({pc[c] / mi, mi, c, 2});
     }
   }
-  std::sort(ups.begin(), ups.end(), [](const Stage& a, const Stage& b) {
+  // ties: theta desc, delta-m asc, lower request id, then input order
+  std::sort(ups.begin(), ups.end(), [&](const Stage& a, const Stage& b) {
     if (a.theta != b.theta) return a.theta > b.theta;
     if (a.dm != b.dm) return a.dm < b.dm;
+    const int64_t ia = reqs[cand[a.idx]].id, ib = reqs[cand[b.idx]].id;
+    if (ia != ib) return ia < ib;
     if (a.idx != b.idx) return a.idx < b.idx;
     return a.kind < b.kind;
   });

@@ -554,22 +554,16 @@ __global__ void __launch_bounds__(128) prefill_attn_simt_kernel(const PrefillAtt
 
 bool prefill_attn_mma_supported(int dtype, int dh) { return dtype == 0 && (dh == 128 || dh == 64); }
 
-bool prefill_attn_tc_enabled() {   // read per call so tests can switch paths
-  const char* e = std::getenv("HC_PREFILL_TC");
-  return !e || std::atoi(e) != 0;
-}
-
 // Configuration of the tcgen05 prefill kernel (A/B knob HC_PREFILL_CFG): 1 = one query tile
 // per CTA, 64-key tiles, 2 K/V stages, two CTAs per SM (default, fastest measured);
 // 2 = two query tiles per CTA sharing 3 K/V stages (FA4-style pair of softmax warpgroups);
 // 128 = one query tile, 128-key tiles.
-int prefill_attn_tc_cfg() {
-  const char* e = std::getenv("HC_PREFILL_CFG");
-  const int v = e ? std::atoi(e) : 1;
+static int prefill_attn_tc_cfg(const Tuning& t) {
+  const int v = t.prefill_cfg;
   return (v == 2 || v == 128) ? v : 1;
 }
-int prefill_attn_tc_keys() { return prefill_attn_tc_cfg() == 128 ? 128 : 64; }
-int prefill_attn_tc_rows() { return prefill_attn_tc_cfg() == 2 ? 256 : 128; }
+int prefill_attn_tc_keys(const Tuning& t) { return prefill_attn_tc_cfg(t) == 128 ? 128 : 64; }
+int prefill_attn_tc_rows(const Tuning& t) { return prefill_attn_tc_cfg(t) == 2 ? 256 : 128; }
 
 template <int DH, int BK, int NQ, int ST>
 static cudaError_t launch_tc(const PrefillAttnParams& p, const CUtensorMap& tq, const CUtensorMap& tkv,
@@ -584,11 +578,11 @@ static cudaError_t launch_tc(const PrefillAttnParams& p, const CUtensorMap& tq, 
 }
 
 cudaError_t launch_prefill_attn_tc(const PrefillAttnParams& p, const void* tmap_q, const void* tmap_kv,
-                                   cudaStream_t s) {
+                                   const Tuning& t, cudaStream_t s) {
   if (p.n_qtiles <= 0) return cudaSuccess;
   const CUtensorMap& tq = *static_cast<const CUtensorMap*>(tmap_q);
   const CUtensorMap& tkv = *static_cast<const CUtensorMap*>(tmap_kv);
-  const int cfg = prefill_attn_tc_cfg();
+  const int cfg = prefill_attn_tc_cfg(t);
   if (p.dh == 128) {
     if (cfg == 128) return launch_tc<128, 128, 1, 2>(p, tq, tkv, s);
     if (cfg == 1) return launch_tc<128, 64, 1, 2>(p, tq, tkv, s);

@@ -247,14 +247,9 @@ cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_hal
 
 }  // namespace
 
-static int getenv_int(const char* k) {
-  const char* v = std::getenv(k);
-  return v ? std::atoi(v) : 0;
-}
-
 bool dense_tc_supported(int d) { return d % 256 == 0; }
 
-bool recon_pair_mode(int B) { return (B <= 128 || B % 256 == 0) && getenv_int("HC_TC_1SM") == 0; }
+bool recon_pair_mode(int B, const Tuning& t) { return (B <= 128 || B % 256 == 0) && t.tc_1sm == 0; }
 
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s) {
   if (p.M <= 0) return cudaSuccess;
@@ -290,7 +285,7 @@ bool recon_tc_supported(int d, int H, int dh, int B) {
 }
 
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
-                            const void* tmap_w_half, int num_sms, cudaStream_t s) {
+                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s) {
   if (p.n_hblocks <= 0) return cudaSuccess;
   pg::TcArgs a{};
   a.gather = p.gather;
@@ -323,17 +318,15 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   // Default schedule: n-major raster with 2 n-tiles per group, so pairs p and p^1 of a wave
   // share one A panel and every wave shares the group's W panels; the partner lockstep
   // makes the shared A panel hit in L2 (measured: DRAM reads 190 GB -> ~60 GB at OPT-66B).
-  a.group_m = getenv_int("HC_GROUP_M") != 0 ? getenv_int("HC_GROUP_M") : -2;
-  a.l2_hint = getenv_int("HC_L2HINT");
-  const int sw = getenv_int("HC_SYNC_W");
-  a.sync_w = sw != 0 ? sw : 8;
+  a.group_m = t.group_m != 0 ? t.group_m : -2;
+  a.l2_hint = t.l2_hint;
+  a.sync_w = t.sync_w >= 0 ? t.sync_w : 8;
   a.sync = (a.sync_w > 0 && a.group_m == -2) ? p.sync_counter : nullptr;
-  const bool pair_mode = recon_pair_mode(p.B) || p.rope_inv || p.epi_attend;
+  const bool pair_mode = recon_pair_mode(p.B, t) || p.rope_inv || p.epi_attend;
   if (pair_mode) {
-    const int nsub_env = getenv_int("HC_TC_NSUB");
     const bool can2 = (2 * p.d) % 512 == 0;
-    if (can2 && nsub_env != 1) {
-      if (getenv_int("HC_TC_STAGES") == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s);
+    if (can2 && t.tc_nsub != 1) {
+      if (t.tc_stages == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s);
       return launch_pair<2, 4>(a, tmap_x, tmap_w_half, num_sms, s);
     }
     return launch_pair<1, 6>(a, tmap_x, tmap_w_half, num_sms, s);

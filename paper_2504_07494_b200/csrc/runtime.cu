@@ -128,14 +128,43 @@ bool make_tmap_2d(CUtensorMap* m, void* base, uint64_t inner, uint64_t outer, ui
   cuuint64_t strides[1] = {inner * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  const char* pe = std::getenv("HC_PROMO");
-  const int promo = pe ? std::atoi(pe) : 3;
-  const CUtensorMapL2promotion pr = promo == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                    : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// The library's only environment read: schedule / A-B knobs, once per hc_pool_create
+// (see internal.h Tuning).  Unparsable values keep the default.
+int env_int(const char* k, int dflt) {
+  const char* v = std::getenv(k);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  const long x = std::strtol(v, &end, 10);
+  return (end && *end == 0) ? (int)x : dflt;
+}
+Tuning tuning_from_env() {
+  Tuning t;
+  t.fused = env_int("HC_FUSED", t.fused);
+  t.epi_attend = env_int("HC_EPI_ATTEND", t.epi_attend);
+  t.fused_cfg = env_int("HC_FUSED_CFG", t.fused_cfg);
+  t.group_n = env_int("HC_GROUP_N", t.group_n);
+  t.sync_w = env_int("HC_SYNC_W", t.sync_w);
+  t.group_m = env_int("HC_GROUP_M", t.group_m);
+  t.l2_hint = env_int("HC_L2HINT", t.l2_hint);
+  t.tc_1sm = env_int("HC_TC_1SM", t.tc_1sm);
+  t.tc_nsub = env_int("HC_TC_NSUB", t.tc_nsub);
+  t.tc_stages = env_int("HC_TC_STAGES", t.tc_stages);
+  t.attn_cfg = env_int("HC_ATTN_CFG", t.attn_cfg);
+  t.prefill_tc = env_int("HC_PREFILL_TC", t.prefill_tc);
+  t.prefill_cfg = env_int("HC_PREFILL_CFG", t.prefill_cfg);
+  t.z_cfg = env_int("HC_Z_CFG", t.z_cfg);
+  t.score_st = env_int("HC_SCORE_ST", t.score_st);
+  t.qt_bn = env_int("HC_QT_BN", t.qt_bn);
+#ifdef HC_DIAG
+  t.diag_epi = env_int("HC_DIAG_EPI", 0);
+  t.diag_box = env_int("HC_DIAG_BOX", 0);
+#endif
+  return t;
 }
 
 struct DeviceGuard {
@@ -182,6 +211,7 @@ struct Plan {
 struct hc_pool {
   hc_pool_config cfg{};
   Layout L{};
+  Tuning tune{};   // read once at create
   size_t elem = 2;
   bool accounting = false;
   bool has_bias = false;
@@ -299,12 +329,8 @@ struct hc_pool {
     P.n_req = (int32_t)rs.size();
     P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
     P.absorb = (cfg.flags & HC_FLAG_ABSORB_HIDDEN) != 0;
-    {
-      const char* ea = std::getenv("HC_EPI_ATTEND");   // 0: rebuild K/V into scratch instead
-      P.attend = !P.absorb && tc_ok && cfg.dtype == HC_BF16 && !(ea && std::atoi(ea) == 0) &&
-                 recon_pair_mode(B);
-      P.seg = std::min(B, 32);
-    }
+    P.attend = !P.absorb && tc_ok && cfg.dtype == HC_BF16 && tune.epi_attend != 0 && recon_pair_mode(B, tune);
+    P.seg = std::min(B, 32);
     for (auto* r : rs) {
       const int64_t nb = cdiv(r->n, B);
       const int32_t ns = (int32_t)cdiv(nb, P.split_blocks);
@@ -327,9 +353,7 @@ struct hc_pool {
       }
     }
     P.Hp = (int32_t)align_up((size_t)H, 16);
-    const char* fe = std::getenv("HC_FUSED");
-    const int fused_env = fe ? std::atoi(fe) : -1;
-    P.fused = !P.absorb && tc_ok && P.n_hb > 0 && fused_env != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
+    P.fused = !P.absorb && tc_ok && P.n_hb > 0 && tune.fused != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
               fused_supported(cfg.d_model, cfg.n_heads, cfg.head_dim, B);
     if (P.fused) {
       P.gemm_m_tiles = (int32_t)cdiv((int64_t)P.n_hb * B, fused_tile_m());
@@ -443,6 +467,7 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   hc_pool* p = new hc_pool();
   p->cfg = *cfg;
   p->L = L;
+  p->tune = tuning_from_env();
   p->elem = e;
   p->accounting = accounting;
   p->has_bias = cfg->b_kv != nullptr;
@@ -503,8 +528,8 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     }
     if (cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) &&
         recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)) {
-      // HC_DIAG_BOX=1 (timing diagnostic only, wrong results): 128-row A boxes as if dense
-      const uint32_t rpb = std::getenv("HC_DIAG_BOX") ? 128u : (uint32_t)std::min(cfg->block_size, 128);
+      // -DHC_DIAG builds, HC_DIAG_BOX=1 (timing diagnostic, wrong results): 128-row A boxes as if dense
+      const uint32_t rpb = p->tune.diag_box ? 128u : (uint32_t)std::min(cfg->block_size, 128);
       const bool ok1 = make_tmap_2d(&p->tmap_x, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
                                     (uint64_t)cfg->num_blocks * cfg->block_size, 64, rpb);
       const bool ok2 = make_tmap_2d(&p->tmap_w, p->storage + L.w_off, (uint64_t)cfg->d_model,
@@ -925,13 +950,13 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
           !make_tmap_2d(&tm_w, pool->storage + pool->L.w_off, dd, 2 * dd, 64, (uint32_t)bp.dh) ||
           !make_tmap_2d(&tm_z, ws + P.off_z, dd, (uint64_t)H * P.n_h, 64, 128))
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (absorbed path)");
-      err = launch_absorbed(bp, &pool->tmap_x, &pool->tmap_x64, &tm_qt, &tm_p, &tm_w, &tm_z, &tm_w, s);
+      err = launch_absorbed(bp, &pool->tmap_x, &pool->tmap_x64, &tm_qt, &tm_p, &tm_w, &tm_z, &tm_w, pool->tune, s);
       if (err != cudaSuccess) return cuda_fail(err, "absorbed hidden attention");
       launches += absorb_launches();
     }
     if (pool->profiling) cudaEventRecord(ev[2], s);
     if (P.n_splits > 0) {
-      err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
+      err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s);
       if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
       ++launches;
     }
@@ -942,7 +967,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     ap.n_kv_tasks = P.n_kv_splits * H;
     ap.n_hid_splits = P.n_hid_splits;
     err = launch_fused(rp, ap, &pool->tmap_x, &pool->tmap_w_half, reinterpret_cast<int32_t*>(ws + P.off_tiledone),
-                       pool->num_sms, s);
+                       pool->num_sms, pool->tune, s);
     if (err != cudaSuccess) return cuda_fail(err, "fused step kernel");
     ++launches;
     if (pool->profiling) {
@@ -951,13 +976,13 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     }
   } else {
     if (P.n_hb > 0) {
-      err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, s)
+      err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, pool->tune, s)
                         : launch_recon_simt(rp, pool->cfg.dtype, s);
       if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
       ++launches;
     }
     if (pool->profiling) cudaEventRecord(ev[2], s);
-    err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, s);
+    err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s);
     if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
     ++launches;
     if (pool->profiling) cudaEventRecord(ev[3], s);
@@ -1200,10 +1225,10 @@ struct PrefillPlan {
 };
 // query rows per prefill attention tile: 128 on the tcgen05 kernel, 64 on the mma.sync one
 bool prefill_uses_tc(const hc_pool* pool) {
-  return prefill_attn_tc_enabled() && prefill_attn_mma_supported(pool->cfg.dtype, pool->cfg.head_dim) &&
+  return pool->tune.prefill_tc != 0 && prefill_attn_mma_supported(pool->cfg.dtype, pool->cfg.head_dim) &&
          !(pool->cfg.flags & HC_FLAG_FORCE_SIMT);
 }
-int prefill_tile_rows(const hc_pool* pool) { return prefill_uses_tc(pool) ? prefill_attn_tc_rows() : 64; }
+int prefill_tile_rows(const hc_pool* pool) { return prefill_uses_tc(pool) ? prefill_attn_tc_rows(pool->tune) : 64; }
 
 PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens) {
   PrefillPlan P;
@@ -1380,9 +1405,9 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   if (prefill_uses_tc(pool)) {
     CUtensorMap tq, tkv;
     if (!make_tmap_2d(&tq, ws + P.off_q, (uint64_t)d, (uint64_t)P.rows, 64, 128) ||
-        !make_tmap_2d(&tkv, ws + P.off_kv, 2 * (uint64_t)d, (uint64_t)P.rows, 64, (uint32_t)prefill_attn_tc_keys()))
+        !make_tmap_2d(&tkv, ws + P.off_kv, 2 * (uint64_t)d, (uint64_t)P.rows, 64, (uint32_t)prefill_attn_tc_keys(pool->tune)))
       return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (prefill attention)");
-    err = launch_prefill_attn_tc(pa, &tq, &tkv, s);
+    err = launch_prefill_attn_tc(pa, &tq, &tkv, pool->tune, s);
   } else {
     err = launch_prefill_attn(pa, pool->cfg.dtype, s);
   }

@@ -250,7 +250,8 @@ def by_name(name: str) -> Workload:
     if name in ("cfg4", "opt66b"):
         return cfg4()
     if name.startswith("cfg5:"):
-        return cfg5(float(name.split(":", 1)[1]))
+        from fractions import Fraction
+        return cfg5(float(Fraction(name.split(":", 1)[1])))   # "cfg5:1/32" or "cfg5:0.03125"
     raise KeyError(name)
 
 

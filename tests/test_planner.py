@@ -171,3 +171,17 @@ def test_native_planner_time_vs_candidates(lib):
             native_schedule(lib, cfg, reqs, 1000.0)
         dt = (time.perf_counter() - t0) / 20 * 1e3
         assert dt < ms, (n, dt)
+
+
+def test_greedy_ties_follow_request_id_not_input_order(lib):
+    """SPEC S:376 / S:412: equal theta and delta-m -> the lower request id is accepted first, so
+    the decision does not depend on the order requests are handed in (oracle and native)."""
+    # four identical running requests (same p, same m); budget fits exactly two hidden stages
+    reqs = [_req(i, 4.0, 8) for i in (7, 3, 9, 1)]
+    cfg = dict(BASE, rho=0.01, total_units=8.0)
+    for order in ([0, 1, 2, 3], [3, 2, 1, 0], [2, 0, 3, 1]):
+        rr = [reqs[k] for k in order]
+        for sched in (PO.schedule, lambda c, r, t: native_schedule(lib, c, r, t)):
+            a, b, _, _ = sched(cfg, rr, 100.0)
+            picked = sorted(r["id"] for r, x in zip(rr, a) if x)
+            assert picked == [1, 3], (order, picked)
