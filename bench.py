@@ -10,9 +10,13 @@ long contexts (lognormal, <= 4096), 50% hidden, bf16, on one B200.
   python bench.py [--gpus N --steps K --warmup W] [--config cfg4|cfg2|cfg3|cfg5:<h>]
   python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
 
-Multi-GPU (torchrun, one process per GPU): weak scaling — every rank processes its own
-full batch of the same recipe (request ids offset by rank), no data-path collective
-(task rule ⑤); the time is the max over ranks.
+Multi-GPU (one process per GPU; `--gpus N` without torchrun spawns the N ranks itself):
+cfg3/cfg4 run STRONG scaling by default — one batch of the recipe split across ranks by LPT on
+the cost model, each rank owning its requests' blocks and a W_KV replica —
+and every step ends with the NCCL all-gather of every rank's (out, lse) (north_star's output
+gather; `--no-gather` drops it).  `--weak` gives every rank its own full batch instead.  The
+time is the max over ranks.  The GPU arm never imports oracle/ or tests/: the oracle runs
+only in the cpu_baseline leg and in `--impl reference`.
 """
 from __future__ import annotations
 
@@ -279,14 +283,15 @@ def run_split(args, rank: int, world: int, local: int, w0):
 
     from paper_2504_07494_b200 import hc
     from synth.configs import MODE_KV
+    from synth import drive as T
     from synth.partition import lpt_split
-    from tests import hc_testlib as T
 
     d, Hh, B = w0.shape.d, w0.shape.H, w0.block_size
     plans = lpt_split(w0.n, w0.modes, d, world, B)
     mine = plans[rank]
     wr = w0.subset(sorted({i for i, _, _ in mine}) or [0])
-    nblk = sum((2 if w0.modes[i] == MODE_KV else 1) * -(-(t1 - t0) // B) for i, t0, t1 in mine)
+    dt = hc.HC_BF16 if w0.dtype == "bf16" else hc.HC_F32
+    nblk = sum(hc.units_needed(d, Hh, w0.shape.dh, B, w0.modes[i], t1 - t0, dt) for i, t0, t1 in mine)
     pool = T.make_pool(wr, device=local, num_blocks=int(nblk * 1.05) + 8)
     dev = torch.device("cuda", local)
     pid = [10_000_000 + 100_000 * rank + j for j in range(len(mine))]
@@ -351,14 +356,12 @@ def run_split(args, rank: int, world: int, local: int, w0):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     n_split = sum(1 for x in parts_of if len(x) > 1)
-    check = None
-    if rank == 0 and os.environ.get("HC_BENCH_CHECK"):
-        # oracle on the longest split request (or the longest request): a few heads
-        cand = [i for i, x in enumerate(parts_of) if len(x) > 1] or [int(np.argmax(w0.n))]
-        i = max(cand, key=lambda j: w0.n[j])
-        heads = [0, Hh // 2, Hh - 1]
-        err, lerr = T.compare(w0, out_all[[i]].cpu().numpy(), lse_all[[i]].cpu().numpy(), [i], {i: heads})
-        check = {"request": i, "n": w0.n[i], "parts": len(parts_of[i]), "max_rel_err": err, "lse_err": lerr}
+    dump = os.environ.get("HC_BENCH_DUMP")
+    if rank == 0 and dump:
+        # test hook: the merged (out, lse) of every request, checked against the oracle by
+        # tests/test_multiproc.py (the bench itself never runs the oracle on this path)
+        np.savez(dump, out=out_all.cpu().numpy(), lse=lse_all.cpu().numpy(),
+                 parts=np.array([len(x) for x in parts_of]))
     if rank == 0:
         print(json.dumps({
             "metric": "decode-attention req-layers/s (hybrid KV/hidden cache, one layer)",
@@ -368,11 +371,137 @@ def run_split(args, rank: int, world: int, local: int, w0):
             "config": {"workload": w0.name, "parallelism": f"request-sharded x{world} (strong, LPT + token-range split)",
                        "split_requests": n_split, "max_parts": P,
                        "output": "all-gather of (out, lse) parts + hc_merge_partials, every step (timed)"},
-            "gpu_launches": (pool.last_launch_count() + 1) * args.steps, "check": check}), flush=True)
+            "gpu_launches": (pool.last_launch_count() + 1) * args.steps}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+# ============================================================================ launch plumbing
+def spawn_ranks(n: int, build: bool = True) -> int:
+    """`python bench.py --gpus N` outside torchrun: build libhc.so once, then launch N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1 with the same arguments;
+    rank 0's JSON line is this process's output."""
+    import socket
+    if build:
+        from paper_2504_07494_b200 import build as hb
+        hb.build()
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_dist(local: int):
+    """One process group per job: NCCL over NVLink (device-bound) — HC_BENCH_BACKEND=gloo is
+    the CPU test hook.  NCCL's INIT log stays on (stderr) so the communicator's rank count is
+    on record."""
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("HC_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+
+
+def shard_workload(args, w0, rank: int, world: int):
+    """This rank's requests: LPT share of one batch (strong) or its own full batch (weak)."""
+    from synth import configs as C
+    if args.strong:
+        from synth.partition import strong_shard
+        return strong_shard(w0, rank, world)
+    return C.shard_for_rank(w0, rank, world)
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    """Every multi-GPU time is the max over ranks (all-reduce MAX of the device-timed value)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class OutputGather:
+    """north_star's output gather: every step, each rank's (out, lse) rows (padded to the
+    largest shard) are all-gathered so every rank holds the whole batch's output."""
+
+    def __init__(self, w, n_req: int, world: int, device):
+        import torch
+        import torch.distributed as dist
+        n_max = torch.tensor([n_req], device=device)
+        dist.all_reduce(n_max, op=dist.ReduceOp.MAX)
+        self.n_req, self.n_max, self.d, self.H = n_req, int(n_max.item()), w.shape.d, w.shape.H
+        self.send = torch.zeros((self.n_max, self.d + self.H), dtype=torch.float32, device=device)
+        self.recv = torch.empty((world * self.n_max, self.d + self.H), dtype=torch.float32, device=device)
+
+    def __call__(self, out, lse):
+        import torch.distributed as dist
+        self.send[:self.n_req, :self.d].copy_(out)
+        self.send[:self.n_req, self.d:].copy_(lse)
+        dist.all_gather_into_tensor(self.recv, self.send)
+
+    def describe(self) -> str:
+        import torch.distributed as dist
+        return (f"{dist.get_backend()} all-gather of out+lse every step (timed), "
+                f"{self.recv.numel() * 4} B gathered per step")
+
+
+def run_dry(args, rank: int, world: int) -> int:
+    """Test hook (HC_BENCH_DRY=1, CPU, gloo): the N>1 control path of the main arm — rank
+    plumbing, strong/weak sharding, the output gather, barriers and the max over ranks — with
+    zero-filled outputs in place of the decode kernel, timed on the host clock.  Prints the
+    same line shape with "dry": true; never a bench number."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        init_dist(0)
+    w0 = workload_from(args.config)
+    args.strong = strong_default(args, w0, world)
+    w = shard_workload(args, w0, rank, world)
+    n_req = len(w.n)
+    out = torch.zeros((n_req, w.shape.d))
+    lse = torch.zeros((n_req, w.shape.H))
+    gather = OutputGather(w, n_req, world, "cpu") if (not args.no_gather and world > 1) else None
+    for _ in range(args.warmup):
+        if gather:
+            gather(out, lse)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if gather:
+            gather(out, lse)
+    if world > 1:
+        dist.barrier()
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / max(args.steps, 1), world, "cpu")
+    n_total = len(w0.n) if args.strong else world * n_req
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": n_total / (ms / 1e3), "unit": "req-layers/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "dry": True,
+                          "scaling": "strong" if args.strong else "weak",
+                          "config": {"workload": w.name, "n_req_per_rank0": n_req, "n_req_total": n_total,
+                                     "output_gather": gather.describe() if gather else "none"}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def strong_default(args, w0, world: int) -> bool:
+    """cfg3/cfg4 (and the cfg5 sweep) are strong-scaling configurations — a
+    fixed batch split across ranks; cfg2 and `--weak` keep a full batch per rank."""
+    if args.weak or world == 1:
+        return False
+    return args.strong or args.split or w0.name.split("-")[0] in ("cfg3", "cfg4", "cfg5")
 
 
 # ============================================================================ main arm
@@ -390,7 +519,9 @@ def main():
     ap.add_argument("--prefill-len", type=int, default=1024)
     ap.add_argument("--prefill-reqs", type=int, default=16)
     ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: one batch split across ranks by LPT (default: weak)")
+                    help="strong scaling: one batch split across ranks by LPT (default for cfg3/cfg4/cfg5)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank processes its own full batch of the recipe")
     ap.add_argument("--rope", type=float, default=0.0,
                     help="RoPE base theta (NEXT row f4 (i)): rebuilt K rotated at its positions")
     ap.add_argument("--absorb", action="store_true",
@@ -399,9 +530,9 @@ def main():
     ap.add_argument("--split", action="store_true",
                     help="with --strong: split requests costlier than total/world across ranks "
                          "(SURVEY §8(e) phase 2) and merge their (out, lse) parts after an all-gather")
-    ap.add_argument("--gather", action="store_true",
-                    help="N>1: all-gather every rank's out + lse over NCCL after each step, inside the "
-                         "timed region (north_star's output gather; not a data-path exchange)")
+    ap.add_argument("--no-gather", action="store_true",
+                    help="N>1: skip the all-gather of every rank's out + lse over NCCL after each step "
+                         "(north_star's output gather, on by default, inside the timed region)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay variant")
@@ -409,6 +540,8 @@ def main():
                     help="run only N untimed steps (for ncu); prints nothing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus, build=not os.environ.get("HC_BENCH_DRY"))
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -419,6 +552,8 @@ def main():
         local = 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if os.environ.get("HC_BENCH_DRY"):
+        return run_dry(args, rank, world)
     if args.mode != "decode":
         return run_module_mode(args, rank, world, local)
 
@@ -426,26 +561,19 @@ def main():
     import torch.distributed as dist
 
     from paper_2504_07494_b200 import build as hb
-    hb.build()
+    hb.build()   # file-locked: concurrent ranks wait for one build
     from paper_2504_07494_b200 import hc
     from synth import configs as C
-    from tests import hc_testlib as T
+    from synth import drive as T
 
     torch.cuda.set_device(local)
     if world > 1:
-        backend = os.environ.get("HC_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        init_dist(local)
     w0 = workload_from(args.config)
+    args.strong = strong_default(args, w0, world)
     if args.split:
         return run_split(args, rank, world, local, w0)
-    if args.strong:
-        from synth.partition import strong_shard
-        w = strong_shard(w0, rank, world)
-    else:
-        w = C.shard_for_rank(w0, rank, world)
+    w = shard_workload(args, w0, rank, world)
     pool = T.make_pool(w, device=local, split_tokens=args.split_tokens,
                        flags=hc.HC_FLAG_ABSORB_HIDDEN if args.absorb else 0, rope_theta=args.rope)
     T.fill(pool, w, device=local)
@@ -457,21 +585,12 @@ def main():
     ws = pool.workspace(ids)
     stream = torch.cuda.current_stream()
 
-    gather = args.gather and world > 1
-    if gather:
-        # every rank holds n_req rows in weak scaling; strong scaling pads to the max
-        n_max = torch.tensor([n_req], device="cuda")
-        dist.all_reduce(n_max, op=dist.ReduceOp.MAX)
-        n_max = int(n_max.item())
-        send = torch.zeros((n_max, w.shape.d + 2 * w.shape.H), dtype=torch.float32, device="cuda")
-        recv = torch.empty((world * n_max, send.shape[1]), dtype=torch.float32, device="cuda")
+    gather = OutputGather(w, n_req, world, "cuda") if (not args.no_gather and world > 1) else None
 
     def step():
         hc.hc_decode_attention(pool.handle, ids, q, w.scale, out, lse, ws, stream)
         if gather:
-            send[:n_req, :w.shape.d].copy_(out)
-            send[:n_req, w.shape.d:w.shape.d + w.shape.H].copy_(lse)
-            dist.all_gather_into_tensor(recv, send)
+            gather(out, lse)
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -509,10 +628,7 @@ def main():
     pct = {"p10": per_step[int(0.1 * (len(per_step) - 1))], "p50": statistics.median(per_step),
            "p90": per_step[int(0.9 * (len(per_step) - 1))], "max": per_step[-1],
            "max_step": per_step_raw.index(per_step[-1])}
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, "cuda")
     n_total = len(w0.n) if args.strong else world * n_req
     value = n_total / (ms / 1e3)
 
@@ -567,11 +683,7 @@ def main():
             lse_host.copy_(lse, non_blocking=True)
         f1.record(stream)
         torch.cuda.synchronize()
-        ms_e2e = f0.elapsed_time(f1) / args.steps
-        if world > 1:
-            t = torch.tensor([ms_e2e], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
+        ms_e2e = max_over_ranks(f0.elapsed_time(f1) / args.steps, world, "cuda")
         e2e = {"value": n_total / (ms_e2e / 1e3), "unit": "req-layers/s",
                "h2d_bytes_per_step": q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size(),
@@ -614,9 +726,10 @@ def main():
             "ms": t_rec, "bound": "tensor", "unit": "TFLOP/s",
             "achieved": (F_alg / (t_rec / 1e3) / 1e12) if t_rec > 0 else None, "flops_per_launch": F_alg,
             "note": "GEMM + split-K attention warps in one kernel; FLOP/s counts the GEMM only" if fused else ""},
-        "attention": {"ms": t_att, "bound": "hbm", "unit": "GB/s",
-                      "bytes_per_launch": (kv_tok + hid_tok) * 2 * d * s,
-                      "achieved": ((kv_tok + hid_tok) * 2 * d * s / (t_att / 1e3) / 1e9) if t_att > 0 else None},
+        "attention": ({"ms": None, "note": "n/a: the attention runs inside fused_step_kernel"} if fused else
+                      {"ms": t_att, "bound": "hbm", "unit": "GB/s",
+                       "bytes_per_launch": (kv_tok + hid_tok) * 2 * d * s,
+                       "achieved": ((kv_tok + hid_tok) * 2 * d * s / (t_att / 1e3) / 1e9) if t_att > 0 else None}),
         "combine": {"ms": t_comb},
         "descriptor_upload": {"ms": t_up},
     }
@@ -630,7 +743,7 @@ def main():
             "note": "5 kernels: q~, scores, Z and W_V GEMMs on tcgen05, P rescale; bytes = x read twice + W_K + W_V + q~/Z round trips"}
         dom = "absorbed_hidden" if t_rec >= t_att else "attention"
     else:
-        dom = ("fused_step" if fused else "recon_gemm") if t_rec >= t_att else "attention"
+        dom = ("fused_step" if fused else "recon_gemm") if (fused or t_rec >= t_att) else "attention"
     k = kernels[dom]
     if dom == "absorbed_hidden":
         roof = {"bound": "hbm", "kernel": "absorbed qt/score/rescale/z/wv kernels", "achieved": k["achieved"],
@@ -640,7 +753,9 @@ def main():
         peak = tf_peak
         roof = {"bound": "tensor", "kernel": "fused_step_kernel (<3,5,2> or, KV-dominated, <2,8,2>)" if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
-                "unit": "TFLOP/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get(dom),
+                "unit": "TFLOP/s", "frac": k["achieved"] / peak,
+                "frac_vs_burst": k["achieved"] / tf_burst, "frac_vs_sustained": k["achieved"] / tf_sus,
+                "traffic": TRAFFIC.get(w.name, {}).get(dom),
                 "ncu_tensor_pipe_pct": TRAFFIC.get(w.name, {}).get(dom + "_tensor_pipe_pct"),
                 "peak_kind": tf_kind}
     else:
@@ -657,7 +772,7 @@ def main():
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
-                   "output_gather": f"{dist.get_backend()} all-gather of out+lse every step (timed)" if gather else "none",
+                   "output_gather": gather.describe() if gather else "none",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
                    "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
                    else "paper (hidden K/V rebuilt every step)",
@@ -689,8 +804,8 @@ def run_module_mode(args, rank, world, local):
     hb.build()
     from paper_2504_07494_b200 import hc
     from synth import configs as C
+    from synth import drive as T
     from synth.configs import Workload
-    from tests import hc_testlib as T
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -112,6 +112,12 @@ typedef struct {
  * Returns 0 for an invalid config. */
 size_t hc_pool_storage_bytes(const hc_pool_config* cfg);
 
+/* Unit blocks a request of n_tokens tokens occupies in `mode` under this config (the
+ * allocation rule of hc_append: KV takes a K and a V unit per B tokens, hidden one unit per
+ * B tokens).  For sizing pools.  Returns -1 for an invalid config/mode or
+ * n_tokens < 0.  Host only. */
+int64_t hc_units_needed(const hc_pool_config* cfg, int32_t mode, int64_t n_tokens);
+
 /* Create a pool ("unified block-wise memory pool").  Zero-fills the block
  * region (so padding rows of a partly filled block are finite), copies W_KV / b_KV into
  * storage, and builds TMA descriptors.  Synchronous w.r.t. the device (cudaDeviceSynchronize

@@ -142,15 +142,22 @@ def head_output(q_h, X, W_K_h, W_V_h, scale: float, b_K_h=None, b_V_h=None):
     return o, l[0]
 
 
-def layer_norm(X, gamma, beta=None, eps: float = 1e-5):
+def layer_norm(X, gamma, beta=None, eps: float = 1e-5, store: Optional[str] = None):
     """Pre-attention LayerNorm of OPT-style layers (the paper's Eq. 1
     specifies none, DESIGN R4/R15): per row, (x - mean) / sqrt(var + eps) * gamma + beta
-    with the population variance over the d features."""
+    with the population variance over the d features.
+    store="bf16" (DESIGN R16): u is a STORED vector — the hidden cache holds it (R15) in the
+    storage precision (R9), and it is the input Eq. 1 multiplies — so the result is rounded
+    once to bf16 (round-to-nearest-even), exactly as the oracle takes stored bf16 x as given."""
     X = _f64(X)
     mu = X.mean(axis=-1, keepdims=True)
     var = ((X - mu) ** 2).mean(axis=-1, keepdims=True)
     Y = (X - mu) / np.sqrt(var + eps) * _f64(gamma)
-    return Y + (0.0 if beta is None else _f64(beta))
+    Y = Y + (0.0 if beta is None else _f64(beta))
+    if store == "bf16":
+        import torch
+        Y = torch.from_numpy(np.ascontiguousarray(Y)).to(torch.bfloat16).to(torch.float64).numpy()
+    return Y
 
 
 def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float,
@@ -161,8 +168,9 @@ def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float
     the cached K, V; hidden mode appends x_t to the cached X and rebuilds K, V from all of X
     (P:269); then Eq. 2-3 with the output map y = W_O o (+b_O) (Eq. 3).
     cache = {'mode': 0, 'K': [n-1, d], 'V': [n-1, d]} or {'mode': 1, 'X': [n-1, d]}.
-    ln = (gamma, beta, eps) or None: the projections see u_t = LN(x_t), and a hidden cache
-    holds u (the vector Eq. 1 multiplies; reading R15) — cache['X'] rows are stored u's.
+    ln = (gamma, beta, eps[, store]) or None: the projections see u_t = LN(x_t), and a hidden
+    cache holds u (the vector Eq. 1 multiplies; reading R15) — cache['X'] rows are stored u's;
+    store = "bf16" rounds u_t to the storage precision (reading R16).
     Returns y [d], q [d], lse [H], and the context the attention saw (dict)."""
     x_t, W_Q, W_O = _f64(x_t), _f64(W_Q), _f64(W_O)
     if ln is not None:

@@ -157,6 +157,7 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     }
   };
   load_task(ptask);
+  const uint64_t kv_pol = (lane == 0 && p.kv_evict_first) ? ptx::policy_evict_first() : 0;
   uint4 qr0 = make_uint4(0, 0, 0, 0), qr1 = qr0, qr2 = qr0;   // QREG: q_h slot per stage
 
   // issue the next chunk of the producer stream into `stage`; false when no work is left
@@ -183,8 +184,13 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       uint8_t* sb = stage_base + stage * C::STAGE;
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive_expect_tx(&bars[stage], 2 * C::CHUNK + (first ? C::QB : 0));
-      ptx::bulk_g2s(sb, ksrc, C::CHUNK, &bars[stage]);
-      ptx::bulk_g2s(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage]);
+      if (p.kv_evict_first && prq.mode == 0) {   // KV-mode chunks are read exactly once
+        ptx::bulk_g2s_hint(sb, ksrc, C::CHUNK, &bars[stage], kv_pol);
+        ptx::bulk_g2s_hint(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage], kv_pol);
+      } else {
+        ptx::bulk_g2s(sb, ksrc, C::CHUNK, &bars[stage]);
+        ptx::bulk_g2s(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage]);
+      }
       if (!QREG && first)
         ptx::bulk_g2s(sb + 2 * C::CHUNK, qg + (size_t)psp.req * d + phead * DH, C::QB, &bars[stage]);
     }

@@ -159,7 +159,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // n-major raster, 4 n-tiles per group: four pairs of a wave share each A panel (same-box
   // A/B vs 2: cfg4 -2.5%, cfg5 1/32 -2..-4%)
   a.group_m = -(t.group_n >= 1 ? t.group_n : 4);
-  a.l2_hint = 0;
+  a.l2_hint = t.l2_hint;
   // Partner lockstep off by default in the fused kernel: with the attend epilogue, tiles of
   // partner pairs finish at different times and the spin costs more than the L2 reuse buys
   // (same-box A/B: cfg4 -2.5%, cfg3 -2%, cfg2 -1%, crossover neutral).

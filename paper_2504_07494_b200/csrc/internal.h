@@ -20,7 +20,8 @@ struct Tuning {
   int group_n = 4;       // HC_GROUP_N: n-tiles per raster group of the fused kernel
   int sync_w = -1;       // HC_SYNC_W: partner k-lockstep window (-1: kernel default, 0 off)
   int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM
-  int l2_hint = 0;       // HC_L2HINT
+  int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
+  int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
   int tc_1sm = 0;        // HC_TC_1SM: 1-SM tcgen05 reconstruction kernel instead of CTA pairs
   int tc_nsub = 0;       // HC_TC_NSUB: 1 = 256-wide pair tiles
   int tc_stages = 4;     // HC_TC_STAGES (3 or 4)
@@ -76,6 +77,7 @@ struct AttnParams {
   int32_t n_hid_splits;
   const int32_t* tile_done;      // [gemm_m_tiles][gemm_n_tiles] finished epilogue warps (8 = ready)
   int32_t gemm_n_tiles, gemm_tile_m, gemm_tile_n;
+  int32_t kv_evict_first;        // 1: KV chunks are streamed with an L2 evict-first policy
 };
 
 struct CombineParams {

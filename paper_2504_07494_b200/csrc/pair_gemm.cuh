@@ -40,7 +40,7 @@ struct TcArgs {
   __nv_bfloat16* scr_v;
   const float* bias;
   int32_t group_m;      // raster group (m-tiles sweeping all n-tiles); < 0: n-major, -group_m n-tiles
-  int32_t l2_hint;      // 0 none, 1 A evict_last + W evict_first, 2 the reverse
+  int32_t l2_hint;      // 0 none, 1 A evict_last + W evict_first, 2 the reverse, 3 A normal + W evict_last
   int32_t* sync;        // zeroed per-pair progress words (stride 32 ints), nullptr = off
   int32_t sync_w;       // partner lockstep window in k-steps
   int32_t* tile_done;   // nullable: per (m-tile, n-tile) count of finished epilogue warps (8 = ready)
@@ -384,8 +384,11 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
   if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
     if (lane == 0) {
-      const uint64_t pol_a = a.l2_hint == 2 ? ptx::policy_evict_first() : ptx::policy_evict_last();
-      const uint64_t pol_b = a.l2_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+      // l2_hint: 1 A evict_last + W evict_first, 2 the reverse, 3 A normal + W evict_last
+      const uint64_t pol_a = a.l2_hint == 2   ? ptx::policy_evict_first()
+                             : a.l2_hint == 3 ? ptx::policy_evict_normal()
+                                              : ptx::policy_evict_last();
+      const uint64_t pol_b = a.l2_hint == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       int my_step = 0;

@@ -151,6 +151,7 @@ Tuning tuning_from_env() {
   t.sync_w = env_int("HC_SYNC_W", t.sync_w);
   t.group_m = env_int("HC_GROUP_M", t.group_m);
   t.l2_hint = env_int("HC_L2HINT", t.l2_hint);
+  t.kv_evict_first = env_int("HC_KV_EF", t.kv_evict_first);
   t.tc_1sm = env_int("HC_TC_1SM", t.tc_1sm);
   t.tc_nsub = env_int("HC_TC_NSUB", t.tc_nsub);
   t.tc_stages = env_int("HC_TC_STAGES", t.tc_stages);
@@ -281,7 +282,10 @@ struct hc_pool {
         r.cap = cap;
       }
     }
-    if (!p->ev && cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (!p->ev) {   // events belong to the pool's device (callers hold a DeviceGuard; be safe anyway)
+      DeviceGuard g(cfg.device);
+      if (cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
     return p;
   }
 
@@ -295,8 +299,9 @@ struct hc_pool {
       p->pending = false;
       return;
     }
-    cudaEventRecord(p->ev, s);
-    p->pending = true;
+    // a failed record leaves the slot free (never "pending" on an event that was not recorded);
+    // the caller's next launch check reports the sticky error
+    p->pending = cudaEventRecord(p->ev, s) == cudaSuccess;
   }
 
   cudaEvent_t get_event() {
@@ -429,6 +434,15 @@ size_t hc_pool_storage_bytes(const hc_pool_config* cfg) {
     return 0;
   }
   return L.total;
+}
+
+int64_t hc_units_needed(const hc_pool_config* cfg, int32_t mode, int64_t n_tokens) {
+  Layout L;
+  if (!layout_for(cfg, &L) || n_tokens < 0 || (mode != HC_MODE_KV && mode != HC_MODE_HIDDEN)) {
+    g_err = "invalid config, mode or n_tokens";
+    return -1;
+  }
+  return cdiv(n_tokens, cfg->block_size) * (mode == HC_MODE_KV ? 2 : 1);
 }
 
 hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
@@ -647,12 +661,43 @@ static hc_status scatter_rows(hc_pool* pool, const std::vector<AppendReq>& ar, c
   return HC_OK;
 }
 
+// What validate_and_allocate changed, so a later failure in the same call can restore the
+// pool exactly ("validation errors leave the pool unchanged", hc.h; a retry must not append
+// the tokens twice).
+struct AllocUndo {
+  struct Entry {
+    int64_t id;
+    bool created;
+    int64_t n;
+    size_t na, nb;
+  };
+  std::vector<Entry> e;
+  void rollback(hc_pool* pool) {
+    for (auto it = e.rbegin(); it != e.rend(); ++it) {
+      auto f = pool->reqs.find(it->id);
+      if (f == pool->reqs.end()) continue;
+      Req& r = f->second;
+      for (size_t j = it->na; j < r.a.size(); ++j) pool->free_ids.push(r.a[j]);
+      for (size_t j = it->nb; j < r.b.size(); ++j) pool->free_ids.push(r.b[j]);
+      if (it->created) {
+        pool->reqs.erase(f);
+      } else {
+        r.a.resize(it->na);
+        r.b.resize(it->nb);
+        r.n = it->n;
+      }
+    }
+    e.clear();
+  }
+};
+
 // Validation + all-or-nothing allocation shared by hc_append and hc_project_append.
 // On success the requests' tables/lengths are extended and `ar`/`tabs` describe the new rows
 // (row_off = running row index per mode, in call order; one entry per request with t > 0).
 static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
                                        const int32_t* n_tokens, const void* k, const void* v, const void* x,
-                                       std::vector<AppendReq>* ar, std::vector<int32_t>* tabs, int32_t* max_rows) {
+                                       std::vector<AppendReq>* ar, std::vector<int32_t>* tabs, int32_t* max_rows,
+                                       AllocUndo* undo) {
   if (!req_ids || !modes || !n_tokens) return fail(HC_E_INVALID, "null id/mode/n_tokens array");
   const int B = pool->cfg.block_size;
   std::unordered_set<int64_t> seen;
@@ -682,7 +727,9 @@ static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64
   int32_t kv_off = 0, x_off = 0;
   *max_rows = 0;
   for (int32_t i = 0; i < n_req; ++i) {
+    const bool created = pool->reqs.find(req_ids[i]) == pool->reqs.end();
     Req& r = pool->reqs[req_ids[i]];
+    undo->e.push_back({req_ids[i], created, r.n, r.a.size(), r.b.size()});
     if (r.n == 0 && r.a.empty()) r.mode = modes[i];
     const int64_t t = n_tokens[i];
     const int64_t new_lb = cdiv(r.n + t, B) - cdiv(r.n, B);
@@ -724,10 +771,13 @@ hc_status hc_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const 
   std::vector<AppendReq> ar;
   std::vector<int32_t> tabs;
   int32_t max_rows = 0;
-  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, n_tokens, k, v, x, &ar, &tabs, &max_rows);
+  AllocUndo undo;
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, n_tokens, k, v, x, &ar, &tabs, &max_rows, &undo);
   if (st != HC_OK) return st;
   if (pool->accounting || ar.empty()) return HC_OK;
-  return scatter_rows(pool, ar, tabs, k, v, x, stream);
+  st = scatter_rows(pool, ar, tabs, k, v, x, stream);
+  if (st != HC_OK) undo.rollback(pool);
+  return st;
 }
 
 static hc_status collect(const hc_pool* pool, int32_t n_req, const int64_t* ids, std::vector<const Req*>* rs) {
@@ -766,6 +816,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   const Plan P = pool->plan(rs);
   if (ws_bytes < P.total) return fail(HC_E_WORKSPACE, "workspace smaller than hc_workspace_size()");
   const int B = pool->cfg.block_size, H = pool->cfg.n_heads;
+  DeviceGuard g(pool->cfg.device);   // before the staging slot: its event belongs to the pool's device
 
   // ---- descriptor (a3): requests, split-K work list, KV block tables, hidden gather list
   Pinned* pin = pool->pinned(P.desc_bytes);
@@ -849,7 +900,6 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     d.split_count = n_split - d.split_begin;
     rd[i] = d;
   }
-  DeviceGuard g(pool->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::array<cudaEvent_t, 5> ev{};
   if (pool->profiling) {
@@ -908,6 +958,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.B = B;
   ap.d = pool->cfg.d_model;
   ap.scale_log2 = scale * 1.4426950408889634f;
+  ap.kv_evict_first = pool->tune.kv_evict_first;
   pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
   if (P.absorb) {
     // f4 (ii): hidden requests never rebuild K/V; KV requests take the split-K path
@@ -1015,6 +1066,9 @@ static bool make_tmap_rows(CUtensorMap* m, const void* base, int rows, int d) {
   return make_tmap_2d(m, const_cast<void*>(base), (uint64_t)d, (uint64_t)rows, 64, 128);
 }
 
+static hc_status project_after_alloc(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const void* x, void* q_out,
+                                     const std::vector<AppendReq>& ar, const std::vector<int32_t>& tabs, void* stream);
+
 hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
                             const void* x, void* q_out, void* stream) {
   if (!pool) return fail(HC_E_INVALID, "pool is null");
@@ -1024,14 +1078,23 @@ hc_status hc_project_append(hc_pool* pool, int32_t n_req, const int64_t* req_ids
   if (pool->accounting) return fail(HC_E_UNSUPPORTED, "accounting-only pool has no device storage");
   if (!pool->L.has_q) return fail(HC_E_UNSUPPORTED, "pool was created without w_q");
   if (!x || !q_out) return fail(HC_E_INVALID, "x / q_out is null");
-  const int B = pool->cfg.block_size, d = pool->cfg.d_model;
   std::vector<int32_t> ones(n_req, 1);
   std::vector<AppendReq> ar;
   std::vector<int32_t> tabs;
   int32_t max_rows = 0;
+  AllocUndo undo;
   // k/v rows come from the projection GEMM itself: pass x to satisfy the row-source check
-  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, ones.data(), x, x, x, &ar, &tabs, &max_rows);
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, ones.data(), x, x, x, &ar, &tabs, &max_rows, &undo);
   if (st != HC_OK) return st;
+  st = project_after_alloc(pool, n_req, req_ids, x, q_out, ar, tabs, stream);
+  if (st != HC_OK) undo.rollback(pool);
+  return st;
+}
+
+static hc_status project_after_alloc(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const void* x, void* q_out,
+                                     const std::vector<AppendReq>& ar, const std::vector<int32_t>& tabs, void* stream) {
+  const int B = pool->cfg.block_size, d = pool->cfg.d_model;
+  hc_status st;
   // cache slot of each request's new token: KV rows are written by the GEMM epilogue,
   // hidden rows (x itself) by the append scatter
   std::vector<AppendReq> har;
@@ -1273,6 +1336,10 @@ size_t hc_prefill_workspace_size(const hc_pool* pool, int32_t n_req, const int32
   return n_req == 0 ? kAlign : prefill_plan(pool, n_req, lens).total;
 }
 
+static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* lens,
+                                     const void* x, float scale, void* y, void* workspace, const PrefillPlan& P,
+                                     const std::vector<AppendReq>& ar, const std::vector<int32_t>& tabs, void* stream);
+
 hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* modes,
                            const int32_t* lens, const void* x, float scale, void* y, void* workspace,
                            size_t ws_bytes, void* stream) {
@@ -1291,12 +1358,23 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
   }
   const PrefillPlan P = prefill_plan(pool, n_req, lens);
   if (ws_bytes < P.total) return fail(HC_E_WORKSPACE, "workspace smaller than hc_prefill_workspace_size()");
-  const int B = pool->cfg.block_size, d = pool->cfg.d_model, H = pool->cfg.n_heads, dh = pool->cfg.head_dim;
   std::vector<AppendReq> ar;
   std::vector<int32_t> tabs;
   int32_t max_rows = 0;
-  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, lens, x, x, x, &ar, &tabs, &max_rows);
+  AllocUndo undo;
+  DeviceGuard g(pool->cfg.device);   // before the staging slot: its event belongs to the pool's device
+  hc_status st = validate_and_allocate(pool, n_req, req_ids, modes, lens, x, x, x, &ar, &tabs, &max_rows, &undo);
   if (st != HC_OK) return st;
+  st = prefill_after_alloc(pool, n_req, req_ids, lens, x, scale, y, workspace, P, ar, tabs, stream);
+  if (st != HC_OK) undo.rollback(pool);
+  return st;
+}
+
+static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t* req_ids, const int32_t* lens,
+                                     const void* x, float scale, void* y, void* workspace, const PrefillPlan& P,
+                                     const std::vector<AppendReq>& ar, const std::vector<int32_t>& tabs, void* stream) {
+  const int B = pool->cfg.block_size, d = pool->cfg.d_model, H = pool->cfg.n_heads, dh = pool->cfg.head_dim;
+  hc_status st;
   // host descriptor: per-row cache targets (KV rows), request row offsets, query tiles
   const size_t desc_bytes = P.total - P.off_rowdst;
   Pinned* pin = pool->pinned(desc_bytes);
@@ -1344,7 +1422,6 @@ hc_status hc_prefill_layer(hc_pool* pool, int32_t n_req, const int64_t* req_ids,
     }
   }
   row0[n_req] = (int32_t)r;
-  DeviceGuard g(pool->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);
   cudaError_t err = cudaMemcpyAsync(ws + P.off_rowdst, hbase, desc_bytes, cudaMemcpyHostToDevice, s);

@@ -84,6 +84,7 @@ def _load() -> ctypes.CDLL:
         "hc_prefill_workspace_size": (SZ, [P, I32, pI32]),
         "hc_prefill_layer": (I32, [P, I32, pI64, pI32, pI32, VP, ctypes.c_float, VP, VP, SZ, VP]),
         "hc_pool_num_free": (I64, [P]),
+        "hc_units_needed": (I64, [ctypes.POINTER(PoolConfig), I32, I64]),
         "hc_request_info": (I32, [P, I64, pI32, pI64, pI64]),
         "hc_request_blocks": (I32, [P, I64, I32, pI32, I64, pI64]),
         "hc_last_launch_count": (I32, [P]),
@@ -136,6 +137,20 @@ def hc_pool_storage_bytes(cfg: PoolConfig) -> int:
     return int(lib.hc_pool_storage_bytes(ctypes.byref(cfg)))
 
 
+def hc_units_needed(cfg: PoolConfig, mode: int, n_tokens: int) -> int:
+    u = int(lib.hc_units_needed(ctypes.byref(cfg), int(mode), int(n_tokens)))
+    if u < 0:
+        raise HcError(HC_E_INVALID, lib.hc_last_error().decode())
+    return u
+
+
+def units_needed(d_model: int, n_heads: int, head_dim: int, block_size: int, mode: int, n_tokens: int,
+                 dtype: int = HC_BF16) -> int:
+    """Unit blocks of one request (the library's allocation rule; for sizing pools)."""
+    cfg = PoolConfig(d_model, n_heads, head_dim, block_size, 1, dtype, HC_FLAG_ACCOUNTING_ONLY)
+    return hc_units_needed(cfg, mode, n_tokens)
+
+
 def hc_pool_create(cfg: PoolConfig) -> ctypes.c_void_p:
     h = ctypes.c_void_p()
     _check(lib.hc_pool_create(ctypes.byref(cfg), ctypes.byref(h)))
@@ -181,8 +196,21 @@ def hc_layer_norm(h, n_rows, x, u, stream=None) -> None:
 
 def hc_merge_partials(outs, lses, out, lse=None, stream=None) -> None:
     """outs [P, rows, H*dh] (bf16/fp32), lses [P, rows, H] fp32 -> out [rows, H*dh], lse [rows, H]."""
+    if lses.dim() != 3 or outs.dim() != 3:
+        raise ValueError("merge: outs [P, rows, H*dh] and lses [P, rows, H] expected")
     n_parts, n_rows, n_heads = lses.shape
-    dt = HC_F32 if outs.dtype.is_floating_point and outs.element_size() == 4 else HC_BF16
+    if outs.dtype not in (torch.bfloat16, torch.float32) or out.dtype != outs.dtype:
+        raise ValueError(f"merge: outs/out must share dtype bf16 or fp32 (got {outs.dtype}, {out.dtype})")
+    if lses.dtype != torch.float32 or (lse is not None and lse.dtype != torch.float32):
+        raise ValueError("merge: lses / lse must be fp32")
+    hd = outs.shape[2]
+    if outs.shape[:2] != (n_parts, n_rows) or hd % n_heads != 0 or tuple(out.shape) != (n_rows, hd) or \
+            (lse is not None and tuple(lse.shape) != (n_rows, n_heads)):
+        raise ValueError("merge: shapes must be outs [P,rows,H*dh], lses [P,rows,H], out [rows,H*dh], lse [rows,H]")
+    for t in (outs, lses, out) + ((lse,) if lse is not None else ()):
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("merge: every tensor must be a contiguous CUDA tensor")
+    dt = HC_F32 if outs.dtype == torch.float32 else HC_BF16
     _check(lib.hc_merge_partials(int(n_parts), int(n_rows), int(n_heads), int(outs.shape[2] // n_heads), dt,
                                  _ptr(outs), _ptr(lses), _ptr(out), _ptr(lse), _stream(stream)))
 

@@ -118,3 +118,19 @@ def test_storage_bytes_and_workspace_queries(hc):
     assert p.workspace_size([5, 6]) > 0
     with pytest.raises(hc.HcError):
         p.workspace_size([5, 5])
+
+
+def test_units_needed_matches_the_pool_contract(hc):
+    """hc_units_needed (used to size every pool) follows SPEC S:58-66 / Fig. 6: KV takes
+    a K and a V unit per B tokens, hidden one unit; and it agrees with what hc_append allocates."""
+    from oracle.pool_oracle import blocks_needed
+    for B in (1, 4, 16, 64):
+        for n in (0, 1, B - 1, B, B + 1, 11, 14, 1000):
+            for mode in (0, 1):
+                assert hc.units_needed(32, 2, 16, B, mode, n) == blocks_needed(n, mode, B)
+    assert hc.units_needed(32, 2, 16, 4, 0, 11) == 6 and hc.units_needed(32, 2, 16, 4, 1, 14) == 4   # Fig. 6
+    p = _acct_pool(hc, 64, 4)
+    p.append([0, 1], [0, 1], [11, 14])
+    assert p.request_info(0)[2] == hc.units_needed(32, 2, 16, 4, 0, 11)
+    with pytest.raises(hc.HcError):
+        hc.units_needed(32, 2, 16, 4, 2, 5)

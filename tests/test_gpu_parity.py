@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 TOL_F32 = 1e-5
 TOL_BF16 = 1e-2
+TOL_LSE = 1e-2          # absolute, natural log (lse of scores ~N(0,1): |lse| ~ ln n)
 
 
 @pytest.fixture(scope="module")
@@ -256,7 +257,7 @@ def test_opt_shaped_sampled_parity(hc, cfg):
     heads = {i: [0, H // 2, H - 1] for i in idx if w.modes[i] == MODE_HIDDEN}
     err, lerr = T.compare(w, out[idx], lse[idx], idx, heads)
     assert err <= TOL_BF16, err
-    assert lerr <= 5e-2, lerr
+    assert lerr <= TOL_LSE, lerr
 
 
 def test_synth_bit_identical_on_device():
@@ -628,7 +629,7 @@ def test_absorbed_opt66b_sampled(hc):
     heads = {i: [0, w.shape.H // 2, w.shape.H - 1] for i in idx if w.modes[i] == MODE_HIDDEN}
     err, lerr = T.compare(w, out[idx], lse[idx], idx, heads)
     assert err <= TOL_BF16, err
-    assert lerr <= 5e-2, lerr
+    assert lerr <= TOL_LSE, lerr
 
 
 def test_absorbed_decode_layer(hc):
@@ -658,9 +659,9 @@ def test_absorbed_unsupported_configs(hc):
 
 # ------------------------------------------------------------------ pre-attention LayerNorm (f1 option, R15)
 LN_CASES = [("tiny-f32", None), ("bf16-512", (512, 4, 128, 16)), ("bf16-dh64", (512, 8, 64, 32))]
-# A layer with LayerNorm stores one more bf16 vector (u = LN(x)) on the way to q, k, v than
-# the plain layer; its composed bar is 1.5e-2 (DESIGN reading R16).  fp32 keeps 1e-5.
-TOL_BF16_LN_LAYER = 1.5e-2
+# A layer with LayerNorm stores u = LN(x) in the pool dtype before q, k, v (the hidden cache
+# holds it, R15); the oracle takes that stored vector, u = bf16(LN(x)) (reading R16), so the
+# bf16 bar stays north_star's 1e-2.  fp32 keeps 1e-5.
 
 
 def _ln_input(t):
@@ -675,15 +676,15 @@ def test_layer_norm_and_decode_layer_with_ln(hc, name, shape):
     if shape is None:
         w, tol = C.tiny(bias=True), TOL_F32
     else:
-        w, tol = _bf16_workload(*shape, n=[1, 40, 700, 129, 2], bias=True), TOL_BF16_LN_LAYER
+        w, tol = _bf16_workload(*shape, n=[1, 40, 700, 129, 2], bias=True), TOL_BF16
     dev = torch.device("cuda", 0)
     pool = T.make_layer_pool(w, ln=True)
-    ln = T.ln_params(w)
+    ln = T.ln_params(w, store=w.dtype)
     xs = [_ln_input(w.x_t(i)) for i in range(len(w.n))]
     x = torch.stack(xs).contiguous().to(dev)
     # hc_layer_norm alone: every element within the storage precision of the fp64 LN
     u = pool.layer_norm(x).float().cpu().numpy()
-    ref = O.layer_norm(torch.stack(xs), *ln)
+    ref = O.layer_norm(torch.stack(xs), *ln[:3])
     assert np.abs(u - ref).max() <= (1e-5 if shape is None else 2e-2) * max(1.0, np.abs(ref).max())
     T.fill(pool, T.prefix_workload(w))
     y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
@@ -701,10 +702,10 @@ def test_prefill_with_ln_then_decode(hc, name, shape):
     if shape is None:
         w, tol = C.tiny(bias=True), TOL_F32
     else:
-        w, tol = _bf16_workload(*shape, n=[65, 1, 300, 129], bias=True, seed=17), TOL_BF16_LN_LAYER
+        w, tol = _bf16_workload(*shape, n=[65, 1, 300, 129], bias=True, seed=17), TOL_BF16
     dev = torch.device("cuda", 0)
     pool = T.make_layer_pool(w, ln=True)
-    ln = T.ln_params(w)
+    ln = T.ln_params(w, store=w.dtype)
     X = [_ln_input(w.x(i)) for i in range(len(w.n))]
     yp = pool.prefill_layer(w.req_ids, w.modes, w.n, torch.cat(X).contiguous().to(dev), w.scale)
     yp = yp.float().cpu().numpy()
@@ -760,4 +761,111 @@ def test_attend_epilogue_rope_and_long_contexts(hc):
     T.fill(pool, w)
     out, lse = T.decode(pool, w, T.queries(w))
     err, lerr = T.compare(w, out, lse, range(len(w.n)), rope_theta=ROPE_THETA)
-    assert err <= TOL_BF16 and lerr <= 5e-2, (err, lerr)
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+
+
+# ------------------------------------------------------------------ where the kernels are most fragile
+def _opt66_workload(n, modes, seed, q_scale=1.0, bias=True):
+    shape = LayerShape("opt66b-shape", 9216, 72, 128)
+    return Workload(f"frag-{seed}", shape, 16, "bf16", seed, list(n), list(modes), list(range(len(n))), bias,
+                    q_scale=q_scale)
+
+
+@pytest.mark.parametrize("q_scale", [4.0, 32.0])
+def test_high_dynamic_range_softmax_on_the_fused_path(hc, q_scale):
+    """Eq. 2 with peaky scores: q x4 (SURVEY §8(d) "peaky" variant, scores ~N(0, 16)) and q x32
+    (scores ~N(0, 1024): softmax is an argmax, out -> v_argmax; exercises the online rescale and
+    the exp2 path in both the KV warps and the attend epilogue).  OPT-66B head shape, all heads."""
+    n = [1, 17, 600, 300, 33, 129, 2, 257]
+    modes = [MODE_HIDDEN, MODE_KV, MODE_KV, MODE_HIDDEN, MODE_HIDDEN, MODE_KV, MODE_KV, MODE_HIDDEN]
+    w = _opt66_workload(n, modes, seed=41 + int(q_scale), q_scale=q_scale)
+    pool, out, lse = _run(w)
+    assert pool.last_decode_path() == 1
+    assert np.isfinite(out).all() and np.isfinite(lse).all()
+    err, lerr = T.compare(w, out, lse, range(len(n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= TOL_LSE * max(1.0, float(np.abs(lse).max()) / 10), lerr
+
+
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg5:1/32"])
+def test_all_heads_of_the_longest_hidden_request_full_size(hc, cfg):
+    """Full-size batch in the bench's launch configuration; the oracle checks EVERY head of the
+    longest hidden request (all 36 GEMM n-tiles at d = 9216) and of one KV request."""
+    w = C.by_name(cfg)
+    pool = T.make_pool(w)
+    T.fill(pool, w)
+    out, lse = T.decode(pool, w, T.queries(w))
+    hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    idx = [max(hid, key=lambda i: w.n[i]), max(kv, key=lambda i: w.n[i])]
+    err, lerr = T.compare(w, out[idx], lse[idx], idx)
+    assert err <= TOL_BF16, err
+    assert lerr <= TOL_LSE, lerr
+
+
+def test_split_and_segment_boundary_lengths_at_d9216(hc):
+    """Context lengths on either side of every boundary the kernels have: the 16-token KV
+    chunk and block, the 32-token attend segment, the 512-token auto split (and 2x, 3x), for
+    both cache modes, in one fused batch at OPT-66B shape.  KV requests: all heads; hidden
+    requests: heads 0, 35, 71 (first, middle and last GEMM n-tiles)."""
+    lens = [15, 16, 17, 31, 32, 33, 511, 512, 513, 1023, 1024, 1025, 1535, 1536, 1537]
+    n = lens + lens
+    modes = [MODE_KV] * len(lens) + [MODE_HIDDEN] * len(lens)
+    w = _opt66_workload(n, modes, seed=77)
+    pool, out, lse = _run(w)
+    assert pool.last_decode_path() == 1
+    heads = {i: [0, 35, 71] for i in range(len(n)) if modes[i] == MODE_HIDDEN}
+    err, lerr = T.compare(w, out, lse, range(len(n)), heads)
+    assert err <= TOL_BF16, err
+    assert lerr <= TOL_LSE, lerr
+
+
+def test_failed_append_after_allocation_leaves_the_pool_unchanged(hc):
+    """hc.h: errors leave the pool unchanged.  With all 16 pinned staging slots held by captured
+    CUDA graphs, hc_append fails AFTER allocating (HC_E_CUDA): the request's length, block
+    table and the free count must be rolled back, and a retry after the graphs are gone
+    appends exactly once."""
+    w = _bf16_workload(512, 4, 128, 16, n=[40, 20], modes=[MODE_KV, MODE_HIDDEN])
+    pool = T.make_pool(w, num_blocks=64)
+    T.fill(pool, w)
+    q = T.queries(w)
+    ids = list(w.req_ids)
+    out = torch.empty_like(q)
+    ws = pool.workspace(ids)
+    graphs = []
+    torch.cuda.synchronize()
+    for _ in range(16):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            hc.hc_decode_attention(pool.handle, ids, q, w.scale, out, None, ws, torch.cuda.current_stream())
+        graphs.append(g)
+    before = (pool.request_info(ids[0]), pool.request_blocks(ids[0], 0), pool.num_free())
+    k = torch.zeros((9, 512), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(hc.HcError) as e:
+        pool.append([ids[0], 99], [MODE_KV, MODE_KV], [9, 9], k=torch.cat([k, k]), v=torch.cat([k, k]))
+    assert e.value.status == hc.HC_E_CUDA
+    assert (pool.request_info(ids[0]), pool.request_blocks(ids[0], 0), pool.num_free()) == before
+    with pytest.raises(hc.HcError):
+        pool.request_info(99)   # the request the failed call would have created does not exist
+
+
+def test_bench_token_range_split_matches_the_oracle(hc, tmp_path):
+    """bench.py --strong --split with 2 ranks (both on this GPU, gloo): a request longer than
+    total/world is split into block-aligned token ranges on both ranks, decoded, all-gathered
+    and merged by hc_merge_partials; the merged (out, lse) of every request (dumped by the
+    bench's HC_BENCH_DUMP hook) equals the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dump = str(tmp_path / "split.npz")
+    env = dict(os.environ, HC_BENCH_ONE_GPU="1", HC_BENCH_BACKEND="gloo", HC_BENCH_DUMP=dump)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", "tiny",
+                        "--strong", "--split", "--steps", "3", "--warmup", "3"], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = np.load(dump)
+    w = C.tiny()
+    assert d["parts"].max() >= 2   # at least one request really was split
+    err, lerr = T.compare(w, d["out"], d["lse"], range(len(w.n)))
+    assert err <= TOL_F32 and lerr <= 1e-5, (err, lerr)

@@ -102,3 +102,29 @@ def test_lpt_split_covers_every_token_once_and_balances():
         unsplit = [sum(costs[i] for i in p) for p in P.lpt(costs, G)]
         assert max(load) <= max(unsplit) + 1e-12
         assert max(load) / ideal < 1.15
+
+
+def _bench_dry(extra, world):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HC_BENCH_DRY="1", HC_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(world), "--steps", "3",
+                        "--warmup", "3"] + extra, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout   # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("extra,scaling,total", [([], "strong", 256), (["--weak"], "weak", 4 * 256),
+                                                 (["--no-gather"], "strong", 256)])
+def test_bench_spawns_ranks_and_runs_its_multi_rank_control_path(extra, scaling, total):
+    """`python bench.py --gpus 4` outside torchrun spawns 4 ranks itself (gloo here); cfg4 is
+    strong-scaled by default (256 requests in total), --weak gives each rank a
+    full batch; the output all-gather is on by default."""
+    d = _bench_dry(extra, 4)
+    assert d["n_gpus"] == 4 and d["scaling"] == scaling and d["config"]["n_req_total"] == total
+    assert d["dry"] is True and d["ms_per_step"] > 0
+    assert ("gloo all-gather" in d["config"]["output_gather"]) == ("--no-gather" not in extra)

@@ -371,3 +371,83 @@ def test_layer_with_ln_is_layer_on_normalised_input():
     # and the LN really changes the layer for this input
     Y3, _, _ = O.prefill_layer(X, Wq, Wkv, Wo, H, 0.25)
     assert np.abs(Y1 - Y3).max() > 1e-3
+
+
+# ---------------------------------------------------------------- the per-head sampling path
+def _sampling_cases():
+    from synth.configs import LayerShape, Workload
+    small = LayerShape("pin-small", 64, 4, 16)
+    n = [1, 17, 40, 33]
+    modes = [C.MODE_HIDDEN, C.MODE_KV, C.MODE_HIDDEN, C.MODE_HIDDEN]
+    return [
+        ("tiny-f32", C.tiny(bias=False), 0.0),
+        ("tiny-f32-bias", C.tiny(bias=True), 0.0),
+        ("small-bf16-bias", Workload("pin-bf16", small, 16, "bf16", 11, n, modes, [5, 6, 7, 8], True), 0.0),
+        ("small-bf16-rope", Workload("pin-rope", small, 16, "bf16", 12, n, modes, [1, 2, 3, 4], True), 10000.0),
+        ("small-bf16-peaky", Workload("pin-peaky", small, 16, "bf16", 13, n, modes, [1, 2, 3, 4], True,
+                                      q_scale=4.0), 0.0),
+    ]
+
+
+@pytest.mark.parametrize("name,w,theta", _sampling_cases(), ids=[c[0] for c in _sampling_cases()])
+def test_per_head_sampling_equals_decode_batch(name, w, theta):
+    """The per-head path every full-size GPU check goes through (tests/hc_testlib.oracle_request
+    -> hc_oracle.head_output, which rebuilds only head h's dh columns of K and V) equals the
+    Decimal-pinned decode_batch on every head, to 1e-13 — for all heads at once and for
+    scattered head subsets, with bias, RoPE and a peaky query (Eq. 1-3)."""
+    from tests import hc_testlib as T
+    d, H = w.shape.d, w.shape.H
+    W, b = w.w_kv(), w.b_kv()
+    for i in range(len(w.n)):
+        q = w.q(i).double().numpy()
+        if w.modes[i] == C.MODE_KV:
+            K, V = w.kv(i)
+            req = {"mode": 0, "q": q, "K": K, "V": V}
+        else:
+            req = {"mode": 1, "q": q, "X": w.x(i)}
+        ref, lref = O.decode_batch([req], W, H, w.scale, b, rope_theta=theta)
+        for heads in (None, [H - 1, 0], [1]):
+            o, l = T.oracle_request(w, i, heads, rope_theta=theta)
+            hs = list(range(H)) if heads is None else heads
+            dh = d // H
+            want = np.concatenate([ref[0, h * dh:(h + 1) * dh] for h in hs])
+            assert np.allclose(o, want, rtol=0, atol=1e-13 * max(1.0, np.abs(want).max())), (name, i, heads)
+            assert np.allclose(l, lref[0, hs], rtol=0, atol=1e-12), (name, i, heads)
+
+
+def test_head_output_against_decimal_bruteforce():
+    """head_output itself against 40-digit Decimal on one hidden request with a bias: k = W_K,h x
+    + b_K,h, v = W_V,h x + b_V,h, softmax with the given scale (catches swapped biases, a
+    wrong scale or a transposed W in the per-head path)."""
+    rs = np.random.default_rng(3)
+    n, d, dh = 7, 12, 4
+    X = rs.normal(size=(n, d))
+    WK, WV = rs.normal(size=(dh, d)), rs.normal(size=(dh, d))
+    bK, bV = rs.normal(size=dh), rs.normal(size=dh) + 3.0
+    q = rs.normal(size=dh)
+    scale = 0.37
+    o, l = O.head_output(q, X, WK, WV, scale, bK, bV)
+    Xd = [[Decimal(repr(float(v))) for v in row] for row in X]
+    Kd = _dec_recon(Xd, _dec_matrix(torch.tensor(WK)), [Decimal(repr(float(v))) for v in bK])
+    Vd = _dec_recon(Xd, _dec_matrix(torch.tensor(WV)), [Decimal(repr(float(v))) for v in bV])
+    o_ref, l_ref = _dec_attend(q, Kd, Vd, 1, scale)
+    assert np.allclose(o, [float(x) for x in o_ref], rtol=0, atol=1e-13)
+    assert abs(l - float(l_ref[0])) < 1e-13
+
+
+def test_layer_norm_store_rounding_is_one_bf16_rounding():
+    """R16: store="bf16" is exactly one round-to-nearest of the fp64 LN to bf16 — every value is
+    representable in bf16 (8 significant bits) and within half an ulp of the unrounded LN,
+    and rounding is idempotent."""
+    rs = np.random.default_rng(8)
+    X = rs.normal(size=(5, 64)) * 2.5 + 1.0
+    g, b = 1 + 0.1 * rs.normal(size=64), 0.02 * rs.normal(size=64)
+    U = O.layer_norm(X, g, b, 1e-5)
+    Us = O.layer_norm(X, g, b, 1e-5, store="bf16")
+    m, e = np.frexp(Us)
+    assert np.array_equal(m * 256, np.round(m * 256))          # 8-bit significand
+    ulp = np.ldexp(1.0, np.frexp(U)[1] - 8)
+    assert np.all(np.abs(Us - U) <= 0.5 * ulp + 1e-300)
+    again = torch.from_numpy(Us).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(again, Us)                             # idempotent
+    assert not np.array_equal(Us, U)                             # and it did round
