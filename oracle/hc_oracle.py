@@ -80,24 +80,32 @@ def reconstruct_kv(X, W_K, W_V, b_K=None, b_V=None):
     return K, V
 
 
-def attend(q, K, V, n_heads: int, scale: float, return_probs: bool = False):
+def attend(q, K, V, n_heads: int, scale: float, return_probs: bool = False, n_kv_heads: Optional[int] = None):
     """Eq. 2-3 for ONE decode query over n cached tokens, per head.
-    q: [d]; K, V: [n, d].  Returns out [d], lse [H] (and probabilities [H, n])."""
+    q: [d]; K, V: [n, Hk*dh].  Returns out [d], lse [H] (and probabilities [H, n]).
+    n_kv_heads = Hk < H: grouped-query attention (the LLaMA-3 / Yi models of §6.6, P:645;
+    DESIGN R18): query head h reads key/value head h // (H / Hk).  Hk = H (default) is Eq. 2-3
+    per head exactly as written."""
     q, K, V = _f64(q), _f64(K), _f64(V)
-    n, d = K.shape
+    n = K.shape[0]
+    d = q.shape[0]
     assert n >= 1, "n_i >= 1: the current token is part of the context (P:135)"
     dh = d // n_heads
+    Hk = n_heads if n_kv_heads is None else n_kv_heads
+    assert n_heads % Hk == 0 and K.shape[1] == Hk * dh and V.shape[1] == Hk * dh
+    G = n_heads // Hk
     out = np.empty(d)
     lse = np.empty(n_heads)
     probs = np.empty((n_heads, n))
     for h in range(n_heads):
         c = slice(h * dh, (h + 1) * dh)
-        s = scale * (K[:, c] @ q[c])          # s_j = q_h . k_{j,h} / sqrt(.)
+        ck = slice((h // G) * dh, (h // G + 1) * dh)   # this query head's key/value head
+        s = scale * (K[:, ck] @ q[c])         # s_j = q_h . k_{j,h} / sqrt(.)
         m = s.max()
         e = np.exp(s - m)
         l = e.sum()
         a = e / l                              # a_j, Eq. 2
-        out[c] = a @ V[:, c]                   # sum_j a_j v_{j,h}, Eq. 3 (pre-W_o)
+        out[c] = a @ V[:, ck]                  # sum_j a_j v_{j,h}, Eq. 3 (pre-W_o)
         lse[h] = m + np.log(l)
         probs[h] = a
     if return_probs:
@@ -106,29 +114,32 @@ def attend(q, K, V, n_heads: int, scale: float, return_probs: bool = False):
 
 
 def hidden_request_kv(X, W_KV, b_KV=None):
-    """Split the stacked [2d, d] W_KV = [W_K; W_V] (and [2d] bias) and rebuild K, V."""
+    """Split the stacked [2 Dk, d] W_KV = [W_K; W_V] (and [2 Dk] bias; Dk = d for multi-head,
+    Hk*dh under GQA) and rebuild K, V [n, Dk]."""
     W_KV = _f64(W_KV)
-    d = W_KV.shape[1]
+    dk = W_KV.shape[0] // 2
     bK = bV = None
     if b_KV is not None:
         b = _f64(b_KV)
-        bK, bV = b[:d], b[d:]
-    return reconstruct_kv(X, W_KV[:d], W_KV[d:], bK, bV)
+        bK, bV = b[:dk], b[dk:]
+    return reconstruct_kv(X, W_KV[:dk], W_KV[dk:], bK, bV)
 
 
-def decode_batch(requests: Sequence[dict], W_KV, n_heads: int, scale: float, b_KV=None, rope_theta: float = 0.0):
+def decode_batch(requests: Sequence[dict], W_KV, n_heads: int, scale: float, b_KV=None, rope_theta: float = 0.0,
+                 n_kv_heads: Optional[int] = None):
     """Hybrid-cache decode step for a batch.  Each request dict has 'q' [d] and either
-    'mode' 0 with 'K', 'V' [n, d] or 'mode' 1 with 'X' [n, d].  With RoPE, rebuilt keys are
-    rotated at their token positions 0..n-1 (cached KV-mode keys are stored rotated; q is
-    given rotated).  Returns out [n_req, d], lse [n_req, H]."""
+    'mode' 0 with 'K', 'V' [n, Dk] or 'mode' 1 with 'X' [n, d] (Dk = Hk*dh, = d unless GQA).
+    With RoPE, rebuilt keys are rotated at their token positions 0..n-1 (cached KV-mode keys
+    are stored rotated; q is given rotated).  Returns out [n_req, d], lse [n_req, H]."""
+    Hk = n_heads if n_kv_heads is None else n_kv_heads
     outs, lses = [], []
     for r in requests:
         if r["mode"] == 1:
             K, V = hidden_request_kv(r["X"], W_KV, b_KV)
-            K = rope(K, np.arange(K.shape[0]), rope_theta, n_heads)
+            K = rope(K, np.arange(K.shape[0]), rope_theta, Hk)
         else:
             K, V = r["K"], r["V"]
-        o, l = attend(r["q"], K, V, n_heads, scale)
+        o, l = attend(r["q"], K, V, n_heads, scale, n_kv_heads=Hk)
         outs.append(o)
         lses.append(l)
     return np.stack(outs), np.stack(lses)

@@ -38,12 +38,25 @@ class LayerShape:
     d: int
     H: int
     dh: int
+    Hk: int = 0    # key/value heads (GQA, the §6.6 models); 0 = H (multi-head)
+
+    @property
+    def n_kv(self) -> int:
+        return self.Hk or self.H
+
+    @property
+    def dk(self) -> int:
+        """Width of one K (or V) row: Hk * dh (= d for multi-head attention)."""
+        return self.n_kv * self.dh
 
 
 TINY = LayerShape("tiny", 32, 2, 16)
 OPT13B = LayerShape("OPT-13B", 5120, 40, 128)
 OPT30B = LayerShape("OPT-30B", 7168, 56, 128)
 OPT66B = LayerShape("OPT-66B", 9216, 72, 128)
+# §6.6 long-context GQA models (P:645): 32 query heads over 8 (LLaMA-3-8B) / 4 (Yi-6B) K/V heads
+LLAMA3_8B = LayerShape("LLaMA3-8B", 4096, 32, 128, 8)
+YI_6B = LayerShape("Yi-6B", 4096, 32, 128, 4)
 
 
 @dataclass
@@ -86,8 +99,8 @@ class Workload:
                                  self.q_scale, self.torch_dtype, device)
 
     def kv(self, i: int, device="cpu", rows=None):
-        """(K, V) of a KV-mode request, [n_i, d] each; `rows=(a,b)` gives a row range."""
-        d = self.shape.d
+        """(K, V) of a KV-mode request, [n_i, Dk] each (Dk = Hk*dh); `rows=(a,b)` gives a row range."""
+        d = self.shape.dk
         a, b = rows if rows is not None else (0, self.n[i])
         K = rng.normal_tensor(self.seed, rng.STREAM_K, self.req_ids[i], [b - a, d], 1.0,
                               self.torch_dtype, device, offset=a * d)
@@ -103,9 +116,9 @@ class Workload:
                                  self.torch_dtype, device, offset=a * d)
 
     def w_kv(self, device="cpu", rows=None) -> torch.Tensor:
-        """W_KV = [W_K; W_V], [2d, d] row-major, rows = output features (Eq. 1: k = W_K x)."""
+        """W_KV = [W_K; W_V], [2 Dk, d] row-major, rows = output features (Eq. 1: k = W_K x)."""
         d = self.shape.d
-        a, b = rows if rows is not None else (0, 2 * d)
+        a, b = rows if rows is not None else (0, 2 * self.shape.dk)
         out = torch.empty((b - a, d), dtype=self.torch_dtype, device=device)
         step = max(1, (1 << 25) // d)
         for r in range(a, b, step):
@@ -151,10 +164,10 @@ class Workload:
                                  self.torch_dtype, device)
 
     def b_kv(self, device="cpu") -> Optional[torch.Tensor]:
-        """Optional bias [2d] (fp32), None when disabled (Eq. 1 has no bias; SURVEY §8(c) #4)."""
+        """Optional bias [2 Dk] (fp32), None when disabled (Eq. 1 has no bias; SURVEY §8(c) #4)."""
         if not self.bias:
             return None
-        return rng.normal_tensor(self.seed, rng.STREAM_B, 0, [2 * self.shape.d], 0.02,
+        return rng.normal_tensor(self.seed, rng.STREAM_B, 0, [2 * self.shape.dk], 0.02,
                                  torch.float32, device)
 
 
@@ -239,6 +252,18 @@ def cfg5(h: float, block_size: int = 16, n_req: int = 256, seed: int = 3) -> Wor
                     list(range(n_req)), note=f"OPT-66B sweep, hidden fraction {h}")
 
 
+def gqa(shape: LayerShape = LLAMA3_8B, block_size: int = 16, n_req: int = 256, seed: int = 6) -> Workload:
+    """f4 (i): a §6.6 GQA model's layer (LLaMA-3-8B: 32 query / 8 K-V heads), cfg4's
+    long-context recipe, 50% hidden.  Hidden tokens cost d = 4096 values, KV tokens 2*Hk*dh =
+    2048: under GQA the hidden cache is the LARGER one (DESIGN R18)."""
+    rs = np.random.default_rng(seed)
+    n = long_lognormal(n_req, rs)
+    tag = "llama3-8b" if shape is LLAMA3_8B else shape.name.lower()
+    return Workload(f"gqa-{tag}", shape, block_size, "bf16", seed, n, _half_hidden(n_req, rs),
+                    list(range(n_req)), note=f"{shape.name} layer (GQA {shape.H}/{shape.n_kv}), batch {n_req}, "
+                                             "long contexts, 50% hidden")
+
+
 def by_name(name: str) -> Workload:
     name = name.lower()
     if name == "tiny":
@@ -252,6 +277,10 @@ def by_name(name: str) -> Workload:
     if name.startswith("cfg5:"):
         from fractions import Fraction
         return cfg5(float(Fraction(name.split(":", 1)[1])))   # "cfg5:1/32" or "cfg5:0.03125"
+    if name in ("gqa", "llama3-8b", "cfg6"):
+        return gqa(LLAMA3_8B)
+    if name in ("yi-6b",):
+        return gqa(YI_6B)
     raise KeyError(name)
 
 

@@ -377,6 +377,7 @@ def test_layer_with_ln_is_layer_on_normalised_input():
 def _sampling_cases():
     from synth.configs import LayerShape, Workload
     small = LayerShape("pin-small", 64, 4, 16)
+    gqa = LayerShape("pin-gqa", 64, 8, 8, 2)      # 8 query heads over 2 K/V heads
     n = [1, 17, 40, 33]
     modes = [C.MODE_HIDDEN, C.MODE_KV, C.MODE_HIDDEN, C.MODE_HIDDEN]
     return [
@@ -386,6 +387,8 @@ def _sampling_cases():
         ("small-bf16-rope", Workload("pin-rope", small, 16, "bf16", 12, n, modes, [1, 2, 3, 4], True), 10000.0),
         ("small-bf16-peaky", Workload("pin-peaky", small, 16, "bf16", 13, n, modes, [1, 2, 3, 4], True,
                                       q_scale=4.0), 0.0),
+        ("small-gqa-bias", Workload("pin-gqa", gqa, 16, "bf16", 14, n, modes, [1, 2, 3, 4], True), 0.0),
+        ("small-gqa-rope", Workload("pin-gqa-rope", gqa, 16, "bf16", 15, n, modes, [1, 2, 3, 4], True), 500000.0),
     ]
 
 
@@ -405,7 +408,7 @@ def test_per_head_sampling_equals_decode_batch(name, w, theta):
             req = {"mode": 0, "q": q, "K": K, "V": V}
         else:
             req = {"mode": 1, "q": q, "X": w.x(i)}
-        ref, lref = O.decode_batch([req], W, H, w.scale, b, rope_theta=theta)
+        ref, lref = O.decode_batch([req], W, H, w.scale, b, rope_theta=theta, n_kv_heads=w.shape.n_kv)
         for heads in (None, [H - 1, 0], [1]):
             o, l = T.oracle_request(w, i, heads, rope_theta=theta)
             hs = list(range(H)) if heads is None else heads
@@ -451,3 +454,85 @@ def test_layer_norm_store_rounding_is_one_bf16_rounding():
     again = torch.from_numpy(Us).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(again, Us)                             # idempotent
     assert not np.array_equal(Us, U)                             # and it did round
+
+
+
+# ---------------------------------------------------------------- grouped-query attention (f4 (i), R18)
+def _gqa_tiny(seed=21, bias=True):
+    from synth.configs import LayerShape, Workload
+    sh = LayerShape("pin-gqa-tiny", 32, 4, 8, 2)
+    return Workload("gqa-tiny", sh, 4, "f32", seed, [9, 1, 6, 12], [C.MODE_KV, C.MODE_HIDDEN, C.MODE_HIDDEN,
+                                                                   C.MODE_KV], [0, 1, 2, 3], bias)
+
+
+def test_gqa_vs_decimal_bruteforce():
+    """GQA decode (query head h reads K/V head h // G) against a 40-digit Decimal brute force
+    that writes the head mapping out by hand: tiny shape, 4 query heads over 2 K/V heads,
+    both cache modes, with bias."""
+    w = _gqa_tiny()
+    d, H, dh, Hk = w.shape.d, w.shape.H, w.shape.dh, w.shape.n_kv
+    dk, G = Hk * dh, H // Hk
+    W, b = w.w_kv(), w.b_kv()
+    Wd = _dec_matrix(W.double())
+    bd = [Decimal(repr(float(v))) for v in b.tolist()]
+    getcontext().prec = 40
+    for i in range(4):
+        q = w.q(i).double().numpy()
+        if w.modes[i] == C.MODE_KV:
+            K, V = w.kv(i)
+            Kd, Vd = _dec_matrix(K.double()), _dec_matrix(V.double())
+            req = {"mode": 0, "q": q, "K": K, "V": V}
+        else:
+            Xd = _dec_matrix(w.x(i).double())
+            Kd, Vd = _dec_recon(Xd, Wd[:dk], bd[:dk]), _dec_recon(Xd, Wd[dk:], bd[dk:])
+            req = {"mode": 1, "q": q, "X": w.x(i)}
+        out, lse = O.decode_batch([req], W, H, w.scale, b, n_kv_heads=Hk)
+        sc = Decimal(repr(w.scale))
+        for h in range(H):
+            hk = h // G
+            s = [sc * sum(Decimal(repr(float(q[h * dh + c]))) * Kd[j][hk * dh + c] for c in range(dh))
+                 for j in range(len(Kd))]
+            m = max(s)
+            e = [(x - m).exp() for x in s]
+            z = sum(e)
+            for c in range(dh):
+                ref = float(sum(e[j] / z * Vd[j][hk * dh + c] for j in range(len(Kd))))
+                assert abs(out[0, h * dh + c] - ref) <= 1e-13 * max(1.0, abs(ref))
+            assert abs(lse[0, h] - float(m + z.ln())) <= 1e-13
+
+
+def test_gqa_equals_multihead_with_repeated_kv_heads():
+    """Closed form: GQA over Hk heads = multi-head attention over K/V whose heads are repeated
+    G times (repeat_interleave over heads), for KV and hidden requests (W_K, W_V rows repeated)."""
+    rs = np.random.default_rng(22)
+    n, H, Hk, dh = 11, 6, 2, 4
+    d, dk, G = H * dh, Hk * dh, H // Hk
+    q, K, V = rs.normal(size=d), rs.normal(size=(n, dk)), rs.normal(size=(n, dk))
+    rep = lambda M: np.repeat(M.reshape(M.shape[0], Hk, dh), G, axis=1).reshape(M.shape[0], d)
+    o1, l1 = O.attend(q, K, V, H, 0.3, n_kv_heads=Hk)
+    o2, l2 = O.attend(q, rep(K), rep(V), H, 0.3)
+    assert np.allclose(o1, o2, rtol=0, atol=1e-14) and np.allclose(l1, l2, rtol=0, atol=1e-14)
+    X, W, bb = rs.normal(size=(n, d)), rs.normal(size=(2 * dk, d)), rs.normal(size=2 * dk)
+    Wrep = np.concatenate([rep(W[:dk].T).T, rep(W[dk:].T).T])
+    brep = np.concatenate([rep(bb[None, :dk])[0], rep(bb[None, dk:])[0]])
+    a1, _ = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.3, bb, n_kv_heads=Hk)
+    a2, _ = O.decode_batch([{"mode": 1, "q": q, "X": X}], Wrep, H, 0.3, brep)
+    assert np.allclose(a1, a2, rtol=0, atol=1e-12)
+
+
+def test_gqa_matches_torch_sdpa_enable_gqa():
+    """Library routine: torch scaled_dot_product_attention(enable_gqa=True) in float64 with one
+    query per request; and the hybrid equivalence hidden(X) = KV(X W_K^T + b_K, X W_V^T + b_V)."""
+    rs = np.random.default_rng(23)
+    n, H, Hk, dh = 13, 8, 2, 16
+    d, dk = H * dh, Hk * dh
+    q, X = rs.normal(size=d), rs.normal(size=(n, d))
+    W, bb = rs.normal(size=(2 * dk, d)) / np.sqrt(d), rs.normal(size=2 * dk) * 0.1
+    K, V = X @ W[:dk].T + bb[:dk], X @ W[dk:].T + bb[dk:]
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q).view(1, H, 1, dh), torch.from_numpy(K).view(n, Hk, dh).transpose(0, 1)[None],
+        torch.from_numpy(V).view(n, Hk, dh).transpose(0, 1)[None], scale=0.25, enable_gqa=True)
+    o_kv, _ = O.decode_batch([{"mode": 0, "q": q, "K": K, "V": V}], W, H, 0.25, bb, n_kv_heads=Hk)
+    o_h, _ = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.25, bb, n_kv_heads=Hk)
+    assert np.allclose(o_kv[0], ref.reshape(-1).numpy(), rtol=0, atol=1e-12)
+    assert np.allclose(o_h[0], o_kv[0], rtol=0, atol=1e-12)
