@@ -50,13 +50,14 @@ def workload_from(name: str):
 
 
 def algorithmic(w):
-    """bytes and FLOPs the method must move / compute (bf16: s = 2)."""
-    d, s = w.shape.d, w.elem_bytes
+    """bytes and FLOPs the method must move / compute (bf16: s = 2).  dk = Hk*dh
+    is the K (or V) row width: d for multi-head, smaller under GQA (R18)."""
+    d, s, dk = w.shape.d, w.elem_bytes, w.shape.dk
     kv_tok = w.n_tokens(0)
     hid_tok = w.n_tokens(1)
     n_req = len(w.n)
-    bytes_ = kv_tok * 2 * d * s + hid_tok * d * s + (2 * d * d * s + 2 * d * 4 if hid_tok else 0) + 2 * n_req * d * s
-    flops = 4 * d * d * hid_tok
+    bytes_ = kv_tok * 2 * dk * s + hid_tok * d * s + (2 * dk * d * s + 2 * dk * 4 if hid_tok else 0) + 2 * n_req * d * s
+    flops = 4 * d * dk * hid_tok
     return bytes_, flops, kv_tok, hid_tok
 
 
@@ -728,8 +729,8 @@ def main():
             "note": "GEMM + split-K attention warps in one kernel; FLOP/s counts the GEMM only" if fused else ""},
         "attention": ({"ms": None, "note": "n/a: the attention runs inside fused_step_kernel"} if fused else
                       {"ms": t_att, "bound": "hbm", "unit": "GB/s",
-                       "bytes_per_launch": (kv_tok + hid_tok) * 2 * d * s,
-                       "achieved": ((kv_tok + hid_tok) * 2 * d * s / (t_att / 1e3) / 1e9) if t_att > 0 else None}),
+                       "bytes_per_launch": (kv_tok + hid_tok) * 2 * w.shape.dk * s,
+                       "achieved": ((kv_tok + hid_tok) * 2 * w.shape.dk * s / (t_att / 1e3) / 1e9) if t_att > 0 else None}),
         "combine": {"ms": t_comb},
         "descriptor_upload": {"ms": t_up},
     }
@@ -770,6 +771,9 @@ def main():
         "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
         "config": {"workload": w.name, "shape": w.shape.name, "d": d, "heads": w.shape.H, "head_dim": w.shape.dh,
+                   "kv_heads": w.shape.n_kv,
+                   "cache_bytes_per_token": {"kv": 2 * w.shape.dk * s, "hidden": d * s,
+                                             "hidden_over_kv": d / (2 * w.shape.dk)},
                    "block_size": w.block_size, "n_req_per_gpu": n_req, "kv_tokens": kv_tok, "hidden_tokens": hid_tok,
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
                    "output_gather": gather.describe() if gather else "none",

@@ -75,10 +75,11 @@ typedef struct {
   int32_t flags;         /* HC_FLAG_* */
   void* storage;         /* device buffer of hc_pool_storage_bytes() bytes, borrowed */
   size_t storage_bytes;
-  const void* w_kv;      /* device [2d, d] row-major, rows = W_K (d rows) then W_V; k = W_K x.
+  const void* w_kv;      /* device [2 Dk, d] row-major, rows = W_K (Dk rows) then W_V; k = W_K x;
+                            Dk = n_kv_heads * head_dim (= d for multi-head attention).
                             Copied once at create into head-interleaved order inside storage;
                             may be freed after create. */
-  const float* b_kv;     /* nullable device [2d] fp32 bias (b_K then b_V); copied at create */
+  const float* b_kv;     /* nullable device [2 Dk] fp32 bias (b_K then b_V); copied at create */
   int32_t device;        /* CUDA device ordinal the storage lives on */
   int32_t split_tokens;  /* split-K chunk in tokens (multiple of B); 0 = automatic */
   /* Optional rest of the attention module (NEXT row f1; all nullable, copied at create):
@@ -105,6 +106,14 @@ typedef struct {
   const float* ln_gamma;
   const float* ln_beta;
   float ln_eps;
+  /* Grouped-query attention (NEXT row f4 (i): the LLaMA-3 / Yi models of §6.6; DESIGN
+   * R18): n_kv_heads = Hk key/value heads, query head h attends K/V head h / (H / Hk).
+   * 0 or n_heads = multi-head (Eq. 2-3 per head as written).  With Hk < H a KV-mode token
+   * holds 2 Dk = 2 Hk dh values (< d): one unit block then stores the K and the V rows of
+   * Bkv = B d / (2 Dk) tokens ([Hk][Bkv][dh] K, then the same for V), so KV takes ONE unit
+   * per Bkv tokens while hidden takes one per B — under GQA the hidden cache is the larger
+   * one.  Requires H % Hk == 0 and d % (2 Dk) == 0; not with HC_FLAG_ABSORB_HIDDEN. */
+  int32_t n_kv_heads;
 } hc_pool_config;
 
 /* Bytes of device storage a pool with this config needs: the unit blocks, the
@@ -114,7 +123,7 @@ size_t hc_pool_storage_bytes(const hc_pool_config* cfg);
 
 /* Unit blocks a request of n_tokens tokens occupies in `mode` under this config (the
  * allocation rule of hc_append: KV takes a K and a V unit per B tokens, hidden one unit per
- * B tokens).  For sizing pools.  Returns -1 for an invalid config/mode or
+ * B tokens; under GQA KV takes one unit per Bkv tokens, see n_kv_heads).  For sizing pools.  Returns -1 for an invalid config/mode or
  * n_tokens < 0.  Host only. */
 int64_t hc_units_needed(const hc_pool_config* cfg, int32_t mode, int64_t n_tokens);
 
@@ -132,7 +141,7 @@ void hc_pool_destroy(hc_pool* pool);
  * For each of the n_req DISTINCT requests, n_tokens[i] >= 0 new tokens are appended at
  * the end of its cache in mode modes[i] (a new id is created with that mode).  Rows are
  * device buffers packed in request order: `k`, `v` hold [sum over KV-mode requests of
- * n_tokens, d]; `x` holds [sum over hidden-mode requests of n_tokens, d] (token-major,
+ * n_tokens, Dk]; `x` holds [sum over hidden-mode requests of n_tokens, d] (token-major,
  * row-major).  Either of k/v or x may be NULL if no request of that mode is present.
  * Block allocation: SPEC memory-pool contract — unit blocks, KV takes a K and a V block
  * per B tokens, hidden one, new blocks only when the last is full,
@@ -280,7 +289,8 @@ int64_t hc_pool_num_free(const hc_pool* pool);
 /* mode (hc_mode), cached tokens and unit blocks of a request; HC_E_UNKNOWN_REQ if absent */
 hc_status hc_request_info(const hc_pool* pool, int64_t req_id, int32_t* mode, int64_t* n_tokens,
                           int64_t* n_units);
-/* block ids of a request's cache map: kind 0 = K (or X for hidden), 1 = V.
+/* block ids of a request's cache map: kind 0 = K (or X for hidden; under GQA the
+ * unit holding K and V), 1 = V (empty under GQA).
  * Writes min(count, cap) ids to out; *count = list length. */
 hc_status hc_request_blocks(const hc_pool* pool, int64_t req_id, int32_t kind, int32_t* out,
                             int64_t cap, int64_t* count);

@@ -188,22 +188,24 @@ def attention_layer(x_t, cache: dict, W_Q, W_KV, W_O, n_heads: int, scale: float
         x_t = layer_norm(x_t[None, :], *ln)[0]
     W_KV = _f64(W_KV)
     d = x_t.shape[0]
+    dk = W_KV.shape[0] // 2                       # K/V row width (d, or Hk*dh under GQA, R18)
+    Hk = n_heads * dk // d
     q = W_Q @ x_t + (0.0 if b_Q is None else _f64(b_Q))
     if cache["mode"] == 1:
         X = np.concatenate([_f64(cache["X"]).reshape(-1, d), x_t[None, :]])
         pos = X.shape[0] - 1
         K, V = hidden_request_kv(X, W_KV, b_KV)
-        K = rope(K, np.arange(X.shape[0]), rope_theta, n_heads)
+        K = rope(K, np.arange(X.shape[0]), rope_theta, Hk)
         ctx = {"mode": 1, "X": X}
     else:
         kv = W_KV @ x_t + (0.0 if b_KV is None else _f64(b_KV))
-        pos = _f64(cache["K"]).reshape(-1, d).shape[0]
-        kv[:d] = rope(kv[None, :d], [pos], rope_theta, n_heads)[0]
-        K = np.concatenate([_f64(cache["K"]).reshape(-1, d), kv[None, :d]])
-        V = np.concatenate([_f64(cache["V"]).reshape(-1, d), kv[None, d:]])
+        pos = _f64(cache["K"]).reshape(-1, dk).shape[0]
+        kv[:dk] = rope(kv[None, :dk], [pos], rope_theta, Hk)[0]
+        K = np.concatenate([_f64(cache["K"]).reshape(-1, dk), kv[None, :dk]])
+        V = np.concatenate([_f64(cache["V"]).reshape(-1, dk), kv[None, dk:]])
         ctx = {"mode": 0, "K": K, "V": V}
     q = rope(q[None, :], [pos], rope_theta, n_heads)[0]
-    o, lse = attend(q, K, V, n_heads, scale)
+    o, lse = attend(q, K, V, n_heads, scale, n_kv_heads=Hk)
     y = W_O @ o + (0.0 if b_O is None else _f64(b_O))
     return y, q, lse, ctx
 
@@ -221,11 +223,12 @@ def prefill_layer(X, W_Q, W_KV, W_O, n_heads: int, scale: float, b_Q=None, b_KV=
     L, d = X.shape
     Q = X @ W_Q.T + (0.0 if b_Q is None else _f64(b_Q)[None, :])
     K, V = hidden_request_kv(X, W_KV, b_KV)
+    Hk = n_heads * K.shape[1] // d                # GQA (R18): K/V heads
     Q = rope(Q, np.arange(L), rope_theta, n_heads)
-    K = rope(K, np.arange(L), rope_theta, n_heads)
+    K = rope(K, np.arange(L), rope_theta, Hk)
     Y = np.empty((L, d))
     for i in range(L):
-        o, _ = attend(Q[i], K[: i + 1], V[: i + 1], n_heads, scale)
+        o, _ = attend(Q[i], K[: i + 1], V[: i + 1], n_heads, scale, n_kv_heads=Hk)
         Y[i] = W_O @ o + (0.0 if b_O is None else _f64(b_O))
     return Y, K, V
 

@@ -57,14 +57,17 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(const AttnParams p) {
     const ReqDesc rq = p.reqs[sp.req];
     for (int c = lane; c < DH; c += 32) q_s[c] = ld_f(qg + (size_t)sp.req * d + h * DH + c) * p.scale_log2;
     __syncwarp();
+    const int hk = h / p.G;   // this query head's K/V head (GQA, R18)
     auto row_ptr = [&](int t, bool is_v) -> const T* {
+      if (rq.mode == 0) {
+        const int tok = sp.lb0 * p.Bkv + t;
+        const int lb = tok / p.Bkv, row = tok - lb * p.Bkv;
+        const int blk = p.tables[rq.tab_off + 2 * lb + (is_v ? 1 : 0)];
+        return pool + (size_t)blk * B * d + (is_v ? p.v_off : 0) + (size_t)hk * p.Bkv * DH + (size_t)row * DH;
+      }
       const int tok = sp.lb0 * B + t;
       const int lb = tok / B, row = tok - lb * B;
-      if (rq.mode == 0) {
-        const int blk = p.tables[rq.tab_off + 2 * lb + (is_v ? 1 : 0)];
-        return pool + (size_t)blk * B * d + (size_t)h * B * DH + (size_t)row * DH;
-      }
-      return (is_v ? scr_v : scr_k) + (((size_t)(rq.scratch_blk0 + lb) * H + h) * B + row) * DH;
+      return (is_v ? scr_v : scr_k) + (((size_t)(rq.scratch_blk0 + lb) * p.Hk + hk) * B + row) * DH;
     };
     float m = -INFINITY, l = 0.f, acc[MAXC];
 #pragma unroll

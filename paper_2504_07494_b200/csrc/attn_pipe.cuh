@@ -128,7 +128,8 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
 
   const int H = p.H, B = p.B, d = p.d;
   const size_t blk_elems = (size_t)B * d;          // one unit block
-  const size_t head_elems = (size_t)B * DH;        // one head of one block
+  const size_t head_elems = (size_t)B * DH;        // one head of one hidden/scratch block
+  const size_t kv_head_elems = (size_t)p.Bkv * DH; // one head of one KV logical block
   const __nv_bfloat16* pool = static_cast<const __nv_bfloat16*>(p.pool);
   const __nv_bfloat16* scr_k = static_cast<const __nv_bfloat16*>(p.scr_k);
   const __nv_bfloat16* scr_v = static_cast<const __nv_bfloat16*>(p.scr_v);
@@ -163,8 +164,10 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
   // issue the next chunk of the producer stream into `stage`; false when no work is left
   auto produce = [&](int stage) -> bool {
     if (ptask >= p.n_tasks) return false;
-    const int tok = psp.lb0 * B + pchunk * TOK;   // token index within the request
-    const int lb = tok / B, row = tok - lb * B;
+    const int Bm = prq.mode == 0 ? p.Bkv : B;     // tokens per logical block of this mode
+    const int tok = psp.lb0 * Bm + pchunk * TOK;  // token index within the request
+    const int lb = tok / Bm, row = tok - lb * Bm;
+    const int hk = phead / p.G;                   // K/V head of this query head (GQA, R18)
     const int rem = psp.ntok - pchunk * TOK;
     const int nvalid = rem < TOK ? rem : TOK;
     const bool first = pchunk == 0, last = pchunk == pnch - 1;
@@ -173,10 +176,10 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       if (prq.mode == 0) {
         const int kb = p.tables[prq.tab_off + 2 * lb];
         const int vb = p.tables[prq.tab_off + 2 * lb + 1];
-        ksrc = pool + (size_t)kb * blk_elems + phead * head_elems + (size_t)row * DH;
-        vsrc = pool + (size_t)vb * blk_elems + phead * head_elems + (size_t)row * DH;
+        ksrc = pool + (size_t)kb * blk_elems + hk * kv_head_elems + (size_t)row * DH;
+        vsrc = pool + (size_t)vb * blk_elems + p.v_off + hk * kv_head_elems + (size_t)row * DH;
       } else {
-        const size_t off = ((size_t)(prq.scratch_blk0 + lb) * H + phead) * head_elems + (size_t)row * DH;
+        const size_t off = ((size_t)(prq.scratch_blk0 + lb) * p.Hk + hk) * head_elems + (size_t)row * DH;
         ksrc = scr_k + off;
         vsrc = scr_v + off;
       }

@@ -37,7 +37,7 @@ struct FusedTaskMap {
       head = t - ks * H;
       return;
     }
-    const int hpt = p->gemm_tile_n / (2 * p->dh);     // heads per GEMM n-tile
+    const int hpt = p->gemm_tile_n / (2 * p->dh) * p->G;   // query heads per GEMM n-tile
     const int u = t - p->n_kv_tasks;
     const int per_nt = p->n_hid_splits * hpt;
     const int nt = u / per_nt;
@@ -53,7 +53,7 @@ struct FusedTaskMap {
       const int g0 = rq.scratch_blk0 + sp.lb0;
       const int nblk = (sp.ntok + B - 1) / B;
       const int mt0 = (g0 * B) / p->gemm_tile_m, mt1 = ((g0 + nblk) * B - 1) / p->gemm_tile_m;
-      const int nt = head * 2 * p->dh / p->gemm_tile_n;
+      const int nt = (head / p->G) * 2 * p->dh / p->gemm_tile_n;
       const long long t0 = clock64();
       for (int mt = mt0; mt <= mt1; ++mt) {
         const int32_t* f = p->tile_done + mt * p->gemm_n_tiles + nt;
@@ -130,8 +130,8 @@ cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx
 
 }  // namespace
 
-bool fused_supported(int d, int H, int dh, int B) {
-  return dh == 128 && d == H * dh && d % 64 == 0 && (2 * d) % (256 * kNsub) == 0 && B % 16 == 0 &&
+bool fused_supported(int d, int dk, int dh, int B) {
+  return dh == 128 && dk % dh == 0 && d % 64 == 0 && (2 * dk) % (256 * kNsub) == 0 && B % 16 == 0 &&
          B >= 16 && (B <= 128 || B % 256 == 0) && (B & (B - 1)) == 0;
 }
 int fused_tile_m() { return pg::P_BM; }
@@ -146,9 +146,11 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.M = rp.n_hblocks * rp.B;
   a.rows_per_box = (rp.B < 128 && !t.diag_box) ? rp.B : 128;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
-  a.n_tiles = 2 * rp.d / PC::TILE_N;
+  a.n_tiles = 2 * rp.dk / PC::TILE_N;
   a.k_iters = rp.d / pg::BK;
-  a.H = rp.H;
+  a.H = rp.Hk;
+  a.grp = rp.H / rp.Hk;
+  a.dk = rp.dk;
   a.dh = rp.dh;
   a.d = rp.d;
   a.scr_k = static_cast<__nv_bfloat16*>(rp.scr_k);
@@ -193,8 +195,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // e.g. 1/64 of OPT-66B requests hidden), a 2-stage GEMM ring and 8 attention warps
   // stream KV faster (-4% at 1/64); from 1/32 up the 2-stage ring starves the tensor cores
   // (+15..+25%), so the default stays <3,5,2>.
-  const double t_gemm = 4.0 * rp.d * (double)rp.d * a.M / 1.3e15;
-  const double t_kv = (double)rp.kv_tokens * 4.0 * rp.d / 6.5e12;
+  const double t_gemm = 4.0 * rp.d * (double)rp.dk * a.M / 1.3e15;
+  const double t_kv = (double)rp.kv_tokens * 4.0 * rp.dk / 6.5e12;
   const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 282 : 352);
   if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
   if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);

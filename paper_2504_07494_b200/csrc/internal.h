@@ -68,7 +68,12 @@ struct AttnParams {
   int32_t n_splits_all;   // splits in the call (partial index = head * n_splits_all + split)
   int32_t* task_counter;  // zero on entry (part of the uploaded descriptor)
   int32_t n_tasks;        // n_splits * H; task = split * H + head
-  int32_t H, dh, B, d;
+  int32_t H, dh, B, d;    // B: hidden block (and scratch) tokens
+  // KV-mode layout (GQA, R18): query head h reads K/V head h / G of Hk; a KV logical block
+  // holds Bkv tokens, K at unit(tab K) + hk*Bkv*dh, V at unit(tab V) + v_off + hk*Bkv*dh
+  // (multi-head: Hk = H, G = 1, Bkv = B, v_off = 0; GQA: K and V share one unit)
+  int32_t Hk, G, Bkv;
+  int64_t v_off;
   float scale_log2;       // scale * log2(e)
   // ---- fused step kernel only: KV tasks first, then hidden tasks in GEMM n-tile order
   const int32_t* kv_split_ids;   // splits of KV-mode requests
@@ -96,9 +101,10 @@ struct ReconParams {
   const void* pool;
   const void* w_int;      // head-interleaved W_KV copy, [2d, d]: row h*2dh + kv*dh + c
   const float* b_int;     // nullable, same interleaving
-  void* scr_k;
+  void* scr_k;            // [hblock][Hk][B][dh]
   void* scr_v;
   int32_t d, H, dh, B;
+  int32_t Hk, dk;         // K/V heads and K (or V) row width Hk*dh (GEMM N = 2 dk; GQA, R18)
   int32_t* sync_counter;  // >= 32*num_sms zeroed ints (pair progress words)
   const int32_t* hblk_pos;  // token position of row 0 of each hidden block (RoPE / attend; nullable)
   const double* rope_inv;   // RoPE: inv_freq table [dh/2] (nullable = no RoPE)
@@ -130,11 +136,13 @@ struct AppendReq {
 struct AppendParams {
   const AppendReq* reqs;
   const int32_t* tabs;
-  const void* k;
+  const void* k;          // [rows, dk]
   const void* v;
-  const void* x;
+  const void* x;          // [rows, d]
   void* pool;
   int32_t n_req, d, H, dh, B;
+  int32_t dk, Bkv;        // KV row width and tokens per KV logical block (AttnParams)
+  int64_t v_off;
 };
 
 // Dense projection GEMM for the current-token q/k/v map and the output map (NEXT row f1):
@@ -149,19 +157,21 @@ struct DenseParams {
   void* pool;              // epi 1: unit blocks
   const int32_t* row_dst;  // epi 1: per row {K block, V block, slot, 0}; K block < 0 = hidden row
   int32_t d, H, dh, B;
-  void* kvbuf;             // epi 1 (prefill): also each row's head-interleaved K||V, [M, 2d]
+  int32_t dk, Bkv;         // epi 1: K/V row width, tokens per KV logical block (GQA, R18)
+  int64_t v_off;           // epi 1: V rows' offset inside the V unit (GQA: K and V share a unit)
+  void* kvbuf;             // epi 1 (prefill): also each row's head-interleaved K||V, [M, 2dk]
   const double* rope_inv;  // epi 1: rotate q and k at row_dst[4r+3] (nullable = no RoPE)
 };
 
 // dtype: 0 bf16, 1 fp32
 cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaStream_t s);
 cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d,
-                              int H, int dh, int dtype, cudaStream_t s);
+                              int dk, int dh, int dtype, cudaStream_t s);
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
 // tmap_w: W_int with 256-row boxes (1-SM kernel); tmap_w_half: 128-row boxes (CTA-pair kernel)
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
                             const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s);
-bool recon_tc_supported(int d, int H, int dh, int B);
+bool recon_tc_supported(int d, int dk, int dh, int B);
 bool dense_tc_supported(int d);
 // tmap_a: A with {64 x 128} boxes; tmap_w: W with {64 x 128} boxes
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s);
@@ -170,7 +180,7 @@ cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sm
 bool attn_pipe_supported(int dtype, int dh, int B);
 // Fused step: reconstruction GEMM (CTA pairs, 256x512 tiles) and split-K attention warps in
 // one persistent kernel; hidden tasks wait on per-tile completion counters.
-bool fused_supported(int d, int H, int dh, int B);
+bool fused_supported(int d, int dk, int dh, int B);
 int fused_tile_m();
 int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
@@ -185,12 +195,13 @@ cudaError_t launch_layer_norm(const void* x, void* u, const float* gamma, const 
 // Causal self-attention over each request's new tokens (prefill / recompute, NEXT row f3).
 struct PrefillAttnParams {
   const void* q;            // [R, d] (R = sum of lens), heads = dh-column slices
-  const void* kv;           // [R, 2d], head-interleaved K_h || V_h per row
+  const void* kv;           // [R, 2dk], head-interleaved K_hk || V_hk per row (hk = h / G)
   void* o;                  // [R, d]
   const int32_t* row0;      // [n_req + 1] first row of each request (prefix sums of lens)
   const int32_t* tile_req;  // [n_qtiles] request of each 64-row query tile
   const int32_t* tile_q0;   // [n_qtiles] first query row (within its request) of each tile
   int32_t n_qtiles, H, dh, d;
+  int32_t dk, G;            // K/V row width and query heads per K/V head (GQA, R18)
   float scale_log2;
 };
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, int dtype, cudaStream_t s);

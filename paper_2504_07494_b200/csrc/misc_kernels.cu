@@ -8,33 +8,36 @@ namespace hc {
 namespace {
 
 // Block-wise cache write, "fusing reshaping with read/write": each appended row
-// goes to (table[pos / B], pos % B).  KV rows are scattered head-major ([H][B][dh] per
-// unit block, so a head's rows of a block are contiguous for the attention reads);
-// hidden rows are stored row-major ([B][d], the GEMM's gathered A operand).
+// goes to (table[pos / Bb], pos % Bb).  KV rows are scattered head-major ([Hk][Bkv][dh] per
+// K (V) region, so a head's rows of a block are contiguous for the attention reads; under
+// GQA the V region sits v_off elements into the same unit); hidden rows are stored
+// row-major ([B][d], the GEMM's gathered A operand).
 // 16-byte vectors; grid.y = request of the call, grid.x strides over its rows.
 template <typename T>
 __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
   const AppendReq rq = p.reqs[blockIdx.y];
   constexpr int VE = 16 / sizeof(T);   // elements per vector
-  const int d = p.d, B = p.B, dh = p.dh;
-  const int nvec = d / VE;
+  const int d = p.d, B = p.B, dh = p.dh, dk = p.dk;
+  const int Bb = rq.mode == 0 ? p.Bkv : B;   // tokens per logical block of this mode
   T* pool = static_cast<T*>(p.pool);
-  const int lb_first = rq.start / B;
+  const int lb_first = rq.start / Bb;
   for (int r = blockIdx.x; r < rq.n_tok; r += gridDim.x) {
     const int pos = rq.start + r;
-    const int lb = pos / B - lb_first, row = pos % B;
-    const size_t src_row = (size_t)(rq.row_off + r) * d;
+    const int lb = pos / Bb - lb_first, row = pos % Bb;
     if (rq.mode == 0) {
+      const size_t src_row = (size_t)(rq.row_off + r) * dk;
       const int kb = p.tabs[rq.tab_off + 2 * lb], vb = p.tabs[rq.tab_off + 2 * lb + 1];
       const uint4* ks = reinterpret_cast<const uint4*>(static_cast<const T*>(p.k) + src_row);
       const uint4* vs = reinterpret_cast<const uint4*>(static_cast<const T*>(p.v) + src_row);
-      for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
+      for (int e = threadIdx.x; e < dk / VE; e += blockDim.x) {
         const int col = e * VE, h = col / dh, c = col - h * dh;
-        const size_t off = (size_t)h * B * dh + (size_t)row * dh + c;
+        const size_t off = (size_t)h * Bb * dh + (size_t)row * dh + c;
         *reinterpret_cast<uint4*>(pool + (size_t)kb * B * d + off) = ks[e];
-        *reinterpret_cast<uint4*>(pool + (size_t)vb * B * d + off) = vs[e];
+        *reinterpret_cast<uint4*>(pool + (size_t)vb * B * d + p.v_off + off) = vs[e];
       }
     } else {
+      const size_t src_row = (size_t)(rq.row_off + r) * d;
+      const int nvec = d / VE;
       const int xb = p.tabs[rq.tab_off + lb];
       const uint4* xs = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + src_row);
       uint4* dst = reinterpret_cast<uint4*>(pool + (size_t)xb * B * d + (size_t)row * d);
@@ -43,15 +46,16 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
   }
 }
 
-// W_int[h*2dh + kv*dh + c, :] = W_KV[kv*d + h*dh + c, :]  (and the bias likewise): one
-// N=256 GEMM tile of the head-interleaved weight then yields K_h || V_h directly.
+// W_int[h*2dh + kv*dh + c, :] = W_KV[kv*dk + h*dh + c, :]  (and the bias likewise; h runs
+// over the Hk K/V heads, dk = Hk*dh): one N=256 GEMM tile of the head-interleaved weight
+// then yields K_h || V_h directly.
 template <typename T>
 __global__ void __launch_bounds__(256) relayout_kernel(const T* __restrict__ w, T* __restrict__ wi,
                                                        const float* __restrict__ b, float* __restrict__ bi,
-                                                       int d, int dh) {
-  const int dst = blockIdx.x;   // 0 .. 2d-1
+                                                       int d, int dk, int dh) {
+  const int dst = blockIdx.x;   // 0 .. 2dk-1
   const int h = dst / (2 * dh), rem = dst - h * 2 * dh, kv = rem / dh, c = rem - kv * dh;
-  const int src = kv * d + h * dh + c;
+  const int src = kv * dk + h * dh + c;
   constexpr int VE = 16 / sizeof(T);
   const uint4* s = reinterpret_cast<const uint4*>(w + (size_t)src * d);
   uint4* o = reinterpret_cast<uint4*>(wi + (size_t)dst * d);
@@ -148,15 +152,14 @@ cudaError_t launch_append(const AppendParams& p, int dtype, int max_rows, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d, int H,
+cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float* b_int, int d, int dk,
                               int dh, int dtype, cudaStream_t s) {
-  (void)H;
   if (dtype == 1)
-    relayout_kernel<float><<<2 * d, 256, 0, s>>>(static_cast<const float*>(w), static_cast<float*>(w_int),
-                                                 b, b_int, d, dh);
+    relayout_kernel<float><<<2 * dk, 256, 0, s>>>(static_cast<const float*>(w), static_cast<float*>(w_int),
+                                                  b, b_int, d, dk, dh);
   else
-    relayout_kernel<__nv_bfloat16><<<2 * d, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(w),
-                                                         static_cast<__nv_bfloat16*>(w_int), b, b_int, d, dh);
+    relayout_kernel<__nv_bfloat16><<<2 * dk, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(w),
+                                                          static_cast<__nv_bfloat16*>(w_int), b, b_int, d, dk, dh);
   return cudaGetLastError();
 }
 

@@ -35,7 +35,10 @@ struct TcArgs {
   const int32_t* gather;
   int32_t n_hblocks, M, B, rows_per_box;
   int32_t m_tiles, n_tiles, k_iters;
-  int32_t H, dh, d;
+  int32_t H, dh, d;         // H: K/V heads of the GEMM's K||V columns (= query heads unless GQA)
+  int32_t grp;              // query heads per K/V head (GQA, R18; 1 = multi-head)
+  int32_t dk, Bkv;          // EPI_PROJECT: K/V row width, tokens per KV logical block
+  int64_t v_off;            // EPI_PROJECT: V rows' offset inside their unit (GQA: K, V share one)
   __nv_bfloat16* scr_k;
   __nv_bfloat16* scr_v;
   const float* bias;
@@ -58,8 +61,8 @@ struct TcArgs {
   const int32_t* hblk_req;  // batch index of each hidden block's request
   const ReqDesc* reqs;
   const __nv_bfloat16* q;   // [n_req, d]
-  float* part_ml;           // [H][n_splits_all][2]
-  float* part_acc;          // [H][n_splits_all][dh]
+  float* part_ml;           // [H*grp][n_splits_all][2]  (query heads)
+  float* part_acc;          // [H*grp][n_splits_all][dh]
   int32_t n_splits_all;
   float scale_log2;
   int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
@@ -171,9 +174,10 @@ __device__ __forceinline__ void store_chunk(const TcArgs& a, int n, const float 
       if (dst_info.x >= 0) {
         const int h = m / (2 * a.dh), rem = m - h * 2 * a.dh, kv = rem / a.dh, c0 = rem - kv * a.dh;
         const int blk = kv ? dst_info.y : dst_info.x;
-        dst = a.pool + (size_t)blk * a.B * a.d + (size_t)h * a.B * a.dh + (size_t)dst_info.z * a.dh + c0;
+        dst = a.pool + (size_t)blk * a.B * a.d + (kv ? a.v_off : 0) + (size_t)h * a.Bkv * a.dh +
+              (size_t)dst_info.z * a.dh + c0;
       }
-      if (a.kvbuf) dst2 = a.kvbuf + (size_t)grow * 2 * a.d + m;
+      if (a.kvbuf) dst2 = a.kvbuf + (size_t)grow * 2 * a.dk + m;
     }
   }
   if (dst == nullptr && dst2 == nullptr) return;
@@ -242,11 +246,12 @@ __device__ __forceinline__ float dot32_q(const float (&f)[32], const uint4 (&u)[
 }
 
 // One pair tile's rows -> partials.  Thread = GEMM row (a token of a hidden block); the
-// tile's columns are HT = TILE_N / (2 dh) heads of K_h || V_h.  Per head: s = scale *
-// q_h . k (bias and RoPE applied to k in registers), segment max / sum over the S lanes of
-// the segment, and the segment's sum_j p_j v_j by a butterfly reduce-scatter; lane i of the
-// segment writes dims [i*32/S, (i+1)*32/S) of every 32-column chunk.  Rows past M and
-// tokens past n get p = 0; a segment that starts past n writes nothing.
+// tile's columns are HT = TILE_N / (2 dh) K/V heads of K_hk || V_hk, each serving grp query
+// heads (GQA, R18).  Per query head: s = scale * q_h . k (bias and RoPE applied to k in
+// registers), segment max / sum over the S lanes of the segment, and the segment's
+// sum_j p_j v_j by a butterfly reduce-scatter; lane i of the segment writes dims
+// [i*32/S, (i+1)*32/S) of every 32-column chunk.  Rows past M and tokens past n get p = 0;
+// a segment that starts past n writes nothing.
 template <int S, int TILE_N>
 __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane) {
   const bool valid = grow < a.M;
@@ -263,9 +268,10 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
   const int split = valid ? a.reqs[req].split_begin + tok0 / S : 0;
   const int dh = a.dh, HT = TILE_N / (2 * dh);
 #pragma unroll 1
-  for (int j = 0; j < HT; ++j) {
-    const int h = nt * HT + j;
-    const int nk = nt * TILE_N + j * 2 * dh;      // interleaved column of K_h (bias index)
+  for (int jg = 0; jg < HT * a.grp; ++jg) {
+    const int j = jg / a.grp;                     // K/V head of the tile
+    const int h = (nt * HT + j) * a.grp + (jg - j * a.grp);   // query head
+    const int nk = nt * TILE_N + j * 2 * dh;      // interleaved column of K_hk (bias index)
     const uint32_t tk = tacc + j * 2 * dh;
     const __nv_bfloat16* qh = a.q + (size_t)req * a.d + h * dh;
     float s = 0.f;

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(128) prefill_attn_mma_kernel(const PrefillAttn
     for (int i = tid; i < KT * CH; i += 128) {
       const int r = i / CH, c = i - r * CH;
       const int tok = min(t * KT + r, L - 1);
-      const __nv_bfloat16* src = KV + (size_t)(row0 + tok) * 2 * d + h * 2 * DH + c * 8;
+      const __nv_bfloat16* src = KV + (size_t)(row0 + tok) * 2 * p.dk + (h / p.G) * 2 * DH + c * 8;
       cp_async16(k + swz<DH>(r, c), src);
       cp_async16(v + swz<DH>(r, c), src + DH);
     }
@@ -322,10 +322,10 @@ __global__ void __launch_bounds__(64 + 128 * NQ, (BK == 64 && NQ == 1) ? 2 : 1)
         ptx::mbar_wait(&kv_empty[st], ((t / ST) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * NCH * KCH);
         for (int c = 0; c < NCH; ++c) {
-          ptx::tma_load_2d(smem + K_OFF + (st * NCH + c) * KCH, &tmap_kv, h * 2 * DH + c * 64, row0 + t * BK,
-                           &kv_full[st]);
-          ptx::tma_load_2d(smem + V_OFF + (st * NCH + c) * KCH, &tmap_kv, h * 2 * DH + DH + c * 64, row0 + t * BK,
-                           &kv_full[st]);
+          ptx::tma_load_2d(smem + K_OFF + (st * NCH + c) * KCH, &tmap_kv, (h / p.G) * 2 * DH + c * 64,
+                           row0 + t * BK, &kv_full[st]);
+          ptx::tma_load_2d(smem + V_OFF + (st * NCH + c) * KCH, &tmap_kv, (h / p.G) * 2 * DH + DH + c * 64,
+                           row0 + t * BK, &kv_full[st]);
         }
       }
     }
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(128) prefill_attn_simt_kernel(const PrefillAtt
       const int j = j0 + lane;
       float sc = -INFINITY;
       if (j <= qi) {
-        const T* kr = KV + (size_t)(row0 + j) * 2 * d + h * 2 * DH;
+        const T* kr = KV + (size_t)(row0 + j) * 2 * p.dk + (h / p.G) * 2 * DH;
         float a = 0.f;
         for (int c = 0; c < DH; ++c) a += qs[warp][c] * ldf(kr + c);
         sc = a;
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(128) prefill_attn_simt_kernel(const PrefillAtt
       const int cnt = min(32, qi + 1 - j0);
       for (int jj = 0; jj < cnt; ++jj) {
         const float pw = __shfl_sync(FULL, pj, jj);
-        const T* vr = KV + (size_t)(row0 + j0 + jj) * 2 * d + h * 2 * DH + DH;
+        const T* vr = KV + (size_t)(row0 + j0 + jj) * 2 * p.dk + (h / p.G) * 2 * DH + DH;
         for (int i = 0; i < 8; ++i) {
           const int c = lane + 32 * i;
           if (c < DH) acc[i] += pw * ldf(vr + c);

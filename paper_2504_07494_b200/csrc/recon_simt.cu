@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) recon_simt_kernel(const ReconParams p) {
   __shared__ float Bs[TK][TN + 1];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
-  const int d = p.d, B = p.B, M = p.n_hblocks * B, N = 2 * d;
+  const int d = p.d, B = p.B, M = p.n_hblocks * B, N = 2 * p.dk;
   const T* pool = static_cast<const T*>(p.pool);
   const T* w = static_cast<const T*>(p.w_int);
   float acc[4][4] = {};
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) recon_simt_kernel(const ReconParams p) {
     }
     __syncthreads();
   }
-  const int H = p.H, dh = p.dh;
+  const int H = p.Hk, dh = p.dh;   // scratch [hblock][Hk][B][dh]
   T* sk = static_cast<T*>(p.scr_k);
   T* sv = static_cast<T*>(p.scr_v);
 #pragma unroll
@@ -154,12 +154,13 @@ __global__ void __launch_bounds__(256) dense_simt_kernel(const DenseParams p) {
         out[(size_t)row * p.d + n] = from_f<T>(v);
       } else {
         const int m = n - p.d;
-        if (p.kvbuf) static_cast<T*>(p.kvbuf)[(size_t)row * 2 * p.d + m] = from_f<T>(v);
+        if (p.kvbuf) static_cast<T*>(p.kvbuf)[(size_t)row * 2 * p.dk + m] = from_f<T>(v);
         const int4 di = reinterpret_cast<const int4*>(p.row_dst)[row];
         if (di.x < 0) continue;
         const int h = m / (2 * p.dh), rem = m - h * 2 * p.dh, kv = rem / p.dh, c = rem - kv * p.dh;
         const int blk = kv ? di.y : di.x;
-        pool[(size_t)blk * p.B * p.d + (size_t)h * p.B * p.dh + (size_t)di.z * p.dh + c] = from_f<T>(v);
+        pool[(size_t)blk * p.B * p.d + (kv ? p.v_off : 0) + (size_t)h * p.Bkv * p.dh + (size_t)di.z * p.dh + c] =
+            from_f<T>(v);
       }
     }
   }
@@ -179,7 +180,7 @@ cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s) {
 
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s) {
   if (p.n_hblocks <= 0) return cudaSuccess;
-  const int M = p.n_hblocks * p.B, N = 2 * p.d;
+  const int M = p.n_hblocks * p.B, N = 2 * p.dk;
   dim3 grid((M + 63) / 64, (N + 63) / 64);
   if (dtype == 1)
     recon_simt_kernel<float><<<grid, 256, 0, s>>>(p);

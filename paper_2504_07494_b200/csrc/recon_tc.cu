@@ -234,7 +234,7 @@ cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_hal
   using PC = pg::PairCfg<NSUB, NSTAGE>;
   constexpr int smem = 1024 + PC::REGION_BYTES;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
-  a.n_tiles = (a.n_total > 0 ? a.n_total : 2 * a.d) / PC::TILE_N;
+  a.n_tiles = (a.n_total > 0 ? a.n_total : 2 * a.dk) / PC::TILE_N;   // reconstruction: N = 2 dk (K || V)
   cudaError_t e = cudaFuncSetAttribute(recon_tc2_kernel<NSUB, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int tiles = a.m_tiles * a.n_tiles;
@@ -259,9 +259,13 @@ cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void
   a.B = p.B;
   a.rows_per_box = 128;
   a.k_iters = p.K / BK;
-  a.H = p.H;
+  a.H = p.dk / p.dh;
+  a.grp = 1;
   a.dh = p.dh;
   a.d = p.d;
+  a.dk = p.dk;
+  a.Bkv = p.Bkv;
+  a.v_off = p.v_off;
   a.bias = p.bias;
   a.group_m = -2;
   a.epi = p.epi;
@@ -275,10 +279,10 @@ cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void
   return launch_pair<1, 6>(a, tmap_a, tmap_w, num_sms, s);
 }
 
-bool recon_tc_supported(int d, int H, int dh, int B) {
-  if (d % BK != 0 || d != H * dh) return false;
+bool recon_tc_supported(int d, int dk, int dh, int B) {
+  if (d % BK != 0 || dk % dh != 0) return false;
   if ((2 * dh) > BN || BN % (2 * dh) != 0 || dh % 32 != 0) return false;
-  if ((2 * d) % BN != 0) return false;
+  if ((2 * dk) % BN != 0) return false;
   if (B < 8 || (B & (B - 1)) != 0) return false;  // power of two >= 8: boxes are whole swizzle atoms
   if (B > BM && B % BM != 0) return false;
   return true;
@@ -294,9 +298,11 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   a.M = p.n_hblocks * p.B;
   a.rows_per_box = p.B < BM ? p.B : BM;
   a.m_tiles = (a.M + BM - 1) / BM;
-  a.n_tiles = 2 * p.d / BN;
+  a.n_tiles = 2 * p.dk / BN;
   a.k_iters = p.d / BK;
-  a.H = p.H;
+  a.H = p.Hk;
+  a.grp = p.H / p.Hk;
+  a.dk = p.dk;
   a.dh = p.dh;
   a.d = p.d;
   a.scr_k = static_cast<__nv_bfloat16*>(p.scr_k);
@@ -324,7 +330,7 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   a.sync = (a.sync_w > 0 && a.group_m == -2) ? p.sync_counter : nullptr;
   const bool pair_mode = recon_pair_mode(p.B, t) || p.rope_inv || p.epi_attend;
   if (pair_mode) {
-    const bool can2 = (2 * p.d) % 512 == 0;
+    const bool can2 = (2 * p.dk) % 512 == 0;
     if (can2 && t.tc_nsub != 1) {
       if (t.tc_stages == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s);
       return launch_pair<2, 4>(a, tmap_x, tmap_w_half, num_sms, s);

@@ -64,13 +64,40 @@ struct Layout {  // storage layout
   bool has_q, has_o, has_ln;
 };
 
+// K/V geometry (GQA, DESIGN R18): Hk K/V heads, K (or V) row width dk = Hk*dh, tokens per KV
+// logical block Bkv, and whether K and V share one unit (packed: Bkv = B d / (2 dk)).
+struct KvGeom {
+  int32_t Hk = 0, dk = 0, Bkv = 0;
+  bool packed = false;
+  int64_t v_off = 0;   // elements from a V unit's base to its V rows
+};
+bool kv_geom(const hc_pool_config* c, KvGeom* g) {
+  const int32_t Hk = c->n_kv_heads > 0 ? c->n_kv_heads : c->n_heads;
+  if (Hk > c->n_heads || c->n_heads % Hk != 0 || c->n_kv_heads < 0) return false;
+  g->Hk = Hk;
+  g->dk = Hk * c->head_dim;
+  if (Hk == c->n_heads) {   // multi-head: a K unit and a V unit per B tokens
+    g->Bkv = c->block_size;
+    g->packed = false;
+    g->v_off = 0;
+    return true;
+  }
+  if (c->d_model % (2 * g->dk) != 0) return false;
+  g->Bkv = c->block_size * (c->d_model / (2 * g->dk));
+  g->packed = true;
+  g->v_off = (int64_t)Hk * g->Bkv * c->head_dim;
+  return true;
+}
+
 bool layout_for(const hc_pool_config* c, Layout* L) {
   if (!c || c->d_model <= 0 || c->n_heads <= 0 || c->head_dim <= 0 || c->block_size <= 0 ||
       c->num_blocks <= 0 || (c->dtype != HC_BF16 && c->dtype != HC_F32))
     return false;
   if ((int64_t)c->n_heads * c->head_dim != c->d_model) return false;
+  KvGeom kg;
+  if (!kv_geom(c, &kg)) return false;
   const size_t e = c->dtype == HC_BF16 ? 2 : 4;
-  const size_t d = (size_t)c->d_model;
+  const size_t d = (size_t)c->d_model, dk = (size_t)kg.dk;
   L->has_q = c->w_q != nullptr;
   L->has_o = c->w_o != nullptr;
   L->has_ln = c->ln_gamma != nullptr;
@@ -78,10 +105,10 @@ bool layout_for(const hc_pool_config* c, Layout* L) {
   L->blocks_bytes = (size_t)c->num_blocks * c->block_size * d * e;
   L->wq_off = align_up(L->blocks_off + L->blocks_bytes, 1024);
   L->w_off = L->wq_off + (L->has_q ? d * d * e : 0);
-  L->w_bytes = 2 * d * d * e;
+  L->w_bytes = 2 * dk * d * e;
   L->bq_off = align_up(L->w_off + L->w_bytes, kAlign);
   L->b_off = L->bq_off + d * sizeof(float);
-  L->b_bytes = 2 * d * sizeof(float);
+  L->b_bytes = 2 * dk * sizeof(float);
   size_t o = align_up(L->b_off + L->b_bytes, 1024);
   L->wo_off = L->bo_off = 0;
   if (L->has_o) {
@@ -190,7 +217,7 @@ struct Pinned {
 
 // Decode-call plan: sizes and offsets inside the caller's workspace.
 struct Plan {
-  int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1;
+  int32_t n_req = 0, n_splits = 0, n_hb = 0, split_blocks = 1, split_blocks_kv = 1;
   int32_t n_kv_splits = 0, n_hid_splits = 0;
   int64_t kv_tokens = 0;
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
@@ -213,6 +240,7 @@ struct hc_pool {
   hc_pool_config cfg{};
   Layout L{};
   Tuning tune{};   // read once at create
+  KvGeom kv{};     // K/V heads, row width, tokens per KV logical block (GQA, R18)
   size_t elem = 2;
   bool accounting = false;
   bool has_bias = false;
@@ -333,12 +361,13 @@ struct hc_pool {
     const int B = cfg.block_size, H = cfg.n_heads, dh = cfg.head_dim;
     P.n_req = (int32_t)rs.size();
     P.split_blocks = cfg.split_tokens > 0 ? std::max(1, (int)cdiv(cfg.split_tokens, B)) : split_tokens_auto(rs);
+    P.split_blocks_kv = std::max(1, P.split_blocks * B / kv.Bkv);   // same tokens per split in KV blocks
     P.absorb = (cfg.flags & HC_FLAG_ABSORB_HIDDEN) != 0;
     P.attend = !P.absorb && tc_ok && cfg.dtype == HC_BF16 && tune.epi_attend != 0 && recon_pair_mode(B, tune);
     P.seg = std::min(B, 32);
     for (auto* r : rs) {
-      const int64_t nb = cdiv(r->n, B);
-      const int32_t ns = (int32_t)cdiv(nb, P.split_blocks);
+      const int64_t nb = cdiv(r->n, r->mode == HC_MODE_KV ? kv.Bkv : B);
+      const int32_t ns = (int32_t)cdiv(nb, r->mode == HC_MODE_KV ? P.split_blocks_kv : P.split_blocks);
       if (r->mode == HC_MODE_KV) {
         P.n_splits += ns;
         P.n_tab += 2 * nb;
@@ -359,10 +388,10 @@ struct hc_pool {
     }
     P.Hp = (int32_t)align_up((size_t)H, 16);
     P.fused = !P.absorb && tc_ok && P.n_hb > 0 && tune.fused != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
-              fused_supported(cfg.d_model, cfg.n_heads, cfg.head_dim, B);
+              fused_supported(cfg.d_model, kv.dk, cfg.head_dim, B);
     if (P.fused) {
       P.gemm_m_tiles = (int32_t)cdiv((int64_t)P.n_hb * B, fused_tile_m());
-      P.gemm_n_tiles = 2 * cfg.d_model / fused_tile_n();
+      P.gemm_n_tiles = 2 * kv.dk / fused_tile_n();
     }
     size_t o = kHeaderBytes;  // header: attention task counter, then GEMM pair-progress words
     P.off_reqs = o = align_up(o, 64);
@@ -399,7 +428,7 @@ struct hc_pool {
     const size_t n_tasks = (size_t)P.n_splits * H;
     P.off_ml = P.desc_bytes;
     P.off_acc = align_up(P.off_ml + n_tasks * 2 * sizeof(float), kAlign);
-    const size_t scr = (P.absorb || P.attend) ? 0 : (size_t)P.n_hb * H * B * dh * elem;
+    const size_t scr = (P.absorb || P.attend) ? 0 : (size_t)P.n_hb * kv.Hk * B * dh * elem;
     P.off_sk = align_up(P.off_acc + n_tasks * dh * sizeof(float), 1024);
     P.off_sv = align_up(P.off_sk + scr, 1024);
     size_t e = align_up(P.off_sv + scr, kAlign);
@@ -442,14 +471,19 @@ int64_t hc_units_needed(const hc_pool_config* cfg, int32_t mode, int64_t n_token
     g_err = "invalid config, mode or n_tokens";
     return -1;
   }
-  return cdiv(n_tokens, cfg->block_size) * (mode == HC_MODE_KV ? 2 : 1);
+  if (mode == HC_MODE_HIDDEN) return cdiv(n_tokens, cfg->block_size);
+  KvGeom kg;
+  kv_geom(cfg, &kg);   // valid: layout_for checked it
+  return cdiv(n_tokens, kg.Bkv) * (kg.packed ? 1 : 2);
 }
 
 hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   if (!out) return fail(HC_E_INVALID, "out is null");
   *out = nullptr;
   Layout L;
-  if (!layout_for(cfg, &L)) return fail(HC_E_INVALID, "invalid pool config (d = H*dh, positive sizes, dtype)");
+  if (!layout_for(cfg, &L))
+    return fail(HC_E_INVALID, "invalid pool config (d = H*dh, positive sizes, dtype; GQA: H % n_kv_heads == 0 and "
+                              "d % (2 n_kv_heads dh) == 0)");
   const size_t e = cfg->dtype == HC_BF16 ? 2 : 4;
   if ((cfg->head_dim * e) % 16 != 0)
     return fail(HC_E_UNSUPPORTED, "head_dim * element size must be a multiple of 16 bytes");
@@ -457,17 +491,21 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   if (cfg->num_blocks > INT32_MAX || (int64_t)cfg->num_blocks * cfg->block_size > INT32_MAX)
     return fail(HC_E_UNSUPPORTED, "num_blocks * block_size must fit in int32");
   const bool accounting = (cfg->flags & HC_FLAG_ACCOUNTING_ONLY) != 0;
+  KvGeom kg;
+  kv_geom(cfg, &kg);   // valid: layout_for checked it (H % Hk == 0, d % (2 Hk dh) == 0 under GQA)
+  if ((cfg->flags & HC_FLAG_ABSORB_HIDDEN) && kg.Hk != cfg->n_heads)
+    return fail(HC_E_UNSUPPORTED, "HC_FLAG_ABSORB_HIDDEN needs multi-head attention (n_kv_heads = n_heads)");
   if (cfg->rope_theta < 0.f) return fail(HC_E_INVALID, "rope_theta < 0");
   if (cfg->ln_gamma && !(cfg->ln_eps >= 0.f)) return fail(HC_E_INVALID, "ln_eps < 0");
   if (cfg->rope_theta > 0.f &&
       (cfg->dtype != HC_BF16 || (cfg->flags & HC_FLAG_FORCE_SIMT) || cfg->head_dim % 64 != 0 ||
-       !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size) ||
+       !recon_tc_supported(cfg->d_model, kg.dk, cfg->head_dim, cfg->block_size) ||
        !dense_tc_supported(cfg->d_model) || !(cfg->block_size <= 128 || cfg->block_size % 256 == 0)))
     return fail(HC_E_UNSUPPORTED, "RoPE needs the bf16 tcgen05 path and head_dim % 64 == 0");
   if ((cfg->flags & HC_FLAG_ABSORB_HIDDEN) &&
       (cfg->rope_theta > 0.f || (cfg->flags & HC_FLAG_FORCE_SIMT) ||
        !absorb_supported(cfg->dtype, cfg->d_model, cfg->head_dim, cfg->n_heads, cfg->block_size) ||
-       !recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)))
+       !recon_tc_supported(cfg->d_model, kg.dk, cfg->head_dim, cfg->block_size)))
     return fail(HC_E_UNSUPPORTED,
                 "HC_FLAG_ABSORB_HIDDEN needs bf16, no RoPE, d % 128 == 0, head_dim % 16 == 0, head_dim <= 128, "
                 "n_heads <= 128, block_size % 8 == 0 dividing or divisible by 128");
@@ -482,6 +520,7 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
   p->cfg = *cfg;
   p->L = L;
   p->tune = tuning_from_env();
+  p->kv = kg;
   p->elem = e;
   p->accounting = accounting;
   p->has_bias = cfg->b_kv != nullptr;
@@ -499,7 +538,7 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     err = cudaMemset(p->storage + L.blocks_off, 0, L.blocks_bytes);
     if (err == cudaSuccess)
       err = launch_relayout_w(cfg->w_kv, p->storage + L.w_off, cfg->b_kv, reinterpret_cast<float*>(p->storage + L.b_off),
-                              cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->dtype, 0);
+                              cfg->d_model, kg.dk, cfg->head_dim, cfg->dtype, 0);
     const size_t dd = (size_t)cfg->d_model * cfg->d_model * e;
     const size_t dbytes = (size_t)cfg->d_model * sizeof(float);
     if (err == cudaSuccess && L.has_q) err = cudaMemcpy(p->storage + L.wq_off, cfg->w_q, dd, cudaMemcpyDeviceToDevice);
@@ -531,7 +570,8 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
     if (p->dense_tc_ok) {
       bool ok = true;
       if (L.has_q)
-        ok &= make_tmap_2d(&p->tmap_wqkv, p->storage + L.wq_off, (uint64_t)cfg->d_model, 3 * (uint64_t)cfg->d_model,
+        ok &= make_tmap_2d(&p->tmap_wqkv, p->storage + L.wq_off, (uint64_t)cfg->d_model,
+                           (uint64_t)cfg->d_model + 2 * (uint64_t)kg.dk,
                            64, 128);
       if (L.has_o)
         ok &= make_tmap_2d(&p->tmap_wo, p->storage + L.wo_off, (uint64_t)cfg->d_model, (uint64_t)cfg->d_model, 64, 128);
@@ -541,15 +581,15 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
       }
     }
     if (cfg->dtype == HC_BF16 && !(cfg->flags & HC_FLAG_FORCE_SIMT) &&
-        recon_tc_supported(cfg->d_model, cfg->n_heads, cfg->head_dim, cfg->block_size)) {
+        recon_tc_supported(cfg->d_model, kg.dk, cfg->head_dim, cfg->block_size)) {
       // -DHC_DIAG builds, HC_DIAG_BOX=1 (timing diagnostic, wrong results): 128-row A boxes as if dense
       const uint32_t rpb = p->tune.diag_box ? 128u : (uint32_t)std::min(cfg->block_size, 128);
       const bool ok1 = make_tmap_2d(&p->tmap_x, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
                                     (uint64_t)cfg->num_blocks * cfg->block_size, 64, rpb);
       const bool ok2 = make_tmap_2d(&p->tmap_w, p->storage + L.w_off, (uint64_t)cfg->d_model,
-                                    2 * (uint64_t)cfg->d_model, 64, 256);
+                                    2 * (uint64_t)kg.dk, 64, 256);
       const bool ok3 = make_tmap_2d(&p->tmap_w_half, p->storage + L.w_off, (uint64_t)cfg->d_model,
-                                    2 * (uint64_t)cfg->d_model, 64, 128);
+                                    2 * (uint64_t)kg.dk, 64, 128);
       const bool ok4 = !(cfg->flags & HC_FLAG_ABSORB_HIDDEN) ||
                        make_tmap_2d(&p->tmap_x64, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
                                     (uint64_t)cfg->num_blocks * cfg->block_size, 64, (uint32_t)std::min(cfg->block_size, 64));
@@ -653,6 +693,9 @@ static hc_status scatter_rows(hc_pool* pool, const std::vector<AppendReq>& ar, c
     ap.H = pool->cfg.n_heads;
     ap.dh = pool->cfg.head_dim;
     ap.B = pool->cfg.block_size;
+    ap.dk = pool->kv.dk;
+    ap.Bkv = pool->kv.Bkv;
+    ap.v_off = pool->kv.v_off;
     err = launch_append(ap, pool->cfg.dtype, rows, s);
     if (err != cudaSuccess) return cuda_fail(err, "append kernel");
     ++pool->last_launches;
@@ -714,8 +757,9 @@ static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64
       n0 = it->second.n;
     }
     if (n0 + n_tokens[i] > INT32_MAX) return fail(HC_E_INVALID, "context too long");
-    const int64_t per = cdiv(n0 + n_tokens[i], B) - cdiv(n0, B);
-    need += modes[i] == HC_MODE_KV ? 2 * per : per;
+    const int Bm = modes[i] == HC_MODE_KV ? pool->kv.Bkv : B;
+    const int64_t per = cdiv(n0 + n_tokens[i], Bm) - cdiv(n0, Bm);
+    need += (modes[i] == HC_MODE_KV && !pool->kv.packed) ? 2 * per : per;
     (modes[i] == HC_MODE_KV ? kv_rows : x_rows) += n_tokens[i];
   }
   if (need > (int64_t)pool->free_ids.size()) return fail(HC_E_OOM, "not enough free blocks (all-or-nothing)");
@@ -732,11 +776,13 @@ static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64
     undo->e.push_back({req_ids[i], created, r.n, r.a.size(), r.b.size()});
     if (r.n == 0 && r.a.empty()) r.mode = modes[i];
     const int64_t t = n_tokens[i];
-    const int64_t new_lb = cdiv(r.n + t, B) - cdiv(r.n, B);
+    const int Bm = r.mode == HC_MODE_KV ? pool->kv.Bkv : B;   // tokens per logical block
+    const bool two = r.mode == HC_MODE_KV && !pool->kv.packed;  // separate K and V units
+    const int64_t new_lb = cdiv(r.n + t, Bm) - cdiv(r.n, Bm);
     for (int64_t j = 0; j < new_lb; ++j) {
       r.a.push_back(pool->free_ids.top());
       pool->free_ids.pop();
-      if (r.mode == HC_MODE_KV) {
+      if (two) {
         r.b.push_back(pool->free_ids.top());
         pool->free_ids.pop();
       }
@@ -748,10 +794,10 @@ static hc_status validate_and_allocate(hc_pool* pool, int32_t n_req, const int64
       q.n_tok = (int32_t)t;
       q.row_off = r.mode == HC_MODE_KV ? kv_off : x_off;
       q.tab_off = (int32_t)tabs->size();
-      const int64_t lb0 = r.n / B, lb1 = (r.n + t - 1) / B;
+      const int64_t lb0 = r.n / Bm, lb1 = (r.n + t - 1) / Bm;
       for (int64_t lb = lb0; lb <= lb1; ++lb) {
         tabs->push_back(r.a[lb]);
-        if (r.mode == HC_MODE_KV) tabs->push_back(r.b[lb]);
+        if (r.mode == HC_MODE_KV) tabs->push_back(two ? r.b[lb] : r.a[lb]);   // (K unit, V unit)
       }
       ar->push_back(q);
       *max_rows = std::max<int32_t>(*max_rows, (int32_t)t);
@@ -843,9 +889,11 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   // split per hidden segment (written by the GEMM epilogue, read only by the combine)
   int32_t next_hid = P.n_kv_splits;
   if (P.fused) std::memset(h + P.off_tiledone, 0, P.desc_bytes - P.off_tiledone);
+  const int Bkv = pool->kv.Bkv;
+  const bool packed = pool->kv.packed;
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = *rs[i];
-    const int32_t nb = (int32_t)cdiv(r.n, B);
+    const int32_t nb = (int32_t)cdiv(r.n, r.mode == HC_MODE_KV ? Bkv : B);
     ReqDesc d{};
     d.mode = r.mode;
     d.n = (int32_t)r.n;
@@ -854,7 +902,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       d.tab_off = n_tab;
       for (int32_t lb = 0; lb < nb; ++lb) {
         tab[n_tab++] = r.a[lb];
-        tab[n_tab++] = r.b[lb];
+        tab[n_tab++] = packed ? r.a[lb] : r.b[lb];
       }
     } else {
       d.scratch_blk0 = n_hb;
@@ -888,12 +936,14 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       continue;
     }
     const bool absorbed = P.absorb && r.mode == HC_MODE_HIDDEN;
-    for (int32_t lb = 0; lb < nb && !absorbed; lb += P.split_blocks) {
+    const int Bm = r.mode == HC_MODE_KV ? Bkv : B;
+    const int sb = r.mode == HC_MODE_KV ? P.split_blocks_kv : P.split_blocks;
+    for (int32_t lb = 0; lb < nb && !absorbed; lb += sb) {
       SplitDesc s{};
       s.req = i;
       s.lb0 = lb;
-      const int64_t t0 = (int64_t)lb * B;
-      s.ntok = (int32_t)std::min<int64_t>((int64_t)P.split_blocks * B, r.n - t0);
+      const int64_t t0 = (int64_t)lb * Bm;
+      s.ntok = (int32_t)std::min<int64_t>((int64_t)sb * Bm, r.n - t0);
       if (P.fused) (r.mode == HC_MODE_KV ? kvs[n_kvs++] : hds[n_hds++]) = n_split;
       sd[n_split++] = s;
     }
@@ -925,6 +975,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.scr_v = ws + P.off_sv;
   rp.d = pool->cfg.d_model;
   rp.H = H;
+  rp.Hk = pool->kv.Hk;
+  rp.dk = pool->kv.dk;
   rp.dh = pool->cfg.head_dim;
   rp.B = B;
   rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
@@ -957,6 +1009,10 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.dh = pool->cfg.head_dim;
   ap.B = B;
   ap.d = pool->cfg.d_model;
+  ap.Hk = pool->kv.Hk;
+  ap.G = H / pool->kv.Hk;
+  ap.Bkv = Bkv;
+  ap.v_off = pool->kv.v_off;
   ap.scale_log2 = scale * 1.4426950408889634f;
   ap.kv_evict_first = pool->tune.kv_evict_first;
   pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
@@ -1099,14 +1155,15 @@ static hc_status project_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
   // hidden rows (x itself) by the append scatter
   std::vector<AppendReq> har;
   std::vector<int32_t> row_dst(4 * (size_t)n_req, 0);
+  const int Bkv = pool->kv.Bkv;
   for (int32_t i = 0; i < n_req; ++i) {
     const Req& r = pool->reqs[req_ids[i]];
-    const int64_t pos = r.n - 1, lb = pos / B;
+    const int64_t pos = r.n - 1, lb = pos / Bkv;
     row_dst[4 * i + 3] = (int32_t)pos;   // RoPE position of the new token
     if (r.mode == HC_MODE_KV) {
       row_dst[4 * i] = r.a[lb];
-      row_dst[4 * i + 1] = r.b[lb];
-      row_dst[4 * i + 2] = (int32_t)(pos - lb * B);
+      row_dst[4 * i + 1] = pool->kv.packed ? r.a[lb] : r.b[lb];
+      row_dst[4 * i + 2] = (int32_t)(pos - lb * Bkv);
     } else {
       row_dst[4 * i] = row_dst[4 * i + 1] = -1;
       AppendReq q = ar[i];   // one token per request: ar[i] is request i
@@ -1135,10 +1192,13 @@ static hc_status project_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
   dp.w = pool->storage + pool->L.wq_off;
   dp.bias = reinterpret_cast<const float*>(pool->storage + pool->L.bq_off);   // [b_Q | b_int] (zeros if absent)
   dp.M = n_req;
-  dp.N = 3 * d;
+  dp.N = d + 2 * pool->kv.dk;
   dp.K = d;
   dp.epi = 1;
   dp.out = q_out;
+  dp.dk = pool->kv.dk;
+  dp.Bkv = pool->kv.Bkv;
+  dp.v_off = pool->kv.v_off;
   dp.pool = pool->storage + pool->L.blocks_off;
   dp.row_dst = reinterpret_cast<const int32_t*>(rd_dev);
   dp.rope_inv = pool->cfg.rope_theta > 0.f ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
@@ -1305,7 +1365,7 @@ PrefillPlan prefill_plan(const hc_pool* pool, int32_t n_req, const int32_t* lens
   P.off_q = o;
   o = align_up(o + P.rows * d * e, kAlign);
   P.off_kv = o;
-  o = align_up(o + P.rows * 2 * d * e, kAlign);
+  o = align_up(o + P.rows * 2 * (size_t)pool->kv.dk * e, kAlign);
   P.off_o = o;
   o = align_up(o + P.rows * d * e, kAlign);
   P.off_u = o;   // LN(x) when the pool has a LayerNorm
@@ -1392,12 +1452,12 @@ static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
     const Req& q = pool->reqs[req_ids[i]];
     row0[i] = (int32_t)r;
     for (int32_t tkn = 0; tkn < lens[i]; ++tkn, ++r) {
-      const int64_t lb = tkn / B;
+      const int64_t lb = tkn / pool->kv.Bkv;
       rowdst[4 * r + 3] = tkn;           // RoPE position
       if (q.mode == HC_MODE_KV) {
         rowdst[4 * r] = q.a[lb];
-        rowdst[4 * r + 1] = q.b[lb];
-        rowdst[4 * r + 2] = (int32_t)(tkn - lb * B);
+        rowdst[4 * r + 1] = pool->kv.packed ? q.a[lb] : q.b[lb];
+        rowdst[4 * r + 2] = (int32_t)(tkn - lb * pool->kv.Bkv);
       } else {
         rowdst[4 * r] = rowdst[4 * r + 1] = -1;
       }
@@ -1446,9 +1506,12 @@ static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
   dp.w = pool->storage + pool->L.wq_off;
   dp.bias = reinterpret_cast<const float*>(pool->storage + pool->L.bq_off);
   dp.M = (int32_t)P.rows;
-  dp.N = 3 * d;
+  dp.N = d + 2 * pool->kv.dk;
   dp.K = d;
   dp.epi = 1;
+  dp.dk = pool->kv.dk;
+  dp.Bkv = pool->kv.Bkv;
+  dp.v_off = pool->kv.v_off;
   dp.out = ws + P.off_q;
   dp.pool = pool->storage + pool->L.blocks_off;
   dp.row_dst = reinterpret_cast<const int32_t*>(ws + P.off_rowdst);
@@ -1478,11 +1541,14 @@ static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
   pa.H = H;
   pa.dh = dh;
   pa.d = d;
+  pa.dk = pool->kv.dk;
+  pa.G = H / pool->kv.Hk;
   pa.scale_log2 = scale * 1.4426950408889634f;
   if (prefill_uses_tc(pool)) {
     CUtensorMap tq, tkv;
     if (!make_tmap_2d(&tq, ws + P.off_q, (uint64_t)d, (uint64_t)P.rows, 64, 128) ||
-        !make_tmap_2d(&tkv, ws + P.off_kv, 2 * (uint64_t)d, (uint64_t)P.rows, 64, (uint32_t)prefill_attn_tc_keys(pool->tune)))
+        !make_tmap_2d(&tkv, ws + P.off_kv, 2 * (uint64_t)pool->kv.dk, (uint64_t)P.rows, 64,
+                      (uint32_t)prefill_attn_tc_keys(pool->tune)))
       return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed (prefill attention)");
     err = launch_prefill_attn_tc(pa, &tq, &tkv, pool->tune, s);
   } else {

@@ -40,6 +40,7 @@ class PoolConfig(ctypes.Structure):
         ("w_q", ctypes.c_void_p), ("b_q", ctypes.c_void_p), ("w_o", ctypes.c_void_p), ("b_o", ctypes.c_void_p),
         ("rope_theta", ctypes.c_float),
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
+        ("n_kv_heads", ctypes.c_int32),
     ]
 
 
@@ -145,9 +146,10 @@ def hc_units_needed(cfg: PoolConfig, mode: int, n_tokens: int) -> int:
 
 
 def units_needed(d_model: int, n_heads: int, head_dim: int, block_size: int, mode: int, n_tokens: int,
-                 dtype: int = HC_BF16) -> int:
+                 dtype: int = HC_BF16, n_kv_heads: int = 0) -> int:
     """Unit blocks of one request (the library's allocation rule; for sizing pools)."""
     cfg = PoolConfig(d_model, n_heads, head_dim, block_size, 1, dtype, HC_FLAG_ACCOUNTING_ONLY)
+    cfg.n_kv_heads = int(n_kv_heads)
     return hc_units_needed(cfg, mode, n_tokens)
 
 
@@ -266,11 +268,14 @@ class HybridCachePool:
                  w_q: Optional[torch.Tensor] = None, b_q: Optional[torch.Tensor] = None,
                  w_o: Optional[torch.Tensor] = None, b_o: Optional[torch.Tensor] = None,
                  rope_theta: float = 0.0, ln_gamma: Optional[torch.Tensor] = None,
-                 ln_beta: Optional[torch.Tensor] = None, ln_eps: float = 1e-5):
+                 ln_beta: Optional[torch.Tensor] = None, ln_eps: float = 1e-5, n_kv_heads: int = 0):
         self.cfg = PoolConfig(d_model, n_heads, head_dim, block_size, num_blocks, dtype, flags, None, 0,
                               None, None, device, split_tokens)
         self.cfg.rope_theta = float(rope_theta)
         self.cfg.ln_eps = float(ln_eps)
+        self.cfg.n_kv_heads = int(n_kv_heads)
+        self.Hk = int(n_kv_heads) or n_heads
+        self.dk = self.Hk * head_dim
         self.dtype = dtype
         self.tdtype = _TORCH_DT[dtype]
         self.d, self.H, self.dh, self.B = d_model, n_heads, head_dim, block_size
@@ -301,10 +306,10 @@ class HybridCachePool:
             self.cfg.storage = base + off
             self.cfg.storage_bytes = nbytes
             assert w_kv is not None and w_kv.is_cuda and w_kv.dtype == self.tdtype and w_kv.is_contiguous()
-            assert tuple(w_kv.shape) == (2 * d_model, d_model)
+            assert tuple(w_kv.shape) == (2 * self.dk, d_model)
             self.cfg.w_kv = w_kv.data_ptr()
             if b_kv is not None:
-                assert b_kv.is_cuda and b_kv.dtype == torch.float32 and b_kv.numel() == 2 * d_model
+                assert b_kv.is_cuda and b_kv.dtype == torch.float32 and b_kv.numel() == 2 * self.dk
                 self._b_keep = b_kv.contiguous()
                 self.cfg.b_kv = self._b_keep.data_ptr()
 

@@ -18,7 +18,7 @@ def pool_blocks(w: Workload, slack: float = 0.05) -> int:
     """Unit blocks for the workload's caches + slack (sized by the library's allocation rule)."""
     from paper_2504_07494_b200 import hc
     dt = hc.HC_BF16 if w.dtype == "bf16" else hc.HC_F32
-    need = sum(hc.units_needed(w.shape.d, w.shape.H, w.shape.dh, w.block_size, m, n, dt)
+    need = sum(hc.units_needed(w.shape.d, w.shape.H, w.shape.dh, w.block_size, m, n, dt, w.shape.n_kv)
                for n, m in zip(w.n, w.modes))
     return int(need * (1 + slack)) + 4
 
@@ -44,7 +44,7 @@ def make_pool(w: Workload, device: int = 0, flags: int = 0, split_tokens: int = 
     dt = hc.HC_BF16 if w.dtype == "bf16" else hc.HC_F32
     return hc.HybridCachePool(w.shape.d, w.shape.H, w.shape.dh, w.block_size,
                               num_blocks or pool_blocks(w), dt, W, b, device, flags, split_tokens,
-                              rope_theta=rope_theta)
+                              rope_theta=rope_theta, n_kv_heads=w.shape.n_kv)
 
 
 def fill(pool, w: Workload, device: int = 0, order: str = "rr", data=None, seed: int = 0, gen: str = "device"):
@@ -118,7 +118,7 @@ def make_layer_pool(w: Workload, device: int = 0, num_blocks: int = None, flags:
     return hc.HybridCachePool(w.shape.d, w.shape.H, w.shape.dh, w.block_size, num_blocks or pool_blocks(w),
                               dt, w.w_kv(device=dev), w.b_kv(device=dev), device, flags,
                               w_q=w.w_q(device=dev), b_q=w.b_q(device=dev), w_o=w.w_o(device=dev),
-                              b_o=w.b_o(device=dev), rope_theta=rope_theta, **lnk)
+                              b_o=w.b_o(device=dev), rope_theta=rope_theta, n_kv_heads=w.shape.n_kv, **lnk)
 
 
 def prefix_workload(w: Workload) -> Workload:

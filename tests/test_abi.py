@@ -134,3 +134,23 @@ def test_units_needed_matches_the_pool_contract(hc):
     assert p.request_info(0)[2] == hc.units_needed(32, 2, 16, 4, 0, 11)
     with pytest.raises(hc.HcError):
         hc.units_needed(32, 2, 16, 4, 2, 5)
+
+
+def test_gqa_unit_accounting(hc):
+    """GQA (R18): a KV token holds 2 Hk dh values, so one unit stores K and V of Bkv = B d/(2 Hk dh)
+    tokens; hidden stays one unit per B tokens.  LLaMA-3-8B (d 4096, 32/8 heads): KV needs half
+    the units of hidden; invalid groupings are refused."""
+    d, H, dh, B = 4096, 32, 128, 16
+    assert hc.units_needed(d, H, dh, B, 0, 100, n_kv_heads=8) == -(-100 // 32)
+    assert hc.units_needed(d, H, dh, B, 1, 100, n_kv_heads=8) == -(-100 // 16)
+    assert hc.units_needed(d, H, dh, B, 0, 100, n_kv_heads=4) == -(-100 // 64)
+    assert hc.units_needed(d, H, dh, B, 0, 100, n_kv_heads=32) == 2 * -(-100 // 16)   # = multi-head
+    with pytest.raises(hc.HcError):
+        hc.units_needed(d, H, dh, B, 0, 100, n_kv_heads=5)     # H % Hk != 0
+    assert hc.units_needed(d, H, dh, B, 0, 100, n_kv_heads=16) == -(-100 // 16)   # G = 2: K+V fill a unit
+    with pytest.raises(hc.HcError):
+        hc.units_needed(384, 6, 64, B, 0, 100, n_kv_heads=2)   # d % (2 Hk dh) != 0
+    p = hc.HybridCachePool(d, H, dh, B, 64, hc.HC_BF16, flags=hc.HC_FLAG_ACCOUNTING_ONLY, n_kv_heads=8)
+    p.append([0, 1], [0, 1], [33, 33])
+    assert p.request_info(0)[2] == 2 and p.request_info(1)[2] == 3
+    assert p.request_blocks(0, 0) == [0, 1] and p.request_blocks(0, 1) == [] and p.request_blocks(1, 0) == [2, 3, 4]

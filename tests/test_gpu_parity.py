@@ -64,8 +64,8 @@ SHAPES = [
 N_MIX = [1, 15, 16, 17, 129, 300, 513, 1000, 33, 2]
 
 
-def _bf16_workload(d, H, dh, B, n=N_MIX, bias=False, seed=11, modes=None):
-    shape = LayerShape(f"test-{d}", d, H, dh)
+def _bf16_workload(d, H, dh, B, n=N_MIX, bias=False, seed=11, modes=None, Hk=0):
+    shape = LayerShape(f"test-{d}" + (f"-gqa{Hk}" if Hk else ""), d, H, dh, Hk)
     if modes is None:
         modes = [MODE_KV if i % 2 == 0 else MODE_HIDDEN for i in range(len(n))]
     return Workload(f"bf16-{d}-{B}", shape, B, "bf16", seed, list(n), list(modes), list(range(len(n))), bias)
@@ -869,3 +869,117 @@ def test_bench_token_range_split_matches_the_oracle(hc, tmp_path):
     assert d["parts"].max() >= 2   # at least one request really was split
     err, lerr = T.compare(w, d["out"], d["lse"], range(len(w.n)))
     assert err <= TOL_F32 and lerr <= 1e-5, (err, lerr)
+
+
+# ------------------------------------------------------------------ grouped-query attention (f4 (i), R18)
+GQA_SHAPES = [
+    # (d, H, dh, B, Hk): fused tcgen05 path needs dh = 128 and 2*Hk*dh % 512 == 0
+    (1024, 8, 128, 16, 2),     # G = 4, Bkv = 32: fused
+    (4096, 32, 128, 16, 8),    # LLaMA-3-8B layer: fused
+    (4096, 32, 128, 16, 4),    # Yi-6B layer: G = 8, Bkv = 64
+    (512, 8, 64, 32, 2),       # dh 64: two-kernel tcgen05 path, Bkv = 64
+    (512, 8, 64, 16, 8),       # Hk = H spelled out: multi-head
+]
+
+
+@pytest.mark.parametrize("d,H,dh,B,Hk", GQA_SHAPES)
+def test_gqa_decode_vs_oracle(hc, d, H, dh, B, Hk):
+    """Mixed KV/hidden batch under GQA: KV tokens take one unit per Bkv = B d / (2 Hk dh) tokens
+    (K and V of Bkv tokens in one unit), hidden tokens one unit per B; query head h reads K/V
+    head h / G in the KV warps and in the attend epilogue (G query heads per rebuilt K/V head)."""
+    n = [1, 17, 300, 129, 64, 511, 33, 1000]
+    w = _bf16_workload(d, H, dh, B, n=n, bias=True, Hk=Hk)
+    pool, out, lse = _run(w)
+    err, lerr = T.compare(w, out, lse, range(len(n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= TOL_LSE, lerr
+    Bkv = B * d // (2 * Hk * dh) if Hk != H else B
+    for i in range(len(n)):
+        units = pool.request_info(w.req_ids[i])[2]
+        want = -(-n[i] // B) if w.modes[i] == MODE_HIDDEN else (-(-n[i] // Bkv) * (1 if Hk != H else 2))
+        assert units == want, (i, units, want)
+
+
+@pytest.mark.parametrize("env", [{"HC_FUSED": "0"}, {"HC_EPI_ATTEND": "0"}, {"HC_EPI_ATTEND": "0", "HC_FUSED": "0"}])
+def test_gqa_alternative_paths(hc, monkeypatch, env):
+    """GQA through the two-kernel path, the fused kernel with K/V scratch ([hblock][Hk][B][dh]),
+    and the stand-alone GEMM + attention kernel, at the LLaMA-3-8B head layout."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = _bf16_workload(1024, 8, 128, 16, n=[1, 17, 300, 129, 64, 511], bias=True, Hk=2)
+    _, out, lse = _run(w, split_tokens=64)
+    err, lerr = T.compare(w, out, lse, range(len(w.n)))
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+
+
+def test_gqa_fp32_simt_and_rope(hc):
+    """fp32 (SIMT reconstruction + generic attention) under GQA at 1e-5, and bf16 GQA with RoPE
+    (rebuilt K rotated per K/V head in the attend epilogue)."""
+    sh = LayerShape("gqa-f32", 128, 8, 16, 2)
+    w = Workload("gqa-f32", sh, 4, "f32", 5, [9, 1, 6, 40, 13], [MODE_KV, MODE_HIDDEN, MODE_HIDDEN, MODE_KV, MODE_HIDDEN],
+                 [0, 1, 2, 3, 4], True)
+    _, out, lse = _run(w)
+    err, lerr = T.compare(w, out, lse, range(len(w.n)))
+    assert err <= TOL_F32 and lerr <= 1e-5, (err, lerr)
+    w2 = _bf16_workload(1024, 8, 128, 16, n=[1, 17, 300, 2049, 64], bias=True, Hk=2)
+    pool = T.make_pool(w2, rope_theta=ROPE_THETA)
+    T.fill(pool, w2)
+    out2, lse2 = T.decode(pool, w2, T.queries(w2))
+    err2, lerr2 = T.compare(w2, out2, lse2, range(len(w2.n)), rope_theta=ROPE_THETA)
+    assert err2 <= TOL_BF16 and lerr2 <= TOL_LSE, (err2, lerr2)
+
+
+@pytest.mark.parametrize("shape", [(1024, 8, 128, 16, 2), (512, 8, 64, 32, 2)])
+def test_gqa_decode_layer_and_prefill_vs_oracle(hc, shape):
+    """f1/f3 under GQA: the projection GEMM's epilogue writes q and the K/V rows of the Hk heads
+    into the packed KV units; prefill attends with query head h on K/V head h / G."""
+    from oracle import hc_oracle as O
+    d, H, dh, B, Hk = shape
+    w = _bf16_workload(d, H, dh, B, n=[1, 2, 17, 129, 300, 33], bias=True, Hk=Hk)
+    dev = torch.device("cuda", 0)
+    pool = T.make_layer_pool(w)
+    T.fill(pool, T.prefix_workload(w))
+    x = torch.stack([w.x_t(i, device=dev) for i in range(len(w.n))]).contiguous()
+    y, lse = pool.decode_layer(w.req_ids, w.modes, x, w.scale)
+    y = y.float().cpu().numpy()
+    for i in range(len(w.n)):
+        y_ref, _, _, _ = T.oracle_layer(w, i)
+        assert O.max_rel_err(y[i][None], y_ref[None], H) <= TOL_BF16, i
+    w2 = _bf16_workload(d, H, dh, B, n=[65, 1, 300, 129], bias=True, seed=19, Hk=Hk)
+    pool2 = T.make_layer_pool(w2)
+    xp = torch.cat([w2.x(i, device=dev) for i in range(len(w2.n))]).contiguous()
+    yp = pool2.prefill_layer(w2.req_ids, w2.modes, w2.n, xp, w2.scale).float().cpu().numpy()
+    r = 0
+    kv_ref = []
+    for i in range(len(w2.n)):
+        Y, K, V = O.prefill_layer(w2.x(i), w2.w_q(), w2.w_kv(), w2.w_o(), H, w2.scale, w2.b_q(), w2.b_kv(), w2.b_o())
+        assert O.max_rel_err(yp[r:r + w2.n[i]], Y, H) <= TOL_BF16, ("prefill", i)
+        kv_ref.append((K, V))
+        r += w2.n[i]
+    # a decode over the caches prefill wrote (packed KV units hold W_KV x + b; hidden units hold x)
+    out, _ = T.decode(pool2, w2, T.queries(w2))
+    for i in range(len(w2.n)):
+        ref, _ = O.attend(w2.q(i).double().numpy(), *kv_ref[i], H, w2.scale, n_kv_heads=Hk)
+        assert O.max_rel_err(out[i][None], ref[None], H) <= TOL_BF16, ("cache", i)
+
+
+def test_gqa_llama3_8b_full_size_sampled(hc):
+    """The bench's GQA workload (LLaMA-3-8B layer, 256 requests, long contexts, 50% hidden) in
+    the bench's launch configuration; every head of the longest hidden and longest KV request."""
+    w = C.by_name("llama3-8b")
+    pool = T.make_pool(w)
+    T.fill(pool, w)
+    out, lse = T.decode(pool, w, T.queries(w))
+    assert pool.last_decode_path() == 1 and np.isfinite(out).all()
+    hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    idx = [max(hid, key=lambda i: w.n[i]), max(kv, key=lambda i: w.n[i]), hid[0], kv[0]]
+    err, lerr = T.compare(w, out[idx], lse[idx], idx)
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+
+
+def test_gqa_refused_with_the_absorbed_variant(hc):
+    w = _bf16_workload(1024, 8, 128, 16, n=[3], Hk=2)
+    with pytest.raises(hc.HcError) as e:
+        T.make_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
+    assert e.value.status == hc.HC_E_UNSUPPORTED

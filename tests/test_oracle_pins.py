@@ -536,3 +536,33 @@ def test_gqa_matches_torch_sdpa_enable_gqa():
     o_h, _ = O.decode_batch([{"mode": 1, "q": q, "X": X}], W, H, 0.25, bb, n_kv_heads=Hk)
     assert np.allclose(o_kv[0], ref.reshape(-1).numpy(), rtol=0, atol=1e-12)
     assert np.allclose(o_h[0], o_kv[0], rtol=0, atol=1e-12)
+
+
+def test_gqa_layers_equal_multihead_layers_with_repeated_kv_weights():
+    """attention_layer / prefill_layer under GQA = the multi-head layers whose W_K, W_V (and
+    biases) repeat each K/V head's rows G times — for both cache modes, with RoPE."""
+    rs = np.random.default_rng(24)
+    H, Hk, dh, n = 4, 2, 8, 7
+    d, dk, G = H * dh, Hk * dh, H // Hk
+    Wq, Wo = rs.normal(size=(d, d)) / 6, rs.normal(size=(d, d)) / 6
+    Wkv, bkv = rs.normal(size=(2 * dk, d)) / 6, rs.normal(size=2 * dk) * 0.1
+    rep_rows = lambda M: np.repeat(M.reshape(Hk, dh, -1), G, axis=0).reshape(d, -1)
+    Wrep = np.concatenate([rep_rows(Wkv[:dk]), rep_rows(Wkv[dk:])])
+    brep = np.concatenate([rep_rows(bkv[:dk, None])[:, 0], rep_rows(bkv[dk:, None])[:, 0]])
+    X = rs.normal(size=(n, d))
+    for theta in (0.0, 10000.0):
+        for mode in (0, 1):
+            if mode == 1:
+                c1 = c2 = {"mode": 1, "X": X[:-1]}
+            else:
+                KV = X[:-1] @ Wkv.T + bkv
+                K = O.rope(KV[:, :dk], np.arange(n - 1), theta, Hk)
+                c1 = {"mode": 0, "K": K, "V": KV[:, dk:]}
+                c2 = {"mode": 0, "K": np.repeat(K.reshape(n - 1, Hk, dh), G, axis=1).reshape(n - 1, d),
+                      "V": np.repeat(KV[:, dk:].reshape(n - 1, Hk, dh), G, axis=1).reshape(n - 1, d)}
+            y1, _, l1, _ = O.attention_layer(X[-1], c1, Wq, Wkv, Wo, H, 0.3, b_KV=bkv, rope_theta=theta)
+            y2, _, l2, _ = O.attention_layer(X[-1], c2, Wq, Wrep, Wo, H, 0.3, b_KV=brep, rope_theta=theta)
+            assert np.allclose(y1, y2, rtol=0, atol=1e-12) and np.allclose(l1, l2, rtol=0, atol=1e-12)
+        Y1, _, _ = O.prefill_layer(X, Wq, Wkv, Wo, H, 0.3, b_KV=bkv, rope_theta=theta)
+        Y2, _, _ = O.prefill_layer(X, Wq, Wrep, Wo, H, 0.3, b_KV=brep, rope_theta=theta)
+        assert np.allclose(Y1, Y2, rtol=0, atol=1e-12)
