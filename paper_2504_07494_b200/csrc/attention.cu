@@ -7,7 +7,10 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "attn_pipe.cuh"
+#include "attn_tc.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -18,6 +21,20 @@ namespace {
 using ap::FULL;
 using ap::warp_max;
 using ap::warp_sum;
+
+// Every task a KV-mode (split, K/V head): the tensor-core loop (attn_tc.cuh), NW warps per CTA.
+template <int DH, int NW, int NST>
+__global__ void __launch_bounds__(NW * 32, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv,
+                                                             const AttnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_tc[];
+  using C = at::TcCfg<DH, NST>;
+  const uint32_t base_u32 = ptx::smem_u32(smem_tc);
+  uint8_t* smem = smem_tc + ((1024 - (base_u32 & 1023)) & 1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ap::DirectTaskMap tm{p.n_tasks, p.th};
+  at::attn_warp_run_tc<DH, NST>(p, &tmap_kv, smem + warp * C::STAGES_BYTES,
+                                smem + NW * C::STAGES_BYTES + warp * C::CTRL_BYTES, lane, tm);
+}
 
 template <int DH, int NW, int NST>
 __global__ void __launch_bounds__(NW * 32, 1) attn_pipe_kernel(const AttnParams p) {
@@ -131,9 +148,30 @@ cudaError_t launch_pipe(const AttnParams& p, int num_sms, cudaStream_t s) {
 bool attn_pipe_supported(int dtype, int dh, int B) {
   return dtype == 0 && (dh == 128 || dh == 64) && B % 16 == 0;
 }
+bool attn_tc_supported(int dtype, int dh, int G, int Bkv) {
+  return dtype == 0 && (dh == 128 || dh == 64) && G >= 1 && G <= 8 && Bkv % 16 == 0;
+}
 
-cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s) {
+template <int DH, int NW, int NST>
+static cudaError_t launch_tc(const AttnParams& p, const void* tmap, int num_sms, cudaStream_t s) {
+  using C = at::TcCfg<DH, NST>;
+  constexpr int smem = 1024 + NW * (C::STAGES_BYTES + C::CTRL_BYTES);
+  auto k = attn_tc_kernel<DH, NW, NST>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int max_ctas = (p.n_tasks + NW - 1) / NW;
+  const int grid = max_ctas < num_sms ? max_ctas : num_sms;
+  k<<<grid, NW * 32, smem, s>>>(*static_cast<const CUtensorMap*>(tmap), p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s,
+                        const void* tmap_kv) {
   if (p.n_tasks <= 0) return cudaSuccess;
+  if (p.tc) {   // every task a KV-mode split: tensor-core loop (the runtime checked attn_tc_supported)
+    if (p.dh == 128) return launch_tc<128, 8, 3>(p, tmap_kv, num_sms, s);
+    return launch_tc<64, 8, 5>(p, tmap_kv, num_sms, s);
+  }
   if (!generic && attn_pipe_supported(dtype, p.dh, p.B)) {
     const int cfg = t.attn_cfg;
     if (p.dh == 128) {

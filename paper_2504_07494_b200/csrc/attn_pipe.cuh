@@ -10,7 +10,11 @@
 // Lane 0 issues 1-D bulk copies (TMA engine) of a 16-token K chunk and V chunk (4 KiB each
 // at dh=128: a head's rows of a block are contiguous) into shared memory; all lanes
 // compute from shared memory: each lane dots 8 dims of a row (128-bit LDS), a butterfly
-// transpose-reduce leaves one complete score per lane pair.
+// transpose-reduce leaves one complete score per lane pair.  The products run as
+// mixed-precision FMAs (fma.rn.f32.bf16 = FHFMA: bf16 x bf16, fp32 accumulate) straight
+// on the stored bf16 words, so no element is converted: q.k is exact per product as before,
+// and Σ p v takes p rounded once to bf16 (l sums the same rounded p, so the weights stay
+// normalised).  One instruction per element instead of a convert + an FMA.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -37,6 +41,26 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// a0 += q.lo * k.lo, a1 += q.hi * k.hi (bf16 products, fp32 accumulation; FHFMA.BF16)
+__device__ __forceinline__ void dot2_bf16(float& a0, float& a1, uint32_t q, uint32_t k) {
+  asm("{\n .reg .b16 ql, qh, kl, kh;\n mov.b32 {ql, qh}, %2;\n mov.b32 {kl, kh}, %3;\n"
+      " fma.rn.f32.bf16 %0, ql, kl, %0;\n fma.rn.f32.bf16 %1, qh, kh, %1;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(q), "r"(k));
+}
+// a0 += p * v.lo, a1 += p * v.hi (p a bf16 scalar)
+__device__ __forceinline__ void axpy2_bf16(float& a0, float& a1, uint16_t p, uint32_t v) {
+  asm("{\n .reg .b16 vl, vh;\n mov.b32 {vl, vh}, %3;\n"
+      " fma.rn.f32.bf16 %0, %2, vl, %0;\n fma.rn.f32.bf16 %1, %2, vh, %1;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "h"(p), "r"(v));
+}
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+  __nv_bfloat16 b = __float2bfloat16_rn(x);
+  return *reinterpret_cast<uint16_t*>(&b);
+}
+__device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+
 __device__ __forceinline__ void bf16x4_to_f32(uint2 u, float (&f)[4]) {
   f[0] = __uint_as_float(u.x << 16);
   f[1] = __uint_as_float(u.x & 0xffff0000u);
@@ -174,8 +198,11 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     if (lane == 0) {
       const __nv_bfloat16 *ksrc, *vsrc;
       if (prq.mode == 0) {
-        const int kb = p.tables[prq.tab_off + 2 * lb];
-        const int vb = p.tables[prq.tab_off + 2 * lb + 1];
+        int kb = p.tables[prq.tab_off + 2 * lb];
+        int vb = p.tables[prq.tab_off + 2 * lb + 1];
+#ifdef HC_DIAG
+        if (p.diag == 2) kb = vb = 0;   // timing diagnostic: every chunk from one L2-resident block
+#endif
         ksrc = pool + (size_t)kb * blk_elems + hk * kv_head_elems + (size_t)row * DH;
         vsrc = pool + (size_t)vb * blk_elems + p.v_off + hk * kv_head_elems + (size_t)row * DH;
       } else {
@@ -219,9 +246,11 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
 
   const int lr = lane % LPR;   // this lane's 16-byte column slot (dims 8*lr .. 8*lr+7)
   const int lg = lane / LPR;   // this lane's row group
-  float qf[8], acc[8];
+  uint16_t* pbuf16 = reinterpret_cast<uint16_t*>(pbuf);
+  uint4 qw = make_uint4(0, 0, 0, 0);   // this lane's 8 dims of q_h, bf16 as stored
+  float acc[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) qf[i] = acc[i] = 0.f;
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
   float m_run = -INFINITY, l_lane = 0.f;   // l kept per lane (rows this lane owns), reduced per task
   int cstage = 0;
   uint32_t cphase = 0;
@@ -231,16 +260,26 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     const int4 mt = meta[cstage];
     ptx::mbar_wait(&bars[cstage], cphase);
     const uint8_t* sb = stage_base + cstage * C::STAGE;
-    if (mt.w & 1) {  // first chunk of a task: fresh state, load q_h (pre-scaled by scale*log2 e)
-      if constexpr (QREG)
-        bf16x8_to_f32(cstage == 0 ? qr0 : (cstage == 1 ? qr1 : qr2), qf);
-      else
-        bf16x8_to_f32(reinterpret_cast<const uint4*>(sb + 2 * C::CHUNK)[lr], qf);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        qf[i] *= p.scale_log2;
-        acc[i] = 0.f;
+#ifdef HC_DIAG
+    if (p.diag == 1) {   // timing diagnostic: stream the chunks, skip the math (wrong outputs)
+      __syncwarp();
+      --in_flight;
+      if (produce(cstage)) ++in_flight;
+      __syncwarp();
+      if (++cstage == NST) {
+        cstage = 0;
+        cphase ^= 1u;
       }
+      continue;
+    }
+#endif
+    if (mt.w & 1) {  // first chunk of a task: fresh state, load q_h (bf16 words as stored)
+      if constexpr (QREG)
+        qw = cstage == 0 ? qr0 : (cstage == 1 ? qr1 : qr2);
+      else
+        qw = reinterpret_cast<const uint4*>(sb + 2 * C::CHUNK)[lr];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
       m_run = -INFINITY;
       l_lane = 0.f;
     }
@@ -249,27 +288,25 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     float part[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      float kf[8];
-      bf16x8_to_f32(ks[(i * RPI + lg) * LPR + lr], kf);
-      float a0 = qf[0] * kf[0], a1 = qf[1] * kf[1];
-      a0 = fmaf(qf[2], kf[2], a0);
-      a1 = fmaf(qf[3], kf[3], a1);
-      a0 = fmaf(qf[4], kf[4], a0);
-      a1 = fmaf(qf[5], kf[5], a1);
-      a0 = fmaf(qf[6], kf[6], a0);
-      a1 = fmaf(qf[7], kf[7], a1);
+      const uint4 kw = ks[(i * RPI + lg) * LPR + lr];
+      float a0 = 0.f, a1 = 0.f;
+      dot2_bf16(a0, a1, qw.x, kw.x);
+      dot2_bf16(a0, a1, qw.y, kw.y);
+      dot2_bf16(a0, a1, qw.z, kw.z);
+      dot2_bf16(a0, a1, qw.w, kw.w);
       part[i] = a0 + a1;
     }
     int idx = 0;
     Bfly<NV, LPR / 2>::run(part, lane, idx);
     const int row = idx * RPI + lg;
     const bool valid = row < mt.z;
-    const float s = valid ? part[0] : -INFINITY;
+    const float s = valid ? part[0] * p.scale_log2 : -INFINITY;
     const float m_new = fmaxf(m_run, warp_max(s));
-    const float pj = valid ? fast_exp2(s - m_new) : 0.f;
+    const uint16_t pj16 = bf16_bits(valid ? fast_exp2(s - m_new) : 0.f);   // the weight Σ p v uses
+    const float pj = bf16_val(pj16);
     const float alpha = fast_exp2(m_run - m_new);   // 0 when m_run = -inf
     if ((lane & 1) == 0) {
-      pbuf[row] = pj;
+      pbuf16[row] = pj16;
       l_lane = l_lane * alpha + pj;
     } else {
       l_lane *= alpha;
@@ -283,11 +320,12 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int r = i * RPI + lg;
-      float vf[8];
-      bf16x8_to_f32(vs[r * LPR + lr], vf);
-      const float pr = pbuf[r];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = fmaf(pr, vf[c], acc[c]);
+      const uint4 vw = vs[r * LPR + lr];
+      const uint16_t pr = pbuf16[r];
+      axpy2_bf16(acc[0], acc[1], pr, vw.x);
+      axpy2_bf16(acc[2], acc[3], pr, vw.y);
+      axpy2_bf16(acc[4], acc[5], pr, vw.z);
+      axpy2_bf16(acc[6], acc[7], pr, vw.w);
     }
     if (mt.w & 2) {  // last chunk of the task: emit the partial (m, l, acc)
       float a[8];

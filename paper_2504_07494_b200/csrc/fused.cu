@@ -16,12 +16,25 @@
 #include <cstdlib>
 
 #include "attn_pipe.cuh"
+#include "attn_tc.cuh"
 #include "internal.h"
 #include "pair_gemm.cuh"
 #include "ptx.cuh"
 
 namespace hc {
 namespace {
+
+#ifdef HC_TIMELINE
+// Diagnostic build only: per-CTA globaltimer stamps of the last fused launch —
+// [0] start, [1] GEMM warps drained, [2] last attention warp done, [3] attention tasks taken
+// (global counter) when this CTA's GEMM drained, [4] first attention warp done.
+__device__ unsigned long long g_timeline[512][5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 constexpr int kNsub = 2;
 constexpr bool kLateJoin = true;
@@ -30,7 +43,7 @@ using PC = pg::PairCfg<kNsub, 3>;   // default GEMM ring (3 x 48 KiB); tile geom
 struct FusedTaskMap {
   const AttnParams* p;
   __device__ __forceinline__ void map(int t, int& split, int& head) const {
-    const int H = p->H;
+    const int H = p->th;   // heads per split in the task numbering (Hk for the tensor-core loop)
     if (t < p->n_kv_tasks) {
       const int ks = t / H;
       split = p->kv_split_ids[ks];
@@ -69,28 +82,56 @@ struct FusedTaskMap {
   }
 };
 
-template <int GS, int NA, int NSTA, bool QR>
+// Shared-memory plan of the attention part: TC = the tensor-core KV loop (attn_tc.cuh), whose
+// stages must be 1024-aligned (128-B swizzle atoms) with the per-warp control words apart.
+template <int GS, int NA, int NSTA, bool QR, bool TC>
+struct FusedSmem {
+  using PC = pg::PairCfg<kNsub, GS>;
+  using TCC = at::TcCfg<128, NSTA>;
+  using TCJ = at::TcCfg<128, 2>;   // joiners: 2-stage rings in the freed GEMM stage buffers
+  static constexpr int kJoinBytes = TC ? TCJ::STAGES_BYTES : ap::PipeCfg<128, 2, QR>::WARP_BYTES;
+  static constexpr int kJoin = (GS * PC::STAGE_BYTES / kJoinBytes) < 6 ? (GS * PC::STAGE_BYTES / kJoinBytes) : 6;
+  static constexpr int ATTN_OFF = TC ? (PC::REGION_BYTES + 1023) / 1024 * 1024 : PC::REGION_BYTES;
+  static constexpr int WARP_BYTES = TC ? TCC::STAGES_BYTES : ap::PipeCfg<128, NSTA, QR>::WARP_BYTES;
+  static constexpr int CTRL_OFF = ATTN_OFF + NA * WARP_BYTES;
+  static constexpr int TOTAL = CTRL_OFF + (TC ? (NA + 6) * TCC::CTRL_BYTES : 0);
+};
+
+template <int GS, int NA, int NSTA, bool QR, bool TC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * NA, 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                      const pg::TcArgs a, const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tmap_kv, const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
-  using PC = pg::PairCfg<kNsub, GS>;
-  // late-joining GEMM warps: as many 2-stage attention rings as fit in the GEMM stage buffers
-  constexpr int kJoin = (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2, QR>::WARP_BYTES) < 6
-                            ? (GS * PC::STAGE_BYTES / ap::PipeCfg<128, 2, QR>::WARP_BYTES) : 6;
+  using FS = FusedSmem<GS, NA, NSTA, QR, TC>;
+  constexpr int kJoin = FS::kJoin;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
   const pg::PairSmem ps = pg::pair_carve<kNsub, kGemmStages>(smem);
-  uint8_t* attn_base = smem + PC::REGION_BYTES;
+  uint8_t* attn_base = smem + FS::ATTN_OFF;
+  uint8_t* ctrl_base = smem + FS::CTRL_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pg::pair_setup<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *ps.tmem_slot;
+#ifdef HC_TIMELINE
+  if (threadIdx.x == 0) {
+    g_timeline[blockIdx.x][0] = gtimer();
+    g_timeline[blockIdx.x][2] = 0;
+    g_timeline[blockIdx.x][4] = ~0ull;
+  }
+#endif
   if (warp < pg::GEMM_THREADS / 32) {
     pg::pair_roles<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+#ifdef HC_TIMELINE
+    asm volatile("bar.sync 1, %0;" ::"n"(pg::GEMM_THREADS) : "memory");
+    if (threadIdx.x == 0) {
+      g_timeline[blockIdx.x][1] = gtimer();
+      g_timeline[blockIdx.x][3] = (unsigned long long)*(volatile int32_t*)p.task_counter;
+    }
+#endif
     if (p.n_tasks > 0 && kLateJoin) {
       // This CTA's GEMM has drained (the epilogue consumed the last tile, so the leader's
       // UMMAs no longer read these stages): its 6 warps join the attention pool, each with a
@@ -99,14 +140,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
       ptx::fence_proxy_async_smem();
       if (warp < kJoin) {
         const FusedTaskMap tm{&p};
-        ap::attn_warp_run<128, 2, FusedTaskMap, QR>(p, ps.stages + warp * ap::PipeCfg<128, 2, QR>::WARP_BYTES,
-                                                    lane, tm);
+        if constexpr (TC)
+          at::attn_warp_run_tc<128, 2>(p, &tmap_kv, ps.stages + warp * FS::kJoinBytes,
+                                       ctrl_base + (NA + warp) * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm);
+        else
+          ap::attn_warp_run<128, 2, FusedTaskMap, QR>(p, ps.stages + warp * FS::kJoinBytes, lane, tm);
       }
     }
   } else {
     const FusedTaskMap tm{&p};
-    ap::attn_warp_run<128, NSTA, FusedTaskMap, QR>(
-        p, attn_base + (warp - pg::GEMM_THREADS / 32) * ap::PipeCfg<128, NSTA, QR>::WARP_BYTES, lane, tm);
+    const int aw = warp - pg::GEMM_THREADS / 32;
+    if constexpr (TC)
+      at::attn_warp_run_tc<128, NSTA>(p, &tmap_kv, attn_base + aw * FS::WARP_BYTES,
+                                      ctrl_base + aw * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm);
+    else
+      ap::attn_warp_run<128, NSTA, FusedTaskMap, QR>(p, attn_base + aw * FS::WARP_BYTES, lane, tm);
+#ifdef HC_TIMELINE
+    if (lane == 0) {
+      const unsigned long long t = gtimer();
+      atomicMax(&g_timeline[blockIdx.x][2], t);
+      atomicMin(&g_timeline[blockIdx.x][4], t);
+    }
+#endif
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -114,18 +169,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   pg::pair_teardown<kNsub, kGemmStages>(warp, tmem_base);
 }
 
-template <int GS, int NA, int NSTA, bool QR = false>
-cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, int num_sms,
-                       cudaStream_t s) {
-  constexpr int smem = 1024 + pg::PairCfg<kNsub, GS>::REGION_BYTES + NA * ap::PipeCfg<128, NSTA, QR>::WARP_BYTES;
+template <int GS, int NA, int NSTA, bool QR, bool TC>
+cudaError_t launch_cfg1(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
+                        int num_sms, cudaStream_t s) {
+  constexpr int smem = 1024 + FusedSmem<GS, NA, NSTA, QR, TC>::TOTAL;
   static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
-  auto k = fused_step_kernel<GS, NA, NSTA, QR>;
+  auto k = fused_step_kernel<GS, NA, NSTA, QR, TC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
   k<<<2 * pairs, pg::GEMM_THREADS + 32 * NA, smem, s>>>(*static_cast<const CUtensorMap*>(tmx),
-                                                        *static_cast<const CUtensorMap*>(tmw), a, p);
+                                                        *static_cast<const CUtensorMap*>(tmw),
+                                                        *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx), a, p);
   return cudaGetLastError();
+}
+template <int GS, int NA, int NSTA, bool QR = false>
+cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
+                       int num_sms, cudaStream_t s) {
+  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true>(a, p, tmx, tmw, tmkv, num_sms, s);
+  return launch_cfg1<GS, NA, NSTA, QR, false>(a, p, tmx, tmw, tmkv, num_sms, s);
 }
 
 }  // namespace
@@ -138,7 +200,7 @@ int fused_tile_m() { return pg::P_BM; }
 int fused_tile_n() { return PC::TILE_N; }
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
-                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s) {
+                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv) {
   pg::TcArgs a{};
   a.gather = rp.gather;
   a.n_hblocks = rp.n_hblocks;
@@ -198,13 +260,21 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   const double t_gemm = 4.0 * rp.d * (double)rp.dk * a.M / 1.3e15;
   const double t_kv = (double)rp.kv_tokens * 4.0 * rp.dk / 6.5e12;
   const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 282 : 352);
-  if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  if (cfg == 342) return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  if (cfg == 3420) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
-  return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, num_sms, s);
+  if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 342) return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 3420) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
 }
 
 }  // namespace hc
+
+#ifdef HC_TIMELINE
+// Diagnostic build only (not in hc.h): copy the per-CTA stamps of the last fused launch.
+extern "C" int hc_debug_timeline(unsigned long long* host, int n_ctas) {
+  if (n_ctas > 512) n_ctas = 512;
+  return (int)cudaMemcpyFromSymbol(host, hc::g_timeline, sizeof(unsigned long long) * 5 * n_ctas);
+}
+#endif

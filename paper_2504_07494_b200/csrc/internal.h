@@ -22,6 +22,7 @@ struct Tuning {
   int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM
   int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
   int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
+  int attn_tc = 1;       // HC_ATTN_TC: KV attention on mma.sync (attn_tc.cuh): 0 never, 1 GQA only, 2 always
   int tc_1sm = 0;        // HC_TC_1SM: 1-SM tcgen05 reconstruction kernel instead of CTA pairs
   int tc_nsub = 0;       // HC_TC_NSUB: 1 = 256-wide pair tiles
   int tc_stages = 4;     // HC_TC_STAGES (3 or 4)
@@ -33,6 +34,7 @@ struct Tuning {
   int qt_bn = 128;       // HC_QT_BN (absorbed variant)
   int diag_epi = 0;      // -DHC_DIAG builds only: HC_DIAG_EPI (wrong outputs, timing only)
   int diag_box = 0;      // -DHC_DIAG builds only: HC_DIAG_BOX (wrong outputs, timing only)
+  int diag_attn = 0;     // -DHC_DIAG builds only: HC_DIAG_ATTN (wrong outputs, timing only)
 };
 
 // Per-request entry of the decode-call descriptor (uploaded once per call).
@@ -83,6 +85,9 @@ struct AttnParams {
   const int32_t* tile_done;      // [gemm_m_tiles][gemm_n_tiles] finished epilogue warps (8 = ready)
   int32_t gemm_n_tiles, gemm_tile_m, gemm_tile_n;
   int32_t kv_evict_first;        // 1: KV chunks are streamed with an L2 evict-first policy
+  int32_t th;                    // heads per split in the task numbering: H (SIMT loop) or Hk (tensor-core loop)
+  int32_t tc;                    // 1: every task is a KV-mode split and runs attn_tc.cuh (task = split * Hk + kvhead)
+  int32_t diag;                  // -DHC_DIAG builds only (HC_DIAG_ATTN): 1 skip the math, 2 read block 0 only
 };
 
 struct CombineParams {
@@ -176,7 +181,10 @@ bool dense_tc_supported(int d);
 // tmap_a: A with {64 x 128} boxes; tmap_w: W with {64 x 128} boxes
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s);
 cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s);
-cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s);
+cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s,
+                        const void* tmap_kv = nullptr);
+// tensor-core KV attention (attn_tc.cuh) serves this shape: bf16, dh 64/128, G <= 8, Bkv % 16 == 0
+bool attn_tc_supported(int dtype, int dh, int G, int Bkv);
 bool attn_pipe_supported(int dtype, int dh, int B);
 // Fused step: reconstruction GEMM (CTA pairs, 256x512 tiles) and split-K attention warps in
 // one persistent kernel; hidden tasks wait on per-tile completion counters.
@@ -184,7 +192,8 @@ bool fused_supported(int d, int dk, int dh, int B);
 int fused_tile_m();
 int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
-                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s);
+                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s,
+                         const void* tmap_kv = nullptr);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
                          void* out, float* lse, cudaStream_t s);

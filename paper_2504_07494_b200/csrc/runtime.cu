@@ -179,6 +179,7 @@ Tuning tuning_from_env() {
   t.group_m = env_int("HC_GROUP_M", t.group_m);
   t.l2_hint = env_int("HC_L2HINT", t.l2_hint);
   t.kv_evict_first = env_int("HC_KV_EF", t.kv_evict_first);
+  t.attn_tc = env_int("HC_ATTN_TC", t.attn_tc);
   t.tc_1sm = env_int("HC_TC_1SM", t.tc_1sm);
   t.tc_nsub = env_int("HC_TC_NSUB", t.tc_nsub);
   t.tc_stages = env_int("HC_TC_STAGES", t.tc_stages);
@@ -191,6 +192,7 @@ Tuning tuning_from_env() {
 #ifdef HC_DIAG
   t.diag_epi = env_int("HC_DIAG_EPI", 0);
   t.diag_box = env_int("HC_DIAG_BOX", 0);
+  t.diag_attn = env_int("HC_DIAG_ATTN", 0);
 #endif
   return t;
 }
@@ -223,6 +225,7 @@ struct Plan {
   bool fused = false;                 // reconstruction + attention in one kernel (fused.cu)
   bool absorb = false;                // hidden requests through absorbed.cu (f4 (ii)), no splits
   bool attend = false;                // fused reconstruct-and-attend epilogue (no K/V scratch)
+  bool tc = false;                    // every attention task is a KV-mode split: tensor-core loop (attn_tc.cuh)
   int32_t seg = 0;                    // attend: tokens per hidden partial (min(B, 32))
   size_t off_hreqblk = 0;             // attend: batch index of each hidden block's request
   int32_t n_h = 0, n_atiles = 0, Hp = 0;
@@ -250,6 +253,8 @@ struct hc_pool {
   CUtensorMap tmap_x{}, tmap_w{}, tmap_w_half{};
   CUtensorMap tmap_wqkv{}, tmap_wo{};   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
   CUtensorMap tmap_x64{};               // pool rows, {64 x min(B,64)} boxes (absorbed Z GEMM)
+  CUtensorMap tmap_kv{};                // pool as rows of dh elements, {64 x 16} boxes, 128-B swizzle (KV chunks)
+  bool attn_tc_ok = false;              // tmap_kv built and attn_tc_supported
   bool tc_ok = false;
   bool dense_tc_ok = false;             // bf16 tcgen05 path for the current-token / output GEMMs
   int num_sms = 148;
@@ -387,6 +392,11 @@ struct hc_pool {
       }
     }
     P.Hp = (int32_t)align_up((size_t)H, 16);
+    // Tensor-core KV loop: for GQA groups by default (one task reads a K/V head once for its G
+    // query heads); for multi-head its mma.sync compete with the fused GEMM's tcgen05 work for the
+    // tensor pipe (same-box A/B: 1/64 -4%, 1/32 -2%), so the FHFMA SIMT loop stays the default.
+    P.tc = attn_tc_ok && !(cfg.flags & HC_FLAG_GENERIC_ATTN) && (P.attend || P.absorb || P.n_hb == 0) &&
+           (tune.attn_tc == 2 || (tune.attn_tc == 1 && kv.Hk < H));
     P.fused = !P.absorb && tc_ok && P.n_hb > 0 && tune.fused != 0 && !(cfg.flags & HC_FLAG_GENERIC_ATTN) &&
               fused_supported(cfg.d_model, kv.dk, cfg.head_dim, B);
     if (P.fused) {
@@ -598,6 +608,13 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed");
       }
       p->tc_ok = true;
+    }
+    if (attn_tc_supported(cfg->dtype, cfg->head_dim, cfg->n_heads / kg.Hk, kg.Bkv) &&
+        !(cfg->flags & HC_FLAG_FORCE_SIMT)) {
+      // the pool viewed as rows of dh elements: a K (V) chunk of 16 tokens of one K/V head is
+      // 16 consecutive rows (KV layout [Hk][Bkv][dh] per K / V region)
+      p->attn_tc_ok = make_tmap_2d(&p->tmap_kv, p->storage + L.blocks_off, (uint64_t)cfg->head_dim,
+                                   (uint64_t)cfg->num_blocks * cfg->block_size * cfg->d_model / cfg->head_dim, 64, 16);
     }
   }
   *out = p;
@@ -1004,7 +1021,9 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.part_acc = reinterpret_cast<float*>(ws + P.off_acc);
   ap.n_splits_all = P.n_splits;
   ap.task_counter = reinterpret_cast<int32_t*>(ws);
-  ap.n_tasks = (P.attend ? P.n_kv_splits : P.n_splits) * H;   // attend: hidden partials come from the GEMM
+  ap.th = P.tc ? pool->kv.Hk : H;   // tensor-core loop: one task per (split, K/V head) serves its G query heads
+  ap.tc = P.tc ? 1 : 0;
+  ap.n_tasks = (P.attend ? P.n_kv_splits : P.n_splits) * ap.th;   // attend: hidden partials come from the GEMM
   ap.H = H;
   ap.dh = pool->cfg.head_dim;
   ap.B = B;
@@ -1015,6 +1034,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.v_off = pool->kv.v_off;
   ap.scale_log2 = scale * 1.4426950408889634f;
   ap.kv_evict_first = pool->tune.kv_evict_first;
+  ap.diag = pool->tune.diag_attn;
   pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
   if (P.absorb) {
     // f4 (ii): hidden requests never rebuild K/V; KV requests take the split-K path
@@ -1063,7 +1083,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     }
     if (pool->profiling) cudaEventRecord(ev[2], s);
     if (P.n_splits > 0) {
-      err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s);
+      err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s,
+                      &pool->tmap_kv);
       if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
       ++launches;
     }
@@ -1071,10 +1092,10 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   } else if (P.fused) {
     ap.kv_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_kvsplit);
     ap.hid_split_ids = reinterpret_cast<const int32_t*>(ws + P.off_hidsplit);
-    ap.n_kv_tasks = P.n_kv_splits * H;
+    ap.n_kv_tasks = P.n_kv_splits * ap.th;
     ap.n_hid_splits = P.n_hid_splits;
     err = launch_fused(rp, ap, &pool->tmap_x, &pool->tmap_w_half, reinterpret_cast<int32_t*>(ws + P.off_tiledone),
-                       pool->num_sms, pool->tune, s);
+                       pool->num_sms, pool->tune, s, &pool->tmap_kv);
     if (err != cudaSuccess) return cuda_fail(err, "fused step kernel");
     ++launches;
     if (pool->profiling) {
@@ -1089,7 +1110,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
       ++launches;
     }
     if (pool->profiling) cudaEventRecord(ev[2], s);
-    err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s);
+    err = launch_attn(ap, pool->cfg.dtype, (pool->cfg.flags & HC_FLAG_GENERIC_ATTN) != 0, pool->num_sms, pool->tune, s,
+                      &pool->tmap_kv);
     if (err != cudaSuccess) return cuda_fail(err, "attention kernel");
     ++launches;
     if (pool->profiling) cudaEventRecord(ev[3], s);

@@ -900,7 +900,8 @@ def test_gqa_decode_vs_oracle(hc, d, H, dh, B, Hk):
         assert units == want, (i, units, want)
 
 
-@pytest.mark.parametrize("env", [{"HC_FUSED": "0"}, {"HC_EPI_ATTEND": "0"}, {"HC_EPI_ATTEND": "0", "HC_FUSED": "0"}])
+@pytest.mark.parametrize("env", [{"HC_FUSED": "0"}, {"HC_EPI_ATTEND": "0"}, {"HC_EPI_ATTEND": "0", "HC_FUSED": "0"},
+                                 {"HC_ATTN_TC": "0"}, {"HC_ATTN_TC": "0", "HC_FUSED": "0"}])
 def test_gqa_alternative_paths(hc, monkeypatch, env):
     """GQA through the two-kernel path, the fused kernel with K/V scratch ([hblock][Hk][B][dh]),
     and the stand-alone GEMM + attention kernel, at the LLaMA-3-8B head layout."""
@@ -983,3 +984,22 @@ def test_gqa_refused_with_the_absorbed_variant(hc):
     with pytest.raises(hc.HcError) as e:
         T.make_pool(w, flags=hc.HC_FLAG_ABSORB_HIDDEN)
     assert e.value.status == hc.HC_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("shape", [(512, 4, 128, 16), (512, 8, 64, 32), (9216, 72, 128, 16)])
+def test_tensor_core_kv_loop_on_multihead(hc, monkeypatch, shape):
+    """HC_ATTN_TC=2: the mma.sync KV loop (attn_tc.cuh) also for multi-head pools — fused
+    (attend epilogue + KV warps), KV-only batches (stand-alone kernel) and peaky scores; it
+    meets the same bar as the FHFMA SIMT loop."""
+    monkeypatch.setenv("HC_ATTN_TC", "2")
+    d, H, dh, B = shape
+    n = [1, 17, 300, 129, 64, 511, 2049]
+    w = _bf16_workload(d, H, dh, B, n=n, bias=True)
+    _, out, lse = _run(w)
+    err, lerr = T.compare(w, out, lse, range(len(n)), {i: [0, H - 1] for i in range(len(n)) if w.modes[i]} if d > 4096 else None)
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+    wk = _bf16_workload(d, H, dh, B, n=n, modes=[MODE_KV] * len(n), seed=5)
+    w4 = Workload(wk.name, wk.shape, B, "bf16", 5, n, [MODE_KV] * len(n), list(range(len(n))), False, q_scale=4.0)
+    _, out, lse = _run(w4)
+    err, lerr = T.compare(w4, out, lse, range(len(n)))
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
