@@ -36,9 +36,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-constexpr int kNsub = 2;
+constexpr int kNsubMax = 2;
 constexpr bool kLateJoin = true;
-using PC = pg::PairCfg<kNsub, 3>;   // default GEMM ring (3 x 48 KiB); tile geometry is stage-independent
+using PC = pg::PairCfg<kNsubMax, 3>;   // widest tile (256 x 512); NSUB = 1 runs 256 x 256 tiles
 
 struct FusedTaskMap {
   const AttnParams* p;
@@ -84,9 +84,9 @@ struct FusedTaskMap {
 
 // Shared-memory plan of the attention part: TC = the tensor-core KV loop (attn_tc.cuh), whose
 // stages must be 1024-aligned (128-B swizzle atoms) with the per-warp control words apart.
-template <int GS, int NA, int NSTA, bool QR, bool TC>
+template <int GS, int NA, int NSTA, bool QR, bool TC, int NS>
 struct FusedSmem {
-  using PC = pg::PairCfg<kNsub, GS>;
+  using PC = pg::PairCfg<NS, GS>;
   using TCC = at::TcCfg<128, NSTA>;
   using TCJ = at::TcCfg<128, 2>;   // joiners: 2-stage rings in the freed GEMM stage buffers
   static constexpr int kJoinBytes = TC ? TCJ::STAGES_BYTES : ap::PipeCfg<128, 2, QR>::WARP_BYTES;
@@ -97,21 +97,21 @@ struct FusedSmem {
   static constexpr int TOTAL = CTRL_OFF + (TC ? (NA + 6) * TCC::CTRL_BYTES : 0);
 };
 
-template <int GS, int NA, int NSTA, bool QR, bool TC>
+template <int GS, int NA, int NSTA, bool QR, bool TC, int NS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * NA, 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                       const __grid_constant__ CUtensorMap tmap_kv, const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
-  using FS = FusedSmem<GS, NA, NSTA, QR, TC>;
+  using FS = FusedSmem<GS, NA, NSTA, QR, TC, NS>;
   constexpr int kJoin = FS::kJoin;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-  const pg::PairSmem ps = pg::pair_carve<kNsub, kGemmStages>(smem);
+  const pg::PairSmem ps = pg::pair_carve<NS, kGemmStages>(smem);
   uint8_t* attn_base = smem + FS::ATTN_OFF;
   uint8_t* ctrl_base = smem + FS::CTRL_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pg::pair_setup<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w);
+  pg::pair_setup<NS, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -124,7 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   }
 #endif
   if (warp < pg::GEMM_THREADS / 32) {
-    pg::pair_roles<kNsub, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+    pg::pair_roles<NS, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
 #ifdef HC_TIMELINE
     asm volatile("bar.sync 1, %0;" ::"n"(pg::GEMM_THREADS) : "memory");
     if (threadIdx.x == 0) {
@@ -166,15 +166,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  pg::pair_teardown<kNsub, kGemmStages>(warp, tmem_base);
+  pg::pair_teardown<NS, kGemmStages>(warp, tmem_base);
 }
 
-template <int GS, int NA, int NSTA, bool QR, bool TC>
+template <int GS, int NA, int NSTA, bool QR, bool TC, int NS>
 cudaError_t launch_cfg1(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
                         int num_sms, cudaStream_t s) {
-  constexpr int smem = 1024 + FusedSmem<GS, NA, NSTA, QR, TC>::TOTAL;
+  constexpr int smem = 1024 + FusedSmem<GS, NA, NSTA, QR, TC, NS>::TOTAL;
   static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
-  auto k = fused_step_kernel<GS, NA, NSTA, QR, TC>;
+  auto k = fused_step_kernel<GS, NA, NSTA, QR, TC, NS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
@@ -183,21 +183,21 @@ cudaError_t launch_cfg1(const pg::TcArgs& a, const AttnParams& p, const void* tm
                                                         *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx), a, p);
   return cudaGetLastError();
 }
-template <int GS, int NA, int NSTA, bool QR = false>
+template <int GS, int NA, int NSTA, bool QR, int NS = 2>
 cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
                        int num_sms, cudaStream_t s) {
-  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true>(a, p, tmx, tmw, tmkv, num_sms, s);
-  return launch_cfg1<GS, NA, NSTA, QR, false>(a, p, tmx, tmw, tmkv, num_sms, s);
+  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true, NS>(a, p, tmx, tmw, tmkv, num_sms, s);
+  return launch_cfg1<GS, NA, NSTA, QR, false, NS>(a, p, tmx, tmw, tmkv, num_sms, s);
 }
 
 }  // namespace
 
 bool fused_supported(int d, int dk, int dh, int B) {
-  return dh == 128 && dk % dh == 0 && d % 64 == 0 && (2 * dk) % (256 * kNsub) == 0 && B % 16 == 0 &&
+  return dh == 128 && dk % dh == 0 && d % 64 == 0 && (2 * dk) % 256 == 0 && B % 16 == 0 &&
          B >= 16 && (B <= 128 || B % 256 == 0) && (B & (B - 1)) == 0;
 }
 int fused_tile_m() { return pg::P_BM; }
-int fused_tile_n() { return PC::TILE_N; }
+int fused_tile_n() { return 256; }   // the narrowest tile (NSUB = 1): sizes per-tile arrays for either
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv) {
@@ -208,7 +208,14 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.M = rp.n_hblocks * rp.B;
   a.rows_per_box = (rp.B < 128 && !t.diag_box) ? rp.B : 128;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
-  a.n_tiles = 2 * rp.dk / PC::TILE_N;
+  // Tile width: 256 x 512 pair tiles (NSUB = 2; one 512-column accumulator) whenever 2 dk is a
+  // multiple of 512; 256 x 256 tiles with two accumulators (NSUB = 1) otherwise.  Measured on
+  // GQA (where the attend epilogue serves G query heads per rebuilt K/V head) the second
+  // accumulator does not pay for the halved operand reuse: LLaMA-3-8B 3.26 vs 2.75 ms, cfg4
+  // 64.5 vs 40.9 ms.
+  const int nsub = t.fused_nsub ? t.fused_nsub : ((2 * rp.dk) % 512 != 0 ? 1 : 2);
+  const int tile_n = 256 * nsub;
+  a.n_tiles = 2 * rp.dk / tile_n;
   a.k_iters = rp.d / pg::BK;
   a.H = rp.Hk;
   a.grp = rp.H / rp.Hk;
@@ -247,7 +254,7 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   ap_.tile_done = tile_done;
   ap_.gemm_n_tiles = a.n_tiles;
   ap_.gemm_tile_m = pg::P_BM;
-  ap_.gemm_tile_n = PC::TILE_N;
+  ap_.gemm_tile_n = tile_n;
   // 3-stage GEMM ring + 5 attention warps x 2 stages with q_h in registers (the stages carry
   // only K and V chunks, which frees the smem for the fifth warp: more KV bytes in flight
   // next to the GEMM; crossover 1/64-1/32 -1.5..-7% on cool boxes, neutral elsewhere).
@@ -259,12 +266,13 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // (+15..+25%), so the default stays <3,5,2>.
   const double t_gemm = 4.0 * rp.d * (double)rp.dk * a.M / 1.3e15;
   const double t_kv = (double)rp.kv_tokens * 4.0 * rp.dk / 6.5e12;
+  if (nsub == 1) {   // 256 x 256 tiles: 32-KiB stages, 4 of them (the same bytes in flight as 3 x 48)
+    const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 382 : 452);
+    if (cfg == 382) return launch_cfg<3, 8, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+    return launch_cfg<4, 5, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  }
   const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 282 : 352);
-  if (cfg == 243) return launch_cfg<2, 4, 3>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 262) return launch_cfg<2, 6, 2>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 333) return launch_cfg<3, 3, 3>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 342) return launch_cfg<3, 4, 2>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 3420) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
 }

@@ -17,6 +17,7 @@ struct Tuning {
   int fused = -1;        // HC_FUSED: 0 = two-kernel path, else the fused step kernel when supported
   int epi_attend = 1;    // HC_EPI_ATTEND: 0 = rebuilt K/V into scratch + attention kernel
   int fused_cfg = 0;     // HC_FUSED_CFG: {GEMM stages, attention warps, stages} of the fused kernel; 0 = auto
+  int fused_nsub = 0;    // HC_FUSED_NSUB: fused GEMM tile 256 x 256*nsub (1 or 2); 0 = auto (1 for GQA)
   int group_n = 4;       // HC_GROUP_N: n-tiles per raster group of the fused kernel
   int sync_w = -1;       // HC_SYNC_W: partner k-lockstep window (-1: kernel default, 0 off)
   int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM

@@ -174,6 +174,7 @@ Tuning tuning_from_env() {
   t.fused = env_int("HC_FUSED", t.fused);
   t.epi_attend = env_int("HC_EPI_ATTEND", t.epi_attend);
   t.fused_cfg = env_int("HC_FUSED_CFG", t.fused_cfg);
+  t.fused_nsub = env_int("HC_FUSED_NSUB", t.fused_nsub);
   t.group_n = env_int("HC_GROUP_N", t.group_n);
   t.sync_w = env_int("HC_SYNC_W", t.sync_w);
   t.group_m = env_int("HC_GROUP_M", t.group_m);

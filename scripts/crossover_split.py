@@ -10,10 +10,10 @@ import torch  # noqa: E402
 
 from paper_2504_07494_b200 import hc  # noqa: E402
 from synth import configs as C  # noqa: E402
-from tests import hc_testlib as T  # noqa: E402
+from synth import drive as T  # noqa: E402
 
 
-def time_ids(pool, ids, q, w, steps=20, warmup=3):
+def time_ids(pool, ids, q, w, steps=int(os.environ.get("CS_STEPS", "20")), warmup=int(os.environ.get("CS_WARMUP", "3"))):
     out = torch.empty((len(ids), w.shape.d), dtype=w.torch_dtype, device="cuda")
     lse = torch.empty((len(ids), w.shape.H), dtype=torch.float32, device="cuda")
     qq = q[[w.req_ids.index(i) for i in ids]].contiguous()
