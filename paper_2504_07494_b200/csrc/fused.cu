@@ -229,7 +229,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   a.row_pos = rp.hblk_pos;
   // n-major raster, 4 n-tiles per group: four pairs of a wave share each A panel (same-box
   // A/B vs 2: cfg4 -2.5%, cfg5 1/32 -2..-4%)
-  a.group_m = -(t.group_n >= 1 ? t.group_n : 4);
+  // (HC_GROUP_N = -g: m-major groups of g m-tiles sweeping all n-tiles instead)
+  a.group_m = t.group_n <= -1 ? -t.group_n : -(t.group_n >= 1 ? t.group_n : 4);
   a.l2_hint = t.l2_hint;
   // Partner lockstep off by default in the fused kernel: with the attend epilogue, tiles of
   // partner pairs finish at different times and the spin costs more than the L2 reuse buys

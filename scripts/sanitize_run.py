@@ -41,5 +41,15 @@ for ln, rope in ((True, 0.0), (False, 10000.0)):
     y2, _ = pool.decode_layer(wl.req_ids, wl.modes, xt, wl.scale)
     torch.cuda.synchronize()
     print("layer ln", ln, "rope", rope, "finite", bool(torch.isfinite(y).all() and torch.isfinite(y2).all()), flush=True)
+# GQA (f4 (i)): fused kernel with the tensor-core KV loop, and the stand-alone tc attention kernel
+shg = LayerShape("san-gqa", 1024, 8, 128, 2)
+wg = Workload("san-gqa", shg, 16, "bf16", 8, n, [0, 1, 0, 1, 1, 0, 1], list(range(len(n))), True)
+run(wg)
+run(Workload("san-gqa-kv", shg, 16, "bf16", 9, n, [0] * len(n), list(range(len(n))), False))
+# tensor-core KV loop forced on a multi-head pool (knobs are read at pool create)
+os.environ["HC_ATTN_TC"] = "2"
+run(w)
+run(Workload("san-kv", shape, 16, "bf16", 10, n, [0] * len(n), list(range(len(n))), False))
+os.environ.pop("HC_ATTN_TC")
 torch.cuda.synchronize()
 print("done")
