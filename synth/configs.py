@@ -9,7 +9,7 @@ Recipe (DESIGN.md §"Input recipe"):
 * cfg2   — OPT-13B layer shape (d=5120, 40x128), 64 requests, ShareGPT-like snapshot,
            50% hidden by seeded permutation, bf16.
 * cfg3   — OPT-30B layer shape (d=7168, 56x128), 128 candidates, ShareGPT-like, beta from
-           the host greedy planner (synth.planner), bf16.
+           the native greedy planner (hc_schedule, via synth.planner), bf16.
 * cfg4   — OPT-66B layer shape (d=9216, 72x128), 256 requests, long contexts
            n = clip(round(exp(N(ln 1024, 0.75))), 32, 4096), 50% hidden, bf16.
 * cfg5   — cfg4 contexts with hidden fraction h in {0,1/64,...,1} as nested prefixes of

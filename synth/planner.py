@@ -1,14 +1,7 @@
-"""Host-side greedy cache-mode planner (bench-input generator for cfg3; NEXT-f2 in full).
-
-Follows PAPER.md §5: the value of scheduling request i is
-    g_i = p_i - beta_i * (|W|+|R|) * t_i,   t_i = rho * m_i          (Eq. 5-6)
-subject to  sum_i (1 - beta_i/2) m_i alpha_i <= M                    (Eq. 7)
-solved greedily by marginal gain per memory unit theta, with SPEC.md's
-tie-break and best-single comparison.  SURVEY.md §4.3 found that the paper's
-refinement ("if p/m < 2N rho, hidden usage is avoided") drops feasible positive-value
-hidden options; the best-single step here therefore also considers the hidden
-assignment (reading R9).  This module produces beta only; it is not on the
-GPU hot path and not an optimisation target (north_star).
+"""cfg3's cache-mode assignment: the request mix comes from the adaptive
+scheduler itself — the library's native planner `hc_schedule` (§5, P:349-390;
+NEXT row f2, pinned bit-exact against oracle/planner_oracle.py in tests/test_planner.py).
+This module only states the cfg3 scenario; it implements none of the planner.
 """
 from __future__ import annotations
 
@@ -16,96 +9,30 @@ from typing import List, Tuple
 
 import numpy as np
 
-HIDDEN, UPGRADE, DIRECT = 0, 1, 2
 
-
-def marginal_gains(p: float, m: float, N: int, rho: float, hybrid: bool = True):
-    """Stages per SPEC S:373-381 / P:363-381: list of (theta, delta_m, stage)."""
-    if m <= 0:
-        return []
-    if hybrid and p / m >= 2 * N * rho:
-        return [(2 * p / m - 2 * N * rho, m / 2, HIDDEN), (2 * N * rho, m / 2, UPGRADE)]
-    return [(p / m, m, DIRECT)]
-
-
-def value(p: float, m: float, beta: int, N: int, rho: float) -> float:
-    """Eq. 5-6 (P:305-311)."""
-    return p - beta * N * rho * m
-
-
-def greedy(p: List[float], m: List[float], N: int, rho: float, M: float,
-           hybrid: bool = True) -> Tuple[List[int], List[int], float]:
-    cands = []
-    for i in range(len(p)):
-        for th, dm, st in marginal_gains(p[i], m[i], N, rho, hybrid):
-            cands.append((-th, dm, i, st))
-    cands.sort()
-    alpha = [0] * len(p)
-    beta = [0] * len(p)
-    used = 0.0
-    hidden_taken = set()
-    for _, dm, i, st in cands:
-        if used + dm > M + 1e-12:
-            continue
-        if st == HIDDEN:
-            alpha[i], beta[i] = 1, 1
-            hidden_taken.add(i)
-        elif st == UPGRADE:
-            if i not in hidden_taken:
-                continue
-            beta[i] = 0
-        else:
-            alpha[i], beta[i] = 1, 0
-        used += dm
-    obj = sum(value(p[i], m[i], beta[i], N, rho) for i in range(len(p)) if alpha[i])
-    # best single item, KV or hidden (SURVEY §4.3 fix)
-    best, best_ab = obj, None
-    for i in range(len(p)):
-        for b in ((0, 1) if hybrid else (0,)):
-            need = m[i] * (1 - b / 2)
-            if need <= M + 1e-12:
-                g = value(p[i], m[i], b, N, rho)
-                if g > best:
-                    best, best_ab = g, (i, b)
-    if best_ab is not None:
-        alpha = [0] * len(p)
-        beta = [0] * len(p)
-        alpha[best_ab[0]], beta[best_ab[0]] = 1, best_ab[1]
-        obj = best
-    return alpha, beta, obj
-
-
-def brute_force(p, m, N, rho, M, hybrid=True):
-    """Exhaustive 3^n search over {skip, hidden, KV}; n <= 12."""
-    n = len(p)
-    assert n <= 12
-    best, best_ab = 0.0, ([0] * n, [0] * n)
-    for code in range(3 ** n):
-        a, b, used, obj, c = [0] * n, [0] * n, 0.0, 0.0, code
-        for i in range(n):
-            s = c % 3
-            c //= 3
-            if s == 0:
-                continue
-            if s == 1 and not hybrid:
-                used = float("inf")
-                break
-            a[i], b[i] = 1, 1 if s == 1 else 0
-            used += m[i] * (1 - b[i] / 2)
-            obj += value(p[i], m[i], b[i], N, rho)
-        if used <= M + 1e-12 and obj > best + 1e-12:
-            best, best_ab = obj, (a, b)
-    return best_ab[0], best_ab[1], best
+def cfg3_scenario(n_ctx: List[int], shape, rs: np.random.Generator) -> Tuple[dict, list, float]:
+    """One decode iteration of an OPT-30B server (SURVEY §8(d) cfg3 recipe):
+    128 running candidates with pending time p_i ~ U(0, 1.5 s) (30B TTFT SLO) and KV
+    need m_i = 2 (n_i + 1) units (block size 1), 64 waiting requests with no
+    pending time (so N = |W| + |R| = 192 and the iteration is a decode iteration),
+    rho = (4 d^2 / F) / 2 with F = 2.25e15 (ideal per-layer rebuild time per unit), and a
+    budget of 0.75 * sum m.  Returns (sched config, requests, now) for hc_schedule."""
+    p = [float(v) for v in rs.uniform(0.0, 1.5, size=len(n_ctx))]
+    now = 1000.0
+    reqs = [{"id": i, "running": 1, "has_token": 1, "arrival_time": 0.0, "last_token_time": now - p[i],
+             "seq_len": int(n_ctx[i])} for i in range(len(n_ctx))]
+    reqs += [{"id": len(n_ctx) + k, "running": 0, "has_token": 0, "arrival_time": now, "last_token_time": 0.0,
+              "seq_len": 1} for k in range(64)]
+    m = [2.0 * (n + 1) for n in n_ctx]
+    cfg = {"rho": (4.0 * shape.d ** 2 / 2.25e15) / 2.0, "total_units": 0.75 * sum(m), "ttft_slo": 0.0,
+           "tbt_slo": 0.0, "fallback": 0, "eps": 1e-6, "decay": 0.4, "hybrid": 1, "block_size": 1}
+    return cfg, reqs, now
 
 
 def plan_cfg3(n_ctx: List[int], shape, rs: np.random.Generator):
-    """cfg3 recipe (SURVEY §8(d)): p_i ~ U(0, 1.5 s) (30B TTFT SLO, P:437);
-    m_i = 2(n_i+1) units; N = 128 + 64; rho = (4 d^2 / F)/2 with F = 2.25e15
-    (per-layer ideal reconstruction time per memory unit); M = 0.75 * sum m."""
-    p = [float(v) for v in rs.uniform(0.0, 1.5, size=len(n_ctx))]
-    m = [2.0 * (n + 1) for n in n_ctx]
-    N = len(n_ctx) + 64
-    rho = (4.0 * shape.d ** 2 / 2.25e15) / 2.0
-    M = 0.75 * sum(m)
-    alpha, beta, _ = greedy(p, m, N, rho, M)
-    return alpha, beta
+    """(alpha, beta) of the 128 candidates, decided by the native planner."""
+    from paper_2504_07494_b200 import hc
+    cfg, reqs, now = cfg3_scenario(n_ctx, shape, rs)
+    alpha, beta, _, _ = hc.schedule(cfg, reqs, now)
+    k = len(n_ctx)
+    return [int(a) for a in alpha[:k]], [int(b) for b in beta[:k]]

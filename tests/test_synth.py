@@ -58,33 +58,20 @@ def test_config_recipes():
     assert all(y >= x for x, y in zip(a, b))
 
 
-def test_planner_spec_instance():
-    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_planner_instance.json")))
-    a, b, obj = planner.greedy(g["p"], g["m"], g["N"], g["rho"], g["M"])
-    assert a == g["alpha"] and b == g["beta"] and abs(obj - g["objective"]) < 1e-12
-    a2, b2, obj2 = planner.brute_force(g["p"], g["m"], g["N"], g["rho"], g["M"])
-    assert abs(obj2 - g["objective"]) < 1e-12
-
-
-def test_planner_marginal_gain_examples():
-    """SPEC S:379-381 examples."""
-    st = planner.marginal_gains(10, 4, 3, 0.25)
-    assert [(round(t, 12), dm) for t, dm, _ in st] == [(3.5, 2.0), (1.5, 2.0)]
-    st = planner.marginal_gains(1, 4, 3, 0.25)
-    assert [(t, dm) for t, dm, _ in st] == [(0.25, 4)]
-
-
-def test_planner_feasible_and_survey_counterexample():
-    """one request p=1.4, m=16, N=3, rho=0.0202, M=11.93 -> hidden is optimal."""
-    a, b, obj = planner.greedy([1.4], [16.0], 3, 0.0202, 11.93)
-    assert a == [1] and b == [1] and obj > 0
-    rs = np.random.default_rng(0)
-    for _ in range(200):
-        n = int(rs.integers(1, 7))
-        p = list(rs.uniform(0, 10, n))
-        m = [float(2 * rs.integers(1, 11)) for _ in range(n)]
-        M = float(rs.uniform(0, sum(m)))
-        a, b, obj = planner.greedy(p, m, 10, 0.05, M)
-        used = sum(mi * (1 - bi / 2) for mi, ai, bi in zip(m, a, b) if ai)
-        assert used <= M + 1e-9
-        assert obj <= planner.brute_force(p, m, 10, 0.05, M)[2] + 1e-9
+def test_cfg3_modes_are_the_oracle_planners_decision():
+    """cfg3's cache modes come from the native planner (synth.planner delegates to
+    hc_schedule); the oracle planner written from the paper (oracle/planner_oracle.py) takes
+    the same decision on the same scenario — 127 of 128 candidates scheduled, 30 hidden."""
+    from oracle import planner_oracle as PO
+    from synth.configs import OPT30B, sharegpt_like
+    rs = np.random.default_rng(2)
+    n_all = sharegpt_like(128, rs)
+    state = rs.bit_generator.state
+    a, b = planner.plan_cfg3(n_all, OPT30B, rs)
+    rs.bit_generator.state = state
+    cfg, reqs, now = planner.cfg3_scenario(n_all, OPT30B, rs)
+    a2, b2, _, res = PO.schedule(cfg, reqs, now)
+    assert a == a2[:128] and b == b2[:128]
+    assert sum(a) == 127 and sum(b) == 30 and res["iter_type"] == 0
+    w = C.cfg3()
+    assert w.req_ids == [i for i in range(128) if a[i]] and w.modes == [b[i] for i in range(128) if a[i]]
