@@ -331,6 +331,114 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
   }
 }
 
+// GQA, grp even: the query heads of a K/V head are taken two at a time — every K and V
+// chunk comes out of TMEM once per pair, and the two heads' dot products, softmax shuffles
+// and Σ p·v reduce-scatters are independent chains the scheduler interleaves (the epilogue
+// of a GQA tile is latency-bound: the per-head loop runs them back to back).
+template <int S, int TILE_N>
+__device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane) {
+  const bool valid = grow < a.M;
+  int req = 0, tok = 0, n = 0;
+  if (valid) {
+    const int g = grow / a.B;
+    req = a.hblk_req[g];
+    tok = a.row_pos[g] + (grow - g * a.B);
+    n = a.reqs[req].n;
+  }
+  const bool live = valid && tok < n;
+  const int tok0 = tok - (lane & (S - 1));
+  const bool seg_live = valid && tok0 < n;
+  const int split = valid ? a.reqs[req].split_begin + tok0 / S : 0;
+  const int dh = a.dh, HT = TILE_N / (2 * dh);
+#pragma unroll 1
+  for (int jg = 0; jg < HT * a.grp; jg += 2) {
+    const int j = jg / a.grp;
+    const int h = (nt * HT + j) * a.grp + (jg - j * a.grp);   // query heads h, h + 1
+    const int nk = nt * TILE_N + j * 2 * dh;
+    const uint32_t tk = tacc + j * 2 * dh;
+    const __nv_bfloat16* qh0 = a.q + (size_t)req * a.d + (size_t)h * dh;
+    const __nv_bfloat16* qh1 = qh0 + dh;
+    float s0 = 0.f, s1 = 0.f;
+    if (a.rope_inv != nullptr) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < dh / 2; c0 += 32) {
+        uint4 qa0[4], qb0[4], qa1[4], qb1[4];
+        load_q32(qh0 + c0, qa0);
+        load_q32(qh0 + c0 + dh / 2, qb0);
+        load_q32(qh1 + c0, qa1);
+        load_q32(qh1 + c0 + dh / 2, qb1);
+        float f[32], f2[32];
+        load_chunk(tk + c0, a.bias, nk + c0, f);
+        load_chunk(tk + c0 + dh / 2, a.bias, nk + c0 + dh / 2, f2);
+        rope_rotate(f, f2, tok, a.rope_inv + c0);
+        s0 += dot32_q(f, qa0) + dot32_q(f2, qb0);
+        s1 += dot32_q(f, qa1) + dot32_q(f2, qb1);
+      }
+    } else {
+#pragma unroll 1
+      for (int c0 = 0; c0 < dh; c0 += 32) {
+        uint4 qa0[4], qa1[4];
+        load_q32(qh0 + c0, qa0);
+        load_q32(qh1 + c0, qa1);
+        float f[32];
+        load_chunk(tk + c0, a.bias, nk + c0, f);
+        s0 += dot32_q(f, qa0);
+        s1 += dot32_q(f, qa1);
+      }
+    }
+    s0 = live ? s0 * a.scale_log2 : -INFINITY;
+    s1 = live ? s1 * a.scale_log2 : -INFINITY;
+    float m0 = s0, m1 = s1;
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) {
+      m0 = fmaxf(m0, __shfl_xor_sync(kFull, m0, o));
+      m1 = fmaxf(m1, __shfl_xor_sync(kFull, m1, o));
+    }
+    const float p0 = live ? exp2f(s0 - m0) : 0.f, p1 = live ? exp2f(s1 - m1) : 0.f;
+    float l0 = p0, l1 = p1;
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) {
+      l0 += __shfl_xor_sync(kFull, l0, o);
+      l1 += __shfl_xor_sync(kFull, l1, o);
+    }
+    const size_t task0 = (size_t)h * a.n_splits_all + split, task1 = task0 + a.n_splits_all;
+#pragma unroll 1
+    for (int c0 = 0; c0 < dh; c0 += 32) {
+      float v[32];
+      load_chunk(tk + dh + c0, a.bias, nk + dh + c0, v);
+      float f0[32], f1[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        f0[e] = v[e] * p0;
+        f1[e] = v[e] * p1;
+      }
+      SegReduceScatter<S / 2, 32>::run(f0, lane);
+      SegReduceScatter<S / 2, 32>::run(f1, lane);
+      if (seg_live) {
+        const int off = c0 + (lane & (S - 1)) * (32 / S);
+        float* d0 = a.part_acc + task0 * dh + off;
+        float* d1 = a.part_acc + task1 * dh + off;
+        if constexpr (S == 32) {
+          d0[0] = f0[0];
+          d1[0] = f1[0];
+        } else if constexpr (S == 16) {
+          *reinterpret_cast<float2*>(d0) = make_float2(f0[0], f0[1]);
+          *reinterpret_cast<float2*>(d1) = make_float2(f1[0], f1[1]);
+        } else {
+          *reinterpret_cast<float4*>(d0) = make_float4(f0[0], f0[1], f0[2], f0[3]);
+          *reinterpret_cast<float4*>(d1) = make_float4(f1[0], f1[1], f1[2], f1[3]);
+        }
+      }
+    }
+    if (seg_live && (lane & (S - 1)) == 0) {
+      a.part_ml[2 * task0] = m0;
+      a.part_ml[2 * task0 + 1] = l0;
+      a.part_ml[2 * task1] = m1;
+      a.part_ml[2 * task1 + 1] = l1;
+    }
+  }
+}
+
 struct PairSmem {
   uint8_t* stages;
   uint64_t* full;
@@ -525,7 +633,11 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
         }
 #endif
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
-        if (a.seg == 8)
+        if (a.grp % 2 == 0) {   // GQA: query heads two at a time
+          if (a.seg == 8) attend_tile_gqa2<8, PC::TILE_N>(a, tacc, nt, grow, lane);
+          else if (a.seg == 16) attend_tile_gqa2<16, PC::TILE_N>(a, tacc, nt, grow, lane);
+          else attend_tile_gqa2<32, PC::TILE_N>(a, tacc, nt, grow, lane);
+        } else if (a.seg == 8)
           attend_tile<8, PC::TILE_N>(a, tacc, nt, grow, lane);
         else if (a.seg == 16)
           attend_tile<16, PC::TILE_N>(a, tacc, nt, grow, lane);
