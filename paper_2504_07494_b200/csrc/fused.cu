@@ -70,7 +70,7 @@ struct FusedTaskMap {
       const long long t0 = clock64();
       for (int mt = mt0; mt <= mt1; ++mt) {
         const int32_t* f = p->tile_done + mt * p->gemm_n_tiles + nt;
-        while (pg::ld_acquire(f) < 8) {
+        while (pg::ld_acquire(f) < p->tile_target) {
           __nanosleep(256);
           if (clock64() - t0 > (1ll << 35)) __trap();
         }
@@ -97,8 +97,11 @@ struct FusedSmem {
   static constexpr int TOTAL = CTRL_OFF + (TC ? (NA + 6) * TCC::CTRL_BYTES : 0);
 };
 
-template <int GS, int NA, int NSTA, bool QR, bool TC, int NS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * NA, 1)
+// EW: extra epilogue warps (0 or 4): with 4, two warps per TMEM lane quarter split each
+// tile's epilogue (every other head / column chunk) — for GQA, whose attend epilogue serves
+// G query heads per rebuilt K/V head and otherwise idles the tensor cores.
+template <int GS, int NA, int NSTA, bool QR, bool TC, int NS, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * (NA + EW), 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                       const __grid_constant__ CUtensorMap tmap_kv, const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
@@ -111,7 +114,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   uint8_t* attn_base = smem + FS::ATTN_OFF;
   uint8_t* ctrl_base = smem + FS::CTRL_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pg::pair_setup<NS, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w);
+  constexpr int kGemmWarps = pg::GEMM_THREADS / 32 + EW;
+  pg::pair_setup<NS, kGemmStages, EW ? 2 : 1>(ps, warp, lane, &tmap_x, &tmap_w);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -123,10 +127,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
     g_timeline[blockIdx.x][4] = ~0ull;
   }
 #endif
-  if (warp < pg::GEMM_THREADS / 32) {
-    pg::pair_roles<NS, kGemmStages>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+  if (warp < kGemmWarps) {
+    pg::pair_roles<NS, kGemmStages, EW ? 2 : 1, (EW > 0)>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
 #ifdef HC_TIMELINE
-    asm volatile("bar.sync 1, %0;" ::"n"(pg::GEMM_THREADS) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kGemmWarps) : "memory");
     if (threadIdx.x == 0) {
       g_timeline[blockIdx.x][1] = gtimer();
       g_timeline[blockIdx.x][3] = (unsigned long long)*(volatile int32_t*)p.task_counter;
@@ -136,7 +140,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
       // This CTA's GEMM has drained (the epilogue consumed the last tile, so the leader's
       // UMMAs no longer read these stages): its 6 warps join the attention pool, each with a
       // 2-stage ring carved from the freed GEMM stage buffers.
-      asm volatile("bar.sync 1, %0;" ::"n"(pg::GEMM_THREADS) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kGemmWarps) : "memory");
       ptx::fence_proxy_async_smem();
       if (warp < kJoin) {
         const FusedTaskMap tm{&p};
@@ -149,7 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
     }
   } else {
     const FusedTaskMap tm{&p};
-    const int aw = warp - pg::GEMM_THREADS / 32;
+    const int aw = warp - kGemmWarps;
     if constexpr (TC)
       at::attn_warp_run_tc<128, NSTA>(p, &tmap_kv, attn_base + aw * FS::WARP_BYTES,
                                       ctrl_base + aw * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm);
@@ -169,25 +173,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   pg::pair_teardown<NS, kGemmStages>(warp, tmem_base);
 }
 
-template <int GS, int NA, int NSTA, bool QR, bool TC, int NS>
-cudaError_t launch_cfg1(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
-                        int num_sms, cudaStream_t s) {
+template <int GS, int NA, int NSTA, bool QR, bool TC, int NS, int EW>
+cudaError_t launch_cfg1(const pg::TcArgs& a0, const AttnParams& p0, const void* tmx, const void* tmw,
+                        const void* tmkv, int num_sms, cudaStream_t s) {
   constexpr int smem = 1024 + FusedSmem<GS, NA, NSTA, QR, TC, NS>::TOTAL;
   static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
-  auto k = fused_step_kernel<GS, NA, NSTA, QR, TC, NS>;
+  auto k = fused_step_kernel<GS, NA, NSTA, QR, TC, NS, EW>;
+  pg::TcArgs a = a0;
+  AttnParams p = p0;
+  a.epi_split = EW ? 2 : 1;
+  p.tile_target = 8 * a.epi_split;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
-  k<<<2 * pairs, pg::GEMM_THREADS + 32 * NA, smem, s>>>(*static_cast<const CUtensorMap*>(tmx),
+  k<<<2 * pairs, pg::GEMM_THREADS + 32 * (NA + EW), smem, s>>>(*static_cast<const CUtensorMap*>(tmx),
                                                         *static_cast<const CUtensorMap*>(tmw),
                                                         *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx), a, p);
   return cudaGetLastError();
 }
-template <int GS, int NA, int NSTA, bool QR, int NS = 2>
+template <int GS, int NA, int NSTA, bool QR, int NS = 2, int EW = 0>
 cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
                        int num_sms, cudaStream_t s) {
-  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true, NS>(a, p, tmx, tmw, tmkv, num_sms, s);
-  return launch_cfg1<GS, NA, NSTA, QR, false, NS>(a, p, tmx, tmw, tmkv, num_sms, s);
+  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true, NS, EW>(a, p, tmx, tmw, tmkv, num_sms, s);
+  return launch_cfg1<GS, NA, NSTA, QR, false, NS, EW>(a, p, tmx, tmw, tmkv, num_sms, s);
 }
 
 }  // namespace
@@ -251,6 +259,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     tile_done = nullptr;
     a.diag = t.diag_epi;
   }
+  a.epi_split = 1;
+  ap_.tile_target = 8;
   a.tile_done = tile_done;
   ap_.tile_done = tile_done;
   ap_.gemm_n_tiles = a.n_tiles;
@@ -272,7 +282,11 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     if (cfg == 382) return launch_cfg<3, 8, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
     return launch_cfg<4, 5, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   }
-  const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 282 : 352);
+  // GQA: the tensor-core KV loop drains the KV stream early, so 2 attention warps suffice and
+  // 4 extra epilogue warps split the G-query-head attend epilogue (cfg 3424)
+  const int cfg = t.fused_cfg ? t.fused_cfg : (rp.H > rp.Hk ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352));
+  if (cfg == 3424) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 3444) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);

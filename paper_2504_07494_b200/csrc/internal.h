@@ -85,6 +85,7 @@ struct AttnParams {
   int32_t n_hid_splits;
   const int32_t* tile_done;      // [gemm_m_tiles][gemm_n_tiles] finished epilogue warps (8 = ready)
   int32_t gemm_n_tiles, gemm_tile_m, gemm_tile_n;
+  int32_t tile_target;           // finished epilogue warps per GEMM tile (8, or 16 with extra epilogue warps)
   int32_t kv_evict_first;        // 1: KV chunks are streamed with an L2 evict-first policy
   int32_t th;                    // heads per split in the task numbering: H (SIMT loop) or Hk (tensor-core loop)
   int32_t tc;                    // 1: every task is a KV-mode split and runs attn_tc.cuh (task = split * Hk + kvhead)

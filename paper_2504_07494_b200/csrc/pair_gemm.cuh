@@ -66,6 +66,8 @@ struct TcArgs {
   int32_t n_splits_all;
   float scale_log2;
   int32_t seg;              // tokens per partial (8, 16 or 32; segments never straddle a block)
+  int32_t epi_split;        // epilogue warps per TMEM lane quarter (1, or 2 with the fused kernel's extra
+                            // epilogue warps: each takes every other head / column chunk)
   int32_t diag;             // -DHC_DIAG builds only (HC_DIAG_EPI): timing diagnostics with wrong outputs
 };
 
@@ -252,8 +254,8 @@ __device__ __forceinline__ float dot32_q(const float (&f)[32], const uint4 (&u)[
 // sum_j p_j v_j by a butterfly reduce-scatter; lane i of the segment writes dims
 // [i*32/S, (i+1)*32/S) of every 32-column chunk.  Rows past M and tokens past n get p = 0;
 // a segment that starts past n writes nothing.
-template <int S, int TILE_N>
-__device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane) {
+template <int S, int TILE_N, int NSPLIT = 1>
+__device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane, int sub) {
   const bool valid = grow < a.M;
   int req = 0, tok = 0, n = 0;
   if (valid) {
@@ -268,7 +270,7 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
   const int split = valid ? a.reqs[req].split_begin + tok0 / S : 0;
   const int dh = a.dh, HT = TILE_N / (2 * dh);
 #pragma unroll 1
-  for (int jg = 0; jg < HT * a.grp; ++jg) {
+  for (int jg = sub; jg < HT * a.grp; jg += NSPLIT) {
     const int j = jg / a.grp;                     // K/V head of the tile
     const int h = (nt * HT + j) * a.grp + (jg - j * a.grp);   // query head
     const int nk = nt * TILE_N + j * 2 * dh;      // interleaved column of K_hk (bias index)
@@ -335,8 +337,8 @@ __device__ __forceinline__ void attend_tile(const TcArgs& a, uint32_t tacc, int 
 // chunk comes out of TMEM once per pair, and the two heads' dot products, softmax shuffles
 // and Σ p·v reduce-scatters are independent chains the scheduler interleaves (the epilogue
 // of a GQA tile is latency-bound: the per-head loop runs them back to back).
-template <int S, int TILE_N>
-__device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane) {
+template <int S, int TILE_N, int NSPLIT>
+__device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc, int nt, int grow, int lane, int sub) {
   const bool valid = grow < a.M;
   int req = 0, tok = 0, n = 0;
   if (valid) {
@@ -351,7 +353,7 @@ __device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc,
   const int split = valid ? a.reqs[req].split_begin + tok0 / S : 0;
   const int dh = a.dh, HT = TILE_N / (2 * dh);
 #pragma unroll 1
-  for (int jg = 0; jg < HT * a.grp; jg += 2) {
+  for (int jg = 2 * sub; jg < HT * a.grp; jg += 2 * NSPLIT) {
     const int j = jg / a.grp;
     const int h = (nt * HT + j) * a.grp + (jg - j * a.grp);   // query heads h, h + 1
     const int nk = nt * TILE_N + j * 2 * dh;
@@ -465,7 +467,7 @@ __device__ __forceinline__ PairSmem pair_carve(uint8_t* base /*1024-aligned*/) {
 
 // Barrier init (warp 0) and pair TMEM allocation (warp 1, both CTAs).  The caller must then
 // run tc_fence_before; cluster_sync; tc_fence_after before reading *tmem_slot.
-template <int NSUB, int NSTAGE>
+template <int NSUB, int NSTAGE, int EPI_SPLIT = 1>
 __device__ __forceinline__ void pair_setup(const PairSmem& s, int warp, int lane, const CUtensorMap* tmx,
                                            const CUtensorMap* tmw) {
   if (warp == 0 && lane == 0) {
@@ -477,15 +479,16 @@ __device__ __forceinline__ void pair_setup(const PairSmem& s, int warp, int lane
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s.tfull[i], 1);
-      ptx::mbar_init(&s.tempty[i], 8);   // 4 epilogue warps x 2 CTAs (used on the leader)
+      ptx::mbar_init(&s.tempty[i], 8 * EPI_SPLIT);   // 4 (or 8) epilogue warps x 2 CTAs (used on the leader)
     }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_cg2<TMEM_COLS>(s.tmem_slot);
 }
 
-// Roles of warps 0..5.  Call with warp < 6 only.
-template <int NSUB, int NSTAGE>
+// Roles of warps 0..5 (+ 4 extra epilogue warps 6..9 when ESPLIT == 2).  Call with
+// warp < 6 (or < 10) only.  GQA2: compile the paired-query-head GQA epilogue in.
+template <int NSUB, int NSTAGE, int ESPLIT = 1, bool GQA2 = false>
 __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane, const CUtensorMap* tmap_x,
                                            const CUtensorMap* tmap_w, const TcArgs& a, uint32_t tmem_base) {
   using PC = PairCfg<NSUB, NSTAGE>;
@@ -601,8 +604,9 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
     }
     __syncwarp();
   } else {
-    // ================= epilogue (warps 2..5 of both CTAs) =================
+    // ================= epilogue (warps 2..5, and 6..9 with epi_split 2, of both CTAs) ==========
     const int q = warp & 3;
+    const int esub = ESPLIT > 1 ? (warp - 2) >> 2 : 0;   // ESPLIT 2: every other head / column chunk
     const int row_in_tile = (int)rank * 128 + q * 32 + lane;
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&s.tempty[0]), 0);
     int it = 0;
@@ -633,16 +637,23 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
         }
 #endif
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
-        if (a.grp % 2 == 0) {   // GQA: query heads two at a time
-          if (a.seg == 8) attend_tile_gqa2<8, PC::TILE_N>(a, tacc, nt, grow, lane);
-          else if (a.seg == 16) attend_tile_gqa2<16, PC::TILE_N>(a, tacc, nt, grow, lane);
-          else attend_tile_gqa2<32, PC::TILE_N>(a, tacc, nt, grow, lane);
-        } else if (a.seg == 8)
-          attend_tile<8, PC::TILE_N>(a, tacc, nt, grow, lane);
-        else if (a.seg == 16)
-          attend_tile<16, PC::TILE_N>(a, tacc, nt, grow, lane);
-        else
-          attend_tile<32, PC::TILE_N>(a, tacc, nt, grow, lane);
+        bool done = false;
+        if constexpr (GQA2) {
+          if (a.grp % 2 == 0) {   // GQA: query heads two at a time
+            if (a.seg == 8) attend_tile_gqa2<8, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+            else if (a.seg == 16) attend_tile_gqa2<16, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+            else attend_tile_gqa2<32, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+            done = true;
+          }
+        }
+        if (!done) {
+          if (a.seg == 8)
+            attend_tile<8, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+          else if (a.seg == 16)
+            attend_tile<16, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+          else
+            attend_tile<32, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
+        }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -655,7 +666,7 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       const int pos = a.rope_inv == nullptr ? 0
                       : (a.epi == EPI_SCRATCH ? (valid ? a.row_pos[g] + r : 0) : dst_info.w);
 #pragma unroll 1
-      for (int c = 0; c < PC::TILE_N / 32; ++c) {
+      for (int c = esub; c < PC::TILE_N / 32; c += ESPLIT) {   // (RoPE partners c, c + dh/64 share parity)
         const int n = nt * PC::TILE_N + c * 32;
         // RoPE pairs columns (c0, c0 + dh/2) of a rotated head segment (K; and q in EPI_PROJECT)
         int seg_c0 = -1;   // column within the rotated head segment, or -1
