@@ -606,6 +606,7 @@ def main():
     torch.cuda.synchronize()
     launches_per_step = pool.last_launch_count()
     decode_path = pool.last_decode_path()
+    kernel_cfg = pool.last_kernel_config()
     sampler.mark()
     pool.set_profiling(True)
     pool.kernel_times()  # clear
@@ -752,7 +753,10 @@ def main():
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
         peak = tf_peak
-        roof = {"bound": "tensor", "kernel": "fused_step_kernel (<3,5,2> or, KV-dominated, <2,8,2>)" if fused else "recon_tc2_kernel<2,4>",
+        fcfg = str(kernel_cfg % 10000)
+        fname = (f"fused_step_kernel<{fcfg[0]},{fcfg[1]},{fcfg[2]}" + (f",+{fcfg[3]} epilogue warps" if len(fcfg) > 3 else "")
+                 + (", 256x256 tiles" if kernel_cfg >= 10000 else "") + ">")
+        roof = {"bound": "tensor", "kernel": fname if fused else "recon_tc2_kernel<2,4>",
                 "achieved": k["achieved"], "peak": peak,
                 "unit": "TFLOP/s", "frac": k["achieved"] / peak,
                 "frac_vs_burst": k["achieved"] / tf_burst, "frac_vs_sustained": k["achieved"] / tf_sus,

@@ -302,6 +302,10 @@ int32_t hc_last_launch_count(const hc_pool* pool);
  * 1 = fused step kernel (GEMM and attention warps in one launch), 2 = attention only (no
  * hidden-mode request), 3 = absorbed hidden attention (HC_FLAG_ABSORB_HIDDEN), -1 = none. */
 int32_t hc_last_decode_path(const hc_pool* pool);
+/* Fused step kernel configuration of the last hc_decode_attention (path 1): decimal digits
+ * {GEMM stages, attention warps, attention stages[, extra epilogue warps]} — 352, 282, 342,
+ * 3424, 3224 (10000 + cfg for 256-wide tiles); 0 when no fused kernel ran. */
+int32_t hc_last_kernel_config(const hc_pool* pool);
 /* When enabled, hc_decode_attention records CUDA events around each of its kernels on
  * the stream it launches them on.  hc_kernel_times() synchronises on all events recorded
  * since the previous read and returns, summed over those calls, the milliseconds of

@@ -208,7 +208,8 @@ int fused_tile_m() { return pg::P_BM; }
 int fused_tile_n() { return 256; }   // the narrowest tile (NSUB = 1): sizes per-tile arrays for either
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
-                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv) {
+                         int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv,
+                         int* cfg_out) {
   pg::TcArgs a{};
   a.gather = rp.gather;
   a.n_hblocks = rp.n_hblocks;
@@ -279,14 +280,21 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   const double t_kv = (double)rp.kv_tokens * 4.0 * rp.dk / 6.5e12;
   if (nsub == 1) {   // 256 x 256 tiles: 32-KiB stages, 4 of them (the same bytes in flight as 3 x 48)
     const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 382 : 452);
+    if (cfg_out) *cfg_out = 10000 + cfg;
     if (cfg == 382) return launch_cfg<3, 8, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
     return launch_cfg<4, 5, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   }
   // GQA: the tensor-core KV loop drains the KV stream early, so 2 attention warps suffice and
-  // 4 extra epilogue warps split the G-query-head attend epilogue (cfg 3424)
-  const int cfg = t.fused_cfg ? t.fused_cfg : (rp.H > rp.Hk ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352));
-  if (cfg == 3424) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 3444) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  // 4 extra epilogue warps split the G-query-head attend epilogue (cfg 3224)
+  // GEMM-dominated multi-head batches (KV stream < 5% of the rebuild): 4 attention warps +
+  // 8 epilogue warps (cfg 3424; same-box A/B: cfg2 -1.7%, cfg3 / cfg4 / all-hidden equal or
+  // better; where the KV stream matters — cfg5 1/16..1/4 — the 5th attention warp wins, +4%)
+  const int cfg = t.fused_cfg ? t.fused_cfg
+                              : (rp.H > rp.Hk ? 3224
+                                              : (t_kv < 0.05 * t_gemm ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352)));
+  if (cfg_out) *cfg_out = cfg;
+  if (cfg == 3224) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 3424) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
   return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);

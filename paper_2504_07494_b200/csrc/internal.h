@@ -195,7 +195,7 @@ int fused_tile_m();
 int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s,
-                         const void* tmap_kv = nullptr);
+                         const void* tmap_kv = nullptr, int* cfg_out = nullptr);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
                          void* out, float* lse, cudaStream_t s);

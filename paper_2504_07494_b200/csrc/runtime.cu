@@ -263,6 +263,7 @@ struct hc_pool {
   int ring_next = 0;
   int32_t last_launches = 0;
   int32_t last_path = -1;
+  int32_t last_cfg = 0;   // fused-kernel configuration of the last decode (see hc_last_kernel_config)
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, 5>> prof_pending;
   std::vector<cudaEvent_t> ev_free;
@@ -1037,6 +1038,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.kv_evict_first = pool->tune.kv_evict_first;
   ap.diag = pool->tune.diag_attn;
   pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
+  pool->last_cfg = 0;
   if (P.absorb) {
     // f4 (ii): hidden requests never rebuild K/V; KV requests take the split-K path
     if (P.n_h > 0) {
@@ -1096,7 +1098,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     ap.n_kv_tasks = P.n_kv_splits * ap.th;
     ap.n_hid_splits = P.n_hid_splits;
     err = launch_fused(rp, ap, &pool->tmap_x, &pool->tmap_w_half, reinterpret_cast<int32_t*>(ws + P.off_tiledone),
-                       pool->num_sms, pool->tune, s, &pool->tmap_kv);
+                       pool->num_sms, pool->tune, s, &pool->tmap_kv, &pool->last_cfg);
     if (err != cudaSuccess) return cuda_fail(err, "fused step kernel");
     ++launches;
     if (pool->profiling) {
@@ -1587,6 +1589,7 @@ static hc_status prefill_after_alloc(hc_pool* pool, int32_t n_req, const int64_t
 
 int32_t hc_last_launch_count(const hc_pool* pool) { return pool ? pool->last_launches : -1; }
 int32_t hc_last_decode_path(const hc_pool* pool) { return pool ? pool->last_path : -1; }
+int32_t hc_last_kernel_config(const hc_pool* pool) { return pool ? pool->last_cfg : -1; }
 
 hc_status hc_set_profiling(hc_pool* pool, int32_t enable) {
   if (!pool) return fail(HC_E_INVALID, "pool is null");

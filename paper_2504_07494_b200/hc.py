@@ -92,6 +92,7 @@ def _load() -> ctypes.CDLL:
         "hc_request_blocks": (I32, [P, I64, I32, pI32, I64, pI64]),
         "hc_last_launch_count": (I32, [P]),
         "hc_last_decode_path": (I32, [P]),
+        "hc_last_kernel_config": (I32, [P]),
         "hc_set_profiling": (I32, [P, I32]),
         "hc_kernel_times": (I32, [P, pF, pI32]),
         "hc_schedule": (I32, [ctypes.POINTER(SchedConfig), I32, ctypes.POINTER(SchedRequest), ctypes.c_double,
@@ -421,6 +422,9 @@ class HybridCachePool:
     # -- measurement hooks
     def last_launch_count(self) -> int:
         return int(lib.hc_last_launch_count(self.handle))
+
+    def last_kernel_config(self) -> int:
+        return int(lib.hc_last_kernel_config(self.handle))
 
     def last_decode_path(self) -> int:
         return int(lib.hc_last_decode_path(self.handle))
