@@ -295,10 +295,14 @@ def test_fused_and_unfused_agree_bitwise(hc, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"HC_GROUP_N": "2"}, {"HC_GROUP_N": "3"}, {"HC_SYNC_W": "8"},
-                                 {"HC_GROUP_N": "2", "HC_SYNC_W": "8"}])
+                                 {"HC_GROUP_N": "2", "HC_SYNC_W": "8"}, {"HC_GROUP_N": "-3"},
+                                 {"HC_FUSED_CFG": "352"}, {"HC_FUSED_CFG": "282"}, {"HC_FUSED_CFG": "342"},
+                                 {"HC_FUSED_CFG": "3424"}, {"HC_FUSED_CFG": "3224"}])
 def test_fused_schedules_agree_bitwise(hc, monkeypatch, env):
-    """The fused kernel's raster (n-tiles per group) and partner lockstep only reorder whole
-    tiles in time: every tile's k-order and epilogue are unchanged => identical bits.  d=1024
+    """The fused kernel's raster (n-tiles per group, m-major groups), partner lockstep and
+    configuration (GEMM stages, attention warps, extra epilogue warps that split a tile's
+    heads) only reorder whole tiles / heads / KV tasks in time: every tile's k-order, every
+    head's epilogue arithmetic and every KV task are unchanged => identical bits.  d=1024
     gives 4 n-tiles; 9 hidden requests give 7 m-tiles with a ragged last one."""
     n = [700, 33, 511, 1, 257, 96, 129, 64, 300, 17, 415, 640]
     modes = [MODE_HIDDEN if i % 4 != 1 else MODE_KV for i in range(len(n))]
