@@ -223,6 +223,17 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       }
       if (!QREG && first)
         ptx::bulk_g2s(sb + 2 * C::CHUNK, qg + (size_t)psp.req * d + phead * DH, C::QB, &bars[stage]);
+      if (p.kv_prefetch > 0 && prq.mode == 0) {   // L2 prefetch of a chunk kv_prefetch ahead (same task)
+        const int pc = pchunk + p.kv_prefetch;
+        if (pc < pnch) {
+          const int ptok = psp.lb0 * Bm + pc * TOK;
+          const int plb = ptok / Bm, prow = ptok - plb * Bm;
+          const int pkb = p.tables[prq.tab_off + 2 * plb], pvb = p.tables[prq.tab_off + 2 * plb + 1];
+          ptx::bulk_prefetch_l2(pool + (size_t)pkb * blk_elems + hk * kv_head_elems + (size_t)prow * DH, C::CHUNK);
+          ptx::bulk_prefetch_l2(pool + (size_t)pvb * blk_elems + p.v_off + hk * kv_head_elems + (size_t)prow * DH,
+                                C::CHUNK);
+        }
+      }
     }
     if (QREG && first) {   // every lane: its 8 dims of q_h (consumed when this stage is)
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(qg + (size_t)psp.req * d + phead * DH) + lane % LPR);

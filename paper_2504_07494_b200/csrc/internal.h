@@ -23,6 +23,7 @@ struct Tuning {
   int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM
   int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
   int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
+  int kv_prefetch = 0;   // HC_KV_PF: KV chunks (of the current task) prefetched into L2 ahead of the smem ring
   int attn_tc = 1;       // HC_ATTN_TC: KV attention on mma.sync (attn_tc.cuh): 0 never, 1 GQA only, 2 always
   int tc_1sm = 0;        // HC_TC_1SM: 1-SM tcgen05 reconstruction kernel instead of CTA pairs
   int tc_nsub = 0;       // HC_TC_NSUB: 1 = 256-wide pair tiles
@@ -90,6 +91,7 @@ struct AttnParams {
   int32_t th;                    // heads per split in the task numbering: H (SIMT loop) or Hk (tensor-core loop)
   int32_t tc;                    // 1: every task is a KV-mode split and runs attn_tc.cuh (task = split * Hk + kvhead)
   int32_t diag;                  // -DHC_DIAG builds only (HC_DIAG_ATTN): 1 skip the math, 2 read block 0 only
+  int32_t kv_prefetch;           // KV chunks ahead of the ring prefetched into L2 (0 = off)
 };
 
 struct CombineParams {
