@@ -25,6 +25,8 @@ using ap::warp_sum;
 // Every task a KV-mode (split, K/V head): the tensor-core loop (attn_tc.cuh), NW warps per CTA.
 template <int DH, int NW, int NST>
 __global__ void __launch_bounds__(NW * 32, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv,
+                                                             const __grid_constant__ CUtensorMap tmap_sk,
+                                                             const __grid_constant__ CUtensorMap tmap_sv,
                                                              const AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_tc[];
   using C = at::TcCfg<DH, NST>;
@@ -33,7 +35,7 @@ __global__ void __launch_bounds__(NW * 32, 1) attn_tc_kernel(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ap::DirectTaskMap tm{p.n_tasks, p.th};
   at::attn_warp_run_tc<DH, NST>(p, &tmap_kv, smem + warp * C::STAGES_BYTES,
-                                smem + NW * C::STAGES_BYTES + warp * C::CTRL_BYTES, lane, tm);
+                                smem + NW * C::STAGES_BYTES + warp * C::CTRL_BYTES, lane, tm, &tmap_sk, &tmap_sv);
 }
 
 template <int DH, int NW, int NST>
@@ -153,7 +155,8 @@ bool attn_tc_supported(int dtype, int dh, int G, int Bkv) {
 }
 
 template <int DH, int NW, int NST>
-static cudaError_t launch_tc(const AttnParams& p, const void* tmap, int num_sms, cudaStream_t s) {
+static cudaError_t launch_tc(const AttnParams& p, const void* tmap, const void* tsk, const void* tsv, int num_sms,
+                             cudaStream_t s) {
   using C = at::TcCfg<DH, NST>;
   constexpr int smem = 1024 + NW * (C::STAGES_BYTES + C::CTRL_BYTES);
   auto k = attn_tc_kernel<DH, NW, NST>;
@@ -161,16 +164,18 @@ static cudaError_t launch_tc(const AttnParams& p, const void* tmap, int num_sms,
   if (e != cudaSuccess) return e;
   const int max_ctas = (p.n_tasks + NW - 1) / NW;
   const int grid = max_ctas < num_sms ? max_ctas : num_sms;
-  k<<<grid, NW * 32, smem, s>>>(*static_cast<const CUtensorMap*>(tmap), p);
+  k<<<grid, NW * 32, smem, s>>>(*static_cast<const CUtensorMap*>(tmap),
+                                *static_cast<const CUtensorMap*>(tsk ? tsk : tmap),
+                                *static_cast<const CUtensorMap*>(tsv ? tsv : tmap), p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s,
-                        const void* tmap_kv) {
+                        const void* tmap_kv, const void* tmap_scr_k, const void* tmap_scr_v) {
   if (p.n_tasks <= 0) return cudaSuccess;
-  if (p.tc) {   // every task a KV-mode split: tensor-core loop (the runtime checked attn_tc_supported)
-    if (p.dh == 128) return launch_tc<128, 8, 3>(p, tmap_kv, num_sms, s);
-    return launch_tc<64, 8, 5>(p, tmap_kv, num_sms, s);
+  if (p.tc) {   // tensor-core loop (the runtime checked attn_tc_supported)
+    if (p.dh == 128) return launch_tc<128, 8, 3>(p, tmap_kv, tmap_scr_k, tmap_scr_v, num_sms, s);
+    return launch_tc<64, 8, 5>(p, tmap_kv, tmap_scr_k, tmap_scr_v, num_sms, s);
   }
   if (!generic && attn_pipe_supported(dtype, p.dh, p.B)) {
     const int cfg = t.attn_cfg;

@@ -73,9 +73,14 @@ __device__ __forceinline__ float ex2(float x) {
 
 // One warp's loop.  stages: NST * STAGE bytes, 1024-aligned; ctrl: CTRL_BYTES, 16-aligned.
 // Tasks t = split * Hk + kvhead from the task map; every task is a KV-mode split.
+// Hidden-mode tasks (the fused kernel's scratch path: the GEMM epilogue wrote rebuilt K and V
+// as [hblock][Hk][B][dh]) read through tmap_scr_k / tmap_scr_v (rows of dh elements) after
+// the task map's wait_ready (the tiles that wrote them are done).
 template <int DH, int NST, class TaskMap>
 __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUtensorMap* tmap, uint8_t* stages,
-                                                 uint8_t* ctrl, int lane, const TaskMap& tm) {
+                                                 uint8_t* ctrl, int lane, const TaskMap& tm,
+                                                 const CUtensorMap* tmap_scr_k = nullptr,
+                                                 const CUtensorMap* tmap_scr_v = nullptr) {
   using C = TcCfg<DH, NST>;
   constexpr int TOK = C::TOK;
   constexpr int KS = DH / 16;       // k-slices of the score mma, m-slices of the output mma
@@ -108,31 +113,42 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
       psp = p.splits[psplit];
       prq = p.reqs[psp.req];
       pnch = (psp.ntok + TOK - 1) / TOK;
+      tm.wait_ready(psplit, phk, psp, prq, lane);
     }
   };
   load_task(ptask);
   auto produce = [&](int stage) -> bool {
     if (ptask >= p.n_tasks) return false;
-    const int tok = psp.lb0 * p.Bkv + pchunk * TOK;
-    const int lb = tok / p.Bkv, row = tok - lb * p.Bkv;
+    const bool hid = prq.mode != 0;
+    const int Bm = hid ? p.B : p.Bkv;
+    const int tok = psp.lb0 * Bm + pchunk * TOK;
+    const int lb = tok / Bm, row = tok - lb * Bm;
     const int rem = psp.ntok - pchunk * TOK;
     const bool first = pchunk == 0, last = pchunk == pnch - 1;
     if (lane == 0) {
-      const int kb = p.tables[prq.tab_off + 2 * lb], vb = p.tables[prq.tab_off + 2 * lb + 1];
-      const int rk = (int)(kb * rows_per_unit + (int64_t)phk * p.Bkv + row);
-      const int rv = (int)(vb * rows_per_unit + v_rows + (int64_t)phk * p.Bkv + row);
+      int rk, rv;
+      const CUtensorMap *tk = tmap, *tv = tmap;
+      if (!hid) {
+        const int kb = p.tables[prq.tab_off + 2 * lb], vb = p.tables[prq.tab_off + 2 * lb + 1];
+        rk = (int)(kb * rows_per_unit + (int64_t)phk * p.Bkv + row);
+        rv = (int)(vb * rows_per_unit + v_rows + (int64_t)phk * p.Bkv + row);
+      } else {   // scratch [hblock][Hk][B][dh]
+        rk = rv = (int)(((int64_t)(prq.scratch_blk0 + lb) * p.Hk + phk) * p.B + row);
+        tk = tmap_scr_k;
+        tv = tmap_scr_v;
+      }
       meta[stage] = make_int4(psplit, phk, rem < TOK ? rem : TOK, (first ? 1 : 0) | (last ? 2 : 0) | (psp.req << 2));
       uint8_t* sb = stages + stage * C::STAGE;
       ptx::fence_proxy_async_smem();   // the warp's ldmatrix reads of this stage precede the TMA writes
       ptx::mbar_arrive_expect_tx(&bars[stage], C::STAGE);
 #pragma unroll
       for (int b = 0; b < C::NB; ++b) {
-        if (p.kv_evict_first) {
-          ptx::tma_load_2d_hint(sb + b * C::BOX, tmap, b * 64, rk, &bars[stage], pol);
-          ptx::tma_load_2d_hint(sb + C::CHUNK + b * C::BOX, tmap, b * 64, rv, &bars[stage], pol);
+        if (p.kv_evict_first && !hid) {
+          ptx::tma_load_2d_hint(sb + b * C::BOX, tk, b * 64, rk, &bars[stage], pol);
+          ptx::tma_load_2d_hint(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage], pol);
         } else {
-          ptx::tma_load_2d(sb + b * C::BOX, tmap, b * 64, rk, &bars[stage]);
-          ptx::tma_load_2d(sb + C::CHUNK + b * C::BOX, tmap, b * 64, rv, &bars[stage]);
+          ptx::tma_load_2d(sb + b * C::BOX, tk, b * 64, rk, &bars[stage]);
+          ptx::tma_load_2d(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage]);
         }
       }
     }

@@ -50,7 +50,8 @@ struct FusedTaskMap {
       head = t - ks * H;
       return;
     }
-    const int hpt = p->gemm_tile_n / (2 * p->dh) * p->G;   // query heads per GEMM n-tile
+    // heads per GEMM n-tile in the task numbering (K/V heads for the tensor-core loop)
+    const int hpt = p->gemm_tile_n / (2 * p->dh) * (p->tc ? 1 : p->G);
     const int u = t - p->n_kv_tasks;
     const int per_nt = p->n_hid_splits * hpt;
     const int nt = u / per_nt;
@@ -66,7 +67,7 @@ struct FusedTaskMap {
       const int g0 = rq.scratch_blk0 + sp.lb0;
       const int nblk = (sp.ntok + B - 1) / B;
       const int mt0 = (g0 * B) / p->gemm_tile_m, mt1 = ((g0 + nblk) * B - 1) / p->gemm_tile_m;
-      const int nt = (head / p->G) * 2 * p->dh / p->gemm_tile_n;
+      const int nt = (p->tc ? head : head / p->G) * 2 * p->dh / p->gemm_tile_n;
       const long long t0 = clock64();
       for (int mt = mt0; mt <= mt1; ++mt) {
         const int32_t* f = p->tile_done + mt * p->gemm_n_tiles + nt;
@@ -103,7 +104,8 @@ struct FusedSmem {
 template <int GS, int NA, int NSTA, bool QR, bool TC, int NS, int EW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * (NA + EW), 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                      const __grid_constant__ CUtensorMap tmap_kv, const pg::TcArgs a, const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_sk,
+                      const __grid_constant__ CUtensorMap tmap_sv, const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
   using FS = FusedSmem<GS, NA, NSTA, QR, TC, NS>;
   constexpr int kJoin = FS::kJoin;
@@ -146,7 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
         const FusedTaskMap tm{&p};
         if constexpr (TC)
           at::attn_warp_run_tc<128, 2>(p, &tmap_kv, ps.stages + warp * FS::kJoinBytes,
-                                       ctrl_base + (NA + warp) * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm);
+                                       ctrl_base + (NA + warp) * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm,
+                                       &tmap_sk, &tmap_sv);
         else
           ap::attn_warp_run<128, 2, FusedTaskMap, QR>(p, ps.stages + warp * FS::kJoinBytes, lane, tm);
       }
@@ -156,7 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
     const int aw = warp - kGemmWarps;
     if constexpr (TC)
       at::attn_warp_run_tc<128, NSTA>(p, &tmap_kv, attn_base + aw * FS::WARP_BYTES,
-                                      ctrl_base + aw * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm);
+                                      ctrl_base + aw * at::TcCfg<128, NSTA>::CTRL_BYTES, lane, tm, &tmap_sk, &tmap_sv);
     else
       ap::attn_warp_run<128, NSTA, FusedTaskMap, QR>(p, attn_base + aw * FS::WARP_BYTES, lane, tm);
 #ifdef HC_TIMELINE
@@ -175,7 +178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
 
 template <int GS, int NA, int NSTA, bool QR, bool TC, int NS, int EW>
 cudaError_t launch_cfg1(const pg::TcArgs& a0, const AttnParams& p0, const void* tmx, const void* tmw,
-                        const void* tmkv, int num_sms, cudaStream_t s) {
+                        const void* tmkv, const void* const* tms, int num_sms, cudaStream_t s) {
   constexpr int smem = 1024 + FusedSmem<GS, NA, NSTA, QR, TC, NS>::TOTAL;
   static_assert(smem <= 232448, "fused kernel exceeds 227 KiB of shared memory");
   auto k = fused_step_kernel<GS, NA, NSTA, QR, TC, NS, EW>;
@@ -188,14 +191,16 @@ cudaError_t launch_cfg1(const pg::TcArgs& a0, const AttnParams& p0, const void* 
   const int pairs = num_sms / 2;
   k<<<2 * pairs, pg::GEMM_THREADS + 32 * (NA + EW), smem, s>>>(*static_cast<const CUtensorMap*>(tmx),
                                                         *static_cast<const CUtensorMap*>(tmw),
-                                                        *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx), a, p);
+                                                        *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx),
+                                                        *static_cast<const CUtensorMap*>(tms[0] ? tms[0] : tmx),
+                                                        *static_cast<const CUtensorMap*>(tms[1] ? tms[1] : tmx), a, p);
   return cudaGetLastError();
 }
 template <int GS, int NA, int NSTA, bool QR, int NS = 2, int EW = 0>
 cudaError_t launch_cfg(const pg::TcArgs& a, const AttnParams& p, const void* tmx, const void* tmw, const void* tmkv,
-                       int num_sms, cudaStream_t s) {
-  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true, NS, EW>(a, p, tmx, tmw, tmkv, num_sms, s);
-  return launch_cfg1<GS, NA, NSTA, QR, false, NS, EW>(a, p, tmx, tmw, tmkv, num_sms, s);
+                       const void* const* tms, int num_sms, cudaStream_t s) {
+  if (p.tc) return launch_cfg1<GS, NA, NSTA, QR, true, NS, EW>(a, p, tmx, tmw, tmkv, tms, num_sms, s);
+  return launch_cfg1<GS, NA, NSTA, QR, false, NS, EW>(a, p, tmx, tmw, tmkv, tms, num_sms, s);
 }
 
 }  // namespace
@@ -209,7 +214,8 @@ int fused_tile_n() { return 256; }   // the narrowest tile (NSUB = 1): sizes per
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv,
-                         int* cfg_out) {
+                         int* cfg_out, const void* tmap_scr_k, const void* tmap_scr_v) {
+  const void* tms[2] = {tmap_scr_k, tmap_scr_v};
   pg::TcArgs a{};
   a.gather = rp.gather;
   a.n_hblocks = rp.n_hblocks;
@@ -281,8 +287,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   if (nsub == 1) {   // 256 x 256 tiles: 32-KiB stages, 4 of them (the same bytes in flight as 3 x 48)
     const int cfg = t.fused_cfg ? t.fused_cfg : (t_gemm < 0.5 * t_kv ? 382 : 452);
     if (cfg_out) *cfg_out = 10000 + cfg;
-    if (cfg == 382) return launch_cfg<3, 8, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-    return launch_cfg<4, 5, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+    if (cfg == 382) return launch_cfg<3, 8, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+    return launch_cfg<4, 5, 2, true, 1>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
   }
   // GQA: the tensor-core KV loop drains the KV stream early, so 2 attention warps suffice and
   // 4 extra epilogue warps split the G-query-head attend epilogue (cfg 3224)
@@ -293,13 +299,14 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // matters (cfg5 1/16..1/4: +4%).
   const bool epi_heavy = t_kv == 0.0 || (rp.d <= 6144 && t_kv < 0.05 * t_gemm);
   const int cfg = t.fused_cfg ? t.fused_cfg
-                              : (rp.H > rp.Hk ? 3224 : (epi_heavy ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352)));
+                              : ((rp.H > rp.Hk && rp.epi_attend) ? 3224
+                                                                  : (epi_heavy ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352)));
   if (cfg_out) *cfg_out = cfg;
-  if (cfg == 3224) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 3424) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
-  return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, num_sms, s);
+  if (cfg == 3224) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+  if (cfg == 3424) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+  if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+  if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+  return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
 }
 
 }  // namespace hc

@@ -24,6 +24,8 @@ struct Tuning {
   int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
   int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
   int kv_prefetch = 0;   // HC_KV_PF: KV chunks (of the current task) prefetched into L2 ahead of the smem ring
+  int gqa_scratch = -1;  // HC_GQA_SCRATCH: GQA hidden requests via rebuilt K/V scratch + the tensor-core KV loop
+                         // (-1 auto: for groups of >= 8 query heads; 0 never; 1 always)
   int attn_tc = 1;       // HC_ATTN_TC: KV attention on mma.sync (attn_tc.cuh): 0 never, 1 GQA only, 2 always
   int tc_1sm = 0;        // HC_TC_1SM: 1-SM tcgen05 reconstruction kernel instead of CTA pairs
   int tc_nsub = 0;       // HC_TC_NSUB: 1 = 256-wide pair tiles
@@ -186,7 +188,8 @@ bool dense_tc_supported(int d);
 cudaError_t launch_dense_tc(const DenseParams& p, const void* tmap_a, const void* tmap_w, int num_sms, cudaStream_t s);
 cudaError_t launch_dense_simt(const DenseParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s,
-                        const void* tmap_kv = nullptr);
+                        const void* tmap_kv = nullptr, const void* tmap_scr_k = nullptr,
+                        const void* tmap_scr_v = nullptr);
 // tensor-core KV attention (attn_tc.cuh) serves this shape: bf16, dh 64/128, G <= 8, Bkv % 16 == 0
 bool attn_tc_supported(int dtype, int dh, int G, int Bkv);
 bool attn_pipe_supported(int dtype, int dh, int B);
@@ -197,7 +200,8 @@ int fused_tile_m();
 int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s,
-                         const void* tmap_kv = nullptr, int* cfg_out = nullptr);
+                         const void* tmap_kv = nullptr, int* cfg_out = nullptr, const void* tmap_scr_k = nullptr,
+                         const void* tmap_scr_v = nullptr);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
                          void* out, float* lse, cudaStream_t s);

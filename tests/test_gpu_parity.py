@@ -905,7 +905,8 @@ def test_gqa_decode_vs_oracle(hc, d, H, dh, B, Hk):
 
 
 @pytest.mark.parametrize("env", [{"HC_FUSED": "0"}, {"HC_EPI_ATTEND": "0"}, {"HC_EPI_ATTEND": "0", "HC_FUSED": "0"},
-                                 {"HC_ATTN_TC": "0"}, {"HC_ATTN_TC": "0", "HC_FUSED": "0"}])
+                                 {"HC_ATTN_TC": "0"}, {"HC_ATTN_TC": "0", "HC_FUSED": "0"},
+                                 {"HC_GQA_SCRATCH": "1"}, {"HC_GQA_SCRATCH": "1", "HC_FUSED": "0"}])
 def test_gqa_alternative_paths(hc, monkeypatch, env):
     """GQA through the two-kernel path, the fused kernel with K/V scratch ([hblock][Hk][B][dh]),
     and the stand-alone GEMM + attention kernel, at the LLaMA-3-8B head layout."""
