@@ -46,6 +46,9 @@ shg = LayerShape("san-gqa", 1024, 8, 128, 2)
 wg = Workload("san-gqa", shg, 16, "bf16", 8, n, [0, 1, 0, 1, 1, 0, 1], list(range(len(n))), True)
 run(wg)
 run(Workload("san-gqa-kv", shg, 16, "bf16", 9, n, [0] * len(n), list(range(len(n))), False))
+# GQA with groups of 8 query heads: rebuilt K/V scratch + the tensor-core loop on hidden tasks
+shg8 = LayerShape("san-gqa8", 2048, 16, 128, 2)
+run(Workload("san-gqa8", shg8, 16, "bf16", 11, n, [0, 1, 0, 1, 1, 0, 1], list(range(len(n))), True))
 # tensor-core KV loop forced on a multi-head pool (knobs are read at pool create)
 os.environ["HC_ATTN_TC"] = "2"
 run(w)
