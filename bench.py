@@ -177,7 +177,7 @@ def run_reference(args, rank: int, world: int):
                 r["X"] = w.x(i)
             reqs.append(r)
         t0 = time.perf_counter()
-        O.decode_batch(reqs, Wd, H, w.scale, w.b_kv())
+        O.decode_batch(reqs, Wd, H, w.scale, w.b_kv(), n_kv_heads=w.shape.n_kv)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             t_total += dt
@@ -233,7 +233,7 @@ def cpu_baseline(w, budget_s: float = 20.0):
             else:
                 r["K"], r["V"] = w.kv(i)
             t0 = time.perf_counter()
-            O.decode_batch([r], Wd, H, w.scale, b)
+            O.decode_batch([r], Wd, H, w.scale, b, n_kv_heads=w.shape.n_kv)
             dt = time.perf_counter() - t0
             t_used += dt
             if is_h:
@@ -260,7 +260,7 @@ def cpu_baseline(w, budget_s: float = 20.0):
                 else:
                     r["K"], r["V"] = w.kv(i)
                 t0 = time.perf_counter()
-                O.decode_batch([r], Wd, H, w.scale, b)
+                O.decode_batch([r], Wd, H, w.scale, b, n_kv_heads=w.shape.n_kv)
                 single[key] = (time.perf_counter() - t0) / w.n[i] * 1e6
     except Exception as ex:   # reported, not fatal: the multi-thread number is the baseline
         single = {"error": f"{type(ex).__name__}: {ex}"[:200]}
