@@ -292,18 +292,20 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   }
   // GQA: the tensor-core KV loop drains the KV stream early, so 2 attention warps suffice and
   // 4 extra epilogue warps split the G-query-head attend epilogue (cfg 3224)
-  // Multi-head batches with a short K loop (d <= 6144) and a small KV stream, or no KV at
-  // all: 4 attention warps + 8 epilogue warps (cfg 3424; same-box A/B: cfg2 -1.7%, all-hidden
-  // cfg5 -0.7%).  At d = 9216 with any KV stream the 5th attention warp wins (cfg4 +3%, and
-  // the fused kernel's DRAM reads grow from 47 to 68 GB), as it does wherever the KV stream
-  // matters (cfg5 1/16..1/4: +4%).
-  const bool epi_heavy = t_kv == 0.0 || (rp.d <= 6144 && t_kv < 0.05 * t_gemm);
+  // GEMM-dominated batches (KV stream < 5% of the rebuild, or none) and GQA with the attend
+  // epilogue: 2 attention warps + 8 epilogue warps (cfg 3224: 12 warps keep 168 registers per
+  // thread; with 3-4 attention warps ptxas drops to 128 and spills).  Same-box A/B against
+  // <3,5,2>: cfg4 40.8 vs 41.2 ms (tensor pipe 88 vs 86%), cfg2 1.020 vs 1.040 ms, cfg3
+  // 3.62-3.67 vs 3.64-3.70 ms, all-hidden -0.7%; wherever the KV stream matters (cfg5
+  // 1/64..1/4) the attention warps win (+4% and more), so those batches keep <3,5,2> / <2,8,2>.
+  const bool epi_heavy = t_kv < 0.05 * t_gemm;
   const int cfg = t.fused_cfg ? t.fused_cfg
-                              : ((rp.H > rp.Hk && rp.epi_attend) ? 3224
-                                                                  : (epi_heavy ? 3424 : (t_gemm < 0.5 * t_kv ? 282 : 352)));
+                              : (((rp.H > rp.Hk && rp.epi_attend) || epi_heavy) ? 3224
+                                                                                 : (t_gemm < 0.5 * t_kv ? 282 : 352));
   if (cfg_out) *cfg_out = cfg;
   if (cfg == 3224) return launch_cfg<3, 2, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
   if (cfg == 3424) return launch_cfg<3, 4, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
+  if (cfg == 3324) return launch_cfg<3, 3, 2, true, 2, 4>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
   if (cfg == 342) return launch_cfg<3, 4, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
   if (cfg == 282) return launch_cfg<2, 8, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
   return launch_cfg<3, 5, 2, true>(a, ap_, tmap_x, tmap_w_half, tmap_kv, tms, num_sms, s);
