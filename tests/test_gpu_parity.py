@@ -794,14 +794,20 @@ def test_high_dynamic_range_softmax_on_the_fused_path(hc, q_scale):
 @pytest.mark.parametrize("cfg", ["cfg4", "cfg5:1/32"])
 def test_all_heads_of_the_longest_hidden_request_full_size(hc, cfg):
     """Full-size batch in the bench's launch configuration; the oracle checks EVERY head of the
-    longest hidden request (all 36 GEMM n-tiles at d = 9216) and of one KV request."""
+    longest hidden request (all 36 GEMM n-tiles at d = 9216), of 3 more hidden requests and of
+    24 KV-mode requests including the longest."""
     w = C.by_name(cfg)
     pool = T.make_pool(w)
     T.fill(pool, w)
     out, lse = T.decode(pool, w, T.queries(w))
     hid = [i for i in range(len(w.n)) if w.modes[i] == MODE_HIDDEN]
     kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
-    idx = [max(hid, key=lambda i: w.n[i]), max(kv, key=lambda i: w.n[i])]
+    rs = np.random.default_rng(5)
+    longest = max(hid, key=lambda i: w.n[i])
+    others = [i for i in hid if i != longest]
+    kv_longest = max(kv, key=lambda i: w.n[i])
+    kv_pick = [kv_longest] + [int(i) for i in rs.choice([i for i in kv if i != kv_longest], size=23, replace=False)]
+    idx = [longest] + [int(i) for i in rs.choice(others, size=min(3, len(others)), replace=False)] + kv_pick
     err, lerr = T.compare(w, out[idx], lse[idx], idx)
     assert err <= TOL_BF16, err
     assert lerr <= TOL_LSE, lerr
