@@ -534,6 +534,9 @@ def main():
     ap.add_argument("--no-gather", action="store_true",
                     help="N>1: skip the all-gather of every rank's out + lse over NCCL after each step "
                          "(north_star's output gather, on by default, inside the timed region)")
+    ap.add_argument("--fill", default="rr", choices=["rr", "seq"],
+                    help="cache fill order: rr = one block per request per round (blocks strided across the "
+                         "pool, the default recipe); seq = request by request (consecutive block ids)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay variant")
@@ -577,7 +580,7 @@ def main():
     w = shard_workload(args, w0, rank, world)
     pool = T.make_pool(w, device=local, split_tokens=args.split_tokens,
                        flags=hc.HC_FLAG_ABSORB_HIDDEN if args.absorb else 0, rope_theta=args.rope)
-    T.fill(pool, w, device=local)
+    T.fill(pool, w, device=local, order=args.fill)
     q = T.queries(w, device=local)
     ids = list(w.req_ids)
     n_req = len(ids)
@@ -782,6 +785,7 @@ def main():
                    "hidden_request_frac": sum(w.modes) / n_req, "parallelism": f"request-sharded x{world} ({'strong, LPT' if args.strong else 'weak'})",
                    "output_gather": gather.describe() if gather else "none",
                    "l2": "inputs larger than L2 (whole cache read every step)", "note": w.note,
+                   "fill": args.fill,
                    "variant": "absorbed hidden attention (NON-PAPER, HC_FLAG_ABSORB_HIDDEN)" if absorbed
                    else "paper (hidden K/V rebuilt every step)",
                    "rope_theta": args.rope},

@@ -105,7 +105,8 @@ template <int GS, int NA, int NSTA, bool QR, bool TC, int NS, int EW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 32 * (NA + EW), 1)
     fused_step_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                       const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_sk,
-                      const __grid_constant__ CUtensorMap tmap_sv, const pg::TcArgs a, const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tmap_sv, const __grid_constant__ CUtensorMap tmap_x128,
+                      const pg::TcArgs a, const AttnParams p) {
   constexpr int kGemmStages = GS;
   using FS = FusedSmem<GS, NA, NSTA, QR, TC, NS>;
   constexpr int kJoin = FS::kJoin;
@@ -130,7 +131,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS + 3
   }
 #endif
   if (warp < kGemmWarps) {
-    pg::pair_roles<NS, kGemmStages, EW ? 2 : 1, (EW > 0)>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+    pg::pair_roles<NS, kGemmStages, EW ? 2 : 1, (EW > 0)>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base,
+                                                         a.runs ? &tmap_x128 : nullptr);
 #ifdef HC_TIMELINE
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kGemmWarps) : "memory");
     if (threadIdx.x == 0) {
@@ -193,7 +195,8 @@ cudaError_t launch_cfg1(const pg::TcArgs& a0, const AttnParams& p0, const void* 
                                                         *static_cast<const CUtensorMap*>(tmw),
                                                         *static_cast<const CUtensorMap*>(tmkv ? tmkv : tmx),
                                                         *static_cast<const CUtensorMap*>(tms[0] ? tms[0] : tmx),
-                                                        *static_cast<const CUtensorMap*>(tms[1] ? tms[1] : tmx), a, p);
+                                                        *static_cast<const CUtensorMap*>(tms[1] ? tms[1] : tmx),
+                                                        *static_cast<const CUtensorMap*>(tms[2] ? tms[2] : tmx), a, p);
   return cudaGetLastError();
 }
 template <int GS, int NA, int NSTA, bool QR, int NS = 2, int EW = 0>
@@ -214,14 +217,15 @@ int fused_tile_n() { return 256; }   // the narrowest tile (NSUB = 1): sizes per
 
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s, const void* tmap_kv,
-                         int* cfg_out, const void* tmap_scr_k, const void* tmap_scr_v) {
-  const void* tms[2] = {tmap_scr_k, tmap_scr_v};
+                         int* cfg_out, const void* tmap_scr_k, const void* tmap_scr_v, const void* tmap_x128) {
+  const void* tms[3] = {tmap_scr_k, tmap_scr_v, tmap_x128};
   pg::TcArgs a{};
   a.gather = rp.gather;
   a.n_hblocks = rp.n_hblocks;
   a.B = rp.B;
   a.M = rp.n_hblocks * rp.B;
   a.rows_per_box = (rp.B < 128 && !t.diag_box) ? rp.B : 128;
+  a.runs = (tmap_x128 != nullptr && a.rows_per_box < 128) ? 1 : 0;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
   // Tile width: 256 x 512 pair tiles (NSUB = 2; one 512-column accumulator) whenever 2 dk is a
   // multiple of 512; 256 x 256 tiles with two accumulators (NSUB = 1) otherwise.  Measured on

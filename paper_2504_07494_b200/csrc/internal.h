@@ -24,6 +24,9 @@ struct Tuning {
   int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
   int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
   int kv_prefetch = 0;   // HC_KV_PF: KV chunks (of the current task) prefetched into L2 ahead of the smem ring
+  int block_runs = 0;    // HC_BLOCK_RUNS: 1 = runs of consecutive hidden blocks as one 128-row TMA box
+                         // (off: at cfg4 with request-by-request fills it lifted the tensor pipe to 93% but
+                         // raised L2/DRAM traffic 309 -> 418 / 46 -> 81 GB and the capped clock fell 10%)
   int gqa_scratch = -1;  // HC_GQA_SCRATCH: GQA hidden requests via rebuilt K/V scratch + the tensor-core KV loop
                          // (-1 auto: for groups of >= 8 query heads; 0 never; 1 always)
   int attn_tc = 1;       // HC_ATTN_TC: KV attention on mma.sync (attn_tc.cuh): 0 never, 1 GQA only, 2 always
@@ -181,7 +184,8 @@ cudaError_t launch_relayout_w(const void* w, void* w_int, const float* b, float*
 cudaError_t launch_recon_simt(const ReconParams& p, int dtype, cudaStream_t s);
 // tmap_w: W_int with 256-row boxes (1-SM kernel); tmap_w_half: 128-row boxes (CTA-pair kernel)
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
-                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s);
+                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s,
+                            const void* tmap_x128 = nullptr);
 bool recon_tc_supported(int d, int dk, int dh, int B);
 bool dense_tc_supported(int d);
 // tmap_a: A with {64 x 128} boxes; tmap_w: W with {64 x 128} boxes
@@ -201,7 +205,7 @@ int fused_tile_n();
 cudaError_t launch_fused(const ReconParams& rp, AttnParams ap, const void* tmap_x, const void* tmap_w_half,
                          int32_t* tile_done, int num_sms, const Tuning& t, cudaStream_t s,
                          const void* tmap_kv = nullptr, int* cfg_out = nullptr, const void* tmap_scr_k = nullptr,
-                         const void* tmap_scr_v = nullptr);
+                         const void* tmap_scr_v = nullptr, const void* tmap_x128 = nullptr);
 cudaError_t launch_combine(const CombineParams& p, int dtype, cudaStream_t s);
 cudaError_t launch_merge(int n_parts, int n_rows, int H, int dh, int dtype, const void* outs, const float* lses,
                          void* out, float* lse, cudaStream_t s);

@@ -34,6 +34,7 @@ constexpr int kMaxSyncPairs = 80;         // progress words reserved in the work
 struct TcArgs {
   const int32_t* gather;
   int32_t n_hblocks, M, B, rows_per_box;
+  int32_t runs;             // 1: fetch runs of consecutive pool blocks as one 128-row box (tmap_x128)
   int32_t m_tiles, n_tiles, k_iters;
   int32_t H, dh, d;         // H: K/V heads of the GEMM's K||V columns (= query heads unless GQA)
   int32_t grp;              // query heads per K/V head (GQA, R18; 1 = multi-head)
@@ -490,7 +491,8 @@ __device__ __forceinline__ void pair_setup(const PairSmem& s, int warp, int lane
 // warp < 6 (or < 10) only.  GQA2: compile the paired-query-head GQA epilogue in.
 template <int NSUB, int NSTAGE, int ESPLIT = 1, bool GQA2 = false>
 __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane, const CUtensorMap* tmap_x,
-                                           const CUtensorMap* tmap_w, const TcArgs& a, uint32_t tmem_base) {
+                                           const CUtensorMap* tmap_w, const TcArgs& a, uint32_t tmem_base,
+                                           const CUtensorMap* tmap_x128 = nullptr) {
   using PC = PairCfg<NSUB, NSTAGE>;
   constexpr int STAGES_ = PC::STAGES, NACC = PC::NACC;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -512,6 +514,10 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       const bool sync_on = a.sync != nullptr && leader && (pair ^ 1) < n_pairs;
       const int nbox = 128 / a.rows_per_box;
       const int box_bytes = a.rows_per_box * BK * 2;
+      // Runs of consecutive pool blocks (a request appended in one go gets consecutive ids,
+      // lowest free first) are fetched as ONE 128-row box instead of 128/B gathered ones: the
+      // smem image is identical (the 128-B swizzle repeats every 8 rows).
+      const bool runs_ok = tmap_x128 != nullptr && a.gather != nullptr && nbox > 1;
       for (int t = pair; t < n_tiles_total; t += n_pairs) {
         int mt, nt;
         tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
@@ -526,6 +532,12 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
             if (a.diag == 3 && i > 0) s.prow[i] = s.prow[0] + i * a.rows_per_box;   // timing diagnostic
 #endif
           }
+        }
+        bool one_box = runs_ok;
+        for (int i = 1; i < nbox && one_box; ++i) one_box = s.prow[i] == s.prow[0] + i * a.rows_per_box;
+        if (one_box) {   // and the first box's block must be a real one (rows past M gather block 0)
+          const int g0 = (mt * P_BM + (int)rank * 128) / a.B;
+          one_box = g0 + nbox * a.rows_per_box / a.B <= a.n_hblocks;
         }
         const int wrow = nt * PC::TILE_N + (int)rank * 128;
         for (int kb = 0; kb < a.k_iters; ++kb) {
@@ -544,7 +556,12 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
           if (leader) ptx::mbar_arrive_expect_tx(&s.full[stage], 2 * PC::STAGE_BYTES);
           uint8_t* dA = s.stages + stage * PC::STAGE_BYTES;
           uint8_t* dB = dA + P_A_BYTES;
-          if (a.l2_hint == 0) {
+          if (one_box) {
+            ptx::tma_load_2d_cg2(dA, tmap_x128, kb * BK, s.prow[0], &s.full[stage]);
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j)
+              ptx::tma_load_2d_cg2(dB + j * P_B_BYTES, tmap_w, kb * BK, wrow + j * 256, &s.full[stage]);
+          } else if (a.l2_hint == 0) {
             for (int i = 0; i < nbox; ++i)
               ptx::tma_load_2d_cg2(dA + i * box_bytes, tmap_x, kb * BK, s.prow[i], &s.full[stage]);
 #pragma unroll

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 template <int NSUB, int NSTAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS, 1)
     recon_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                     const pg::TcArgs a) {
+                     const __grid_constant__ CUtensorMap tmap_x128, const pg::TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
@@ -222,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *ps.tmem_slot;
-  pg::pair_roles<NSUB, NSTAGE>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base);
+  pg::pair_roles<NSUB, NSTAGE>(ps, warp, lane, &tmap_x, &tmap_w, a, tmem_base, a.runs ? &tmap_x128 : nullptr);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -230,7 +230,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pg::GEMM_THREADS, 1)
 }
 
 template <int NSUB, int NSTAGE>
-cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_half, int num_sms, cudaStream_t s) {
+cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_half, int num_sms, cudaStream_t s,
+                        const void* tmap_x128 = nullptr) {
+  a.runs = (tmap_x128 != nullptr && a.gather != nullptr && a.rows_per_box < 128) ? 1 : 0;
   using PC = pg::PairCfg<NSUB, NSTAGE>;
   constexpr int smem = 1024 + PC::REGION_BYTES;
   a.m_tiles = (a.M + pg::P_BM - 1) / pg::P_BM;
@@ -241,7 +243,8 @@ cudaError_t launch_pair(pg::TcArgs a, const void* tmap_x, const void* tmap_w_hal
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   if (pairs > pg::kMaxSyncPairs) a.sync = nullptr;
   recon_tc2_kernel<NSUB, NSTAGE><<<2 * pairs, pg::GEMM_THREADS, smem, s>>>(
-      *static_cast<const CUtensorMap*>(tmap_x), *static_cast<const CUtensorMap*>(tmap_w_half), a);
+      *static_cast<const CUtensorMap*>(tmap_x), *static_cast<const CUtensorMap*>(tmap_w_half),
+      *static_cast<const CUtensorMap*>(tmap_x128 ? tmap_x128 : tmap_x), a);
   return cudaGetLastError();
 }
 
@@ -289,7 +292,8 @@ bool recon_tc_supported(int d, int dk, int dh, int B) {
 }
 
 cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void* tmap_w,
-                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s) {
+                            const void* tmap_w_half, int num_sms, const Tuning& t, cudaStream_t s,
+                            const void* tmap_x128) {
   if (p.n_hblocks <= 0) return cudaSuccess;
   pg::TcArgs a{};
   a.gather = p.gather;
@@ -332,10 +336,10 @@ cudaError_t launch_recon_tc(const ReconParams& p, const void* tmap_x, const void
   if (pair_mode) {
     const bool can2 = (2 * p.dk) % 512 == 0;
     if (can2 && t.tc_nsub != 1) {
-      if (t.tc_stages == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s);
-      return launch_pair<2, 4>(a, tmap_x, tmap_w_half, num_sms, s);
+      if (t.tc_stages == 3) return launch_pair<2, 3>(a, tmap_x, tmap_w_half, num_sms, s, tmap_x128);
+      return launch_pair<2, 4>(a, tmap_x, tmap_w_half, num_sms, s, tmap_x128);
     }
-    return launch_pair<1, 6>(a, tmap_x, tmap_w_half, num_sms, s);
+    return launch_pair<1, 6>(a, tmap_x, tmap_w_half, num_sms, s, tmap_x128);
   }
   cudaError_t e = cudaFuncSetAttribute(recon_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;

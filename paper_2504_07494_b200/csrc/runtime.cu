@@ -183,6 +183,7 @@ Tuning tuning_from_env() {
   t.attn_tc = env_int("HC_ATTN_TC", t.attn_tc);
   t.kv_prefetch = env_int("HC_KV_PF", t.kv_prefetch);
   t.gqa_scratch = env_int("HC_GQA_SCRATCH", t.gqa_scratch);
+  t.block_runs = env_int("HC_BLOCK_RUNS", t.block_runs);
   t.tc_1sm = env_int("HC_TC_1SM", t.tc_1sm);
   t.tc_nsub = env_int("HC_TC_NSUB", t.tc_nsub);
   t.tc_stages = env_int("HC_TC_STAGES", t.tc_stages);
@@ -258,6 +259,8 @@ struct hc_pool {
   CUtensorMap tmap_wqkv{}, tmap_wo{};   // [W_Q; W_int] and W_O with 128-row boxes (dense pair GEMMs)
   CUtensorMap tmap_x64{};               // pool rows, {64 x min(B,64)} boxes (absorbed Z GEMM)
   CUtensorMap tmap_kv{};                // pool as rows of dh elements, {64 x 16} boxes, 128-B swizzle (KV chunks)
+  CUtensorMap tmap_x128{};              // pool rows, {64 x 128} boxes: runs of consecutive hidden blocks
+  bool x128_ok = false;
   bool attn_tc_ok = false;              // tmap_kv built and attn_tc_supported
   bool tc_ok = false;
   bool dense_tc_ok = false;             // bf16 tcgen05 path for the current-token / output GEMMs
@@ -621,6 +624,10 @@ hc_status hc_pool_create(const hc_pool_config* cfg, hc_pool** out) {
         return fail(HC_E_CUDA, "cuTensorMapEncodeTiled failed");
       }
       p->tc_ok = true;
+      // runs of consecutive hidden blocks as one 128-row box (B < 128)
+      p->x128_ok = cfg->block_size < 128 && p->tune.block_runs != 0 &&
+                   make_tmap_2d(&p->tmap_x128, p->storage + L.blocks_off, (uint64_t)cfg->d_model,
+                                (uint64_t)cfg->num_blocks * cfg->block_size, 64, 128);
     }
     if (attn_tc_supported(cfg->dtype, cfg->head_dim, cfg->n_heads / kg.Hk, kg.Bkv) &&
         !(cfg->flags & HC_FLAG_FORCE_SIMT)) {
@@ -1121,7 +1128,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     ap.n_kv_tasks = P.n_kv_splits * ap.th;
     ap.n_hid_splits = P.n_hid_splits;
     err = launch_fused(rp, ap, &pool->tmap_x, &pool->tmap_w_half, reinterpret_cast<int32_t*>(ws + P.off_tiledone),
-                       pool->num_sms, pool->tune, s, &pool->tmap_kv, &pool->last_cfg, psk, psv);
+                       pool->num_sms, pool->tune, s, &pool->tmap_kv, &pool->last_cfg, psk, psv,
+                       pool->x128_ok ? &pool->tmap_x128 : nullptr);
     if (err != cudaSuccess) return cuda_fail(err, "fused step kernel");
     ++launches;
     if (pool->profiling) {
@@ -1130,7 +1138,8 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
     }
   } else {
     if (P.n_hb > 0) {
-      err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, pool->tune, s)
+      err = pool->tc_ok ? launch_recon_tc(rp, &pool->tmap_x, &pool->tmap_w, &pool->tmap_w_half, pool->num_sms, pool->tune, s,
+                                          pool->x128_ok ? &pool->tmap_x128 : nullptr)
                         : launch_recon_simt(rp, pool->cfg.dtype, s);
       if (err != cudaSuccess) return cuda_fail(err, "reconstruction kernel");
       ++launches;

@@ -129,14 +129,21 @@ def test_single_token_returns_v1(hc):
     assert T.compare(w, out[[1]], lse[[1]], [1])[0] <= TOL_BF16
 
 
-def test_block_placement_is_bitwise_irrelevant(hc):
-    """Same logical content, different physical blocks => bitwise-identical output."""
-    w = _bf16_workload(256, 2, 128, 16)
+@pytest.mark.parametrize("d", [256, 1024])
+def test_block_placement_is_bitwise_irrelevant(hc, monkeypatch, d):
+    """Same logical content, different physical blocks => bitwise-identical output.  'seq'
+    fills give each request consecutive block ids; with HC_BLOCK_RUNS=1 the GEMM fetches runs of
+    8 blocks as one 128-row TMA box (same smem image as 8 gathered 16-row boxes)."""
+    n = [700, 33, 511, 1, 257, 96, 129, 64, 300, 17] if d == 1024 else N_MIX
+    w = _bf16_workload(d, d // 128, 128, 16, n=n)
     _, a, la = _run(w, split_tokens=64, order="rr")
     _, b, lb = _run(w, split_tokens=64, order="seq")
     _, c, lc = _run(w, split_tokens=64, order="shuffle")
-    assert np.array_equal(a, b) and np.array_equal(a, c)
-    assert np.array_equal(la, lb) and np.array_equal(la, lc)
+    monkeypatch.setenv("HC_BLOCK_RUNS", "1")
+    _, e, le = _run(w, split_tokens=64, order="seq")
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, e)
+    assert np.array_equal(la, lb) and np.array_equal(la, lc) and np.array_equal(la, le)
+    assert T.compare(w, b, lb, range(len(w.n)))[0] <= TOL_BF16
 
 
 @pytest.mark.parametrize("S", [16, 64, 512, 4096])
