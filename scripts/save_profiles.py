@@ -20,14 +20,21 @@ KEYS = ["dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__time_duration.sum"]
 
 
+def _page(rep, page):
+    """ncu page as CSV text: from a .ncu-rep, or from the <name>.<page>.csv export next to it."""
+    exp = rep[:-len(".ncu-rep")] + f".{page}.csv"
+    if os.path.exists(exp):
+        return open(exp).read()
+    return subprocess.run([NCU, "-i", rep, "--page", page, "--csv"], capture_output=True, text=True).stdout
+
+
 def raw(rep):
-    out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
+    rows = list(csv.reader(_page(rep, "raw").splitlines()))
     return {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
 
 
 def details(rep, title, out_name):
-    out = subprocess.run([NCU, "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    out = _page(rep, "details")
     rows = list(csv.reader(out.splitlines()))
     idx = {h: i for i, h in enumerate(rows[0])}
     lines = [f"{r[idx['Section Name']]}\t{r[idx['Metric Name']]}\t{r[idx['Metric Value']]} {r[idx['Metric Unit']]}"
@@ -61,7 +68,7 @@ traffic = {"_source": f"ncu --set full --clock-control none, one launch each ({t
                       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"}
 for rep, (title, wl, kern) in caps.items():
     path = os.path.join(src, rep + ".ncu-rep")
-    if not os.path.exists(path):
+    if not os.path.exists(path) and not os.path.exists(os.path.join(src, rep + ".details.csv")):
         print("missing", rep)
         continue
     nb, tp = details(path, title, f"{tag}_ncu_{rep[5:]}.txt")
