@@ -173,6 +173,7 @@ static cudaError_t launch_tc(const AttnParams& p, const void* tmap, const void* 
 cudaError_t launch_attn(const AttnParams& p, int dtype, bool generic, int num_sms, const Tuning& t, cudaStream_t s,
                         const void* tmap_kv, const void* tmap_scr_k, const void* tmap_scr_v) {
   if (p.n_tasks <= 0) return cudaSuccess;
+  if (t.attn_sms > 0 && t.attn_sms < num_sms) num_sms = t.attn_sms;   // measurement knob (per-SM KV rate)
   if (p.tc) {   // tensor-core loop (the runtime checked attn_tc_supported)
     if (p.dh == 128) return launch_tc<128, 8, 3>(p, tmap_kv, tmap_scr_k, tmap_scr_v, num_sms, s);
     return launch_tc<64, 8, 5>(p, tmap_kv, tmap_scr_k, tmap_scr_v, num_sms, s);

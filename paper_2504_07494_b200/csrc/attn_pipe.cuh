@@ -168,6 +168,7 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
   int ptask = grab();
   int pchunk = 0;
   int pnch = 0;
+  int plb = 0, prow = 0, phk = 0;   // logical block and row of the next chunk (kept incrementally: no divisions)
   SplitDesc psp{};
   ReqDesc prq{};
   int phead = 0;
@@ -178,6 +179,9 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       psp = p.splits[psplit];
       prq = p.reqs[psp.req];
       pnch = (psp.ntok + TOK - 1) / TOK;
+      plb = psp.lb0;
+      prow = 0;
+      phk = phead / p.G;
       tm.wait_ready(psplit, phead, psp, prq, lane);
     }
   };
@@ -189,9 +193,8 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
   auto produce = [&](int stage) -> bool {
     if (ptask >= p.n_tasks) return false;
     const int Bm = prq.mode == 0 ? p.Bkv : B;     // tokens per logical block of this mode
-    const int tok = psp.lb0 * Bm + pchunk * TOK;  // token index within the request
-    const int lb = tok / Bm, row = tok - lb * Bm;
-    const int hk = phead / p.G;                   // K/V head of this query head (GQA, R18)
+    const int lb = plb, row = prow;               // (lb0 * Bm + pchunk * TOK) as (block, row); Bm % TOK == 0
+    const int hk = phk;                           // K/V head of this query head (GQA, R18)
     const int rem = psp.ntok - pchunk * TOK;
     const int nvalid = rem < TOK ? rem : TOK;
     const bool first = pchunk == 0, last = pchunk == pnch - 1;
@@ -240,6 +243,11 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       if (stage == 0) qr0 = v;
       else if (stage == 1) qr1 = v;
       else qr2 = v;
+    }
+    prow += TOK;
+    if (prow >= Bm) {
+      prow -= Bm;
+      ++plb;
     }
     if (++pchunk == pnch) {
       ptask = grab();

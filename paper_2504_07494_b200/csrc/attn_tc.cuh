@@ -105,6 +105,7 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
     return __shfl_sync(FULL, t, 0);
   };
   int ptask = grab(), pchunk = 0, pnch = 0, psplit = 0, phk = 0;
+  int plb = 0, prow = 0;   // logical block and row of the next chunk (kept incrementally: no divisions)
   SplitDesc psp{};
   ReqDesc prq{};
   auto load_task = [&](int t) {
@@ -113,6 +114,8 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
       psp = p.splits[psplit];
       prq = p.reqs[psp.req];
       pnch = (psp.ntok + TOK - 1) / TOK;
+      plb = psp.lb0;
+      prow = 0;
       tm.wait_ready(psplit, phk, psp, prq, lane);
     }
   };
@@ -121,8 +124,7 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
     if (ptask >= p.n_tasks) return false;
     const bool hid = prq.mode != 0;
     const int Bm = hid ? p.B : p.Bkv;
-    const int tok = psp.lb0 * Bm + pchunk * TOK;
-    const int lb = tok / Bm, row = tok - lb * Bm;
+    const int lb = plb, row = prow;   // (lb0 * Bm + pchunk * TOK) as (block, row); Bm % TOK == 0
     const int rem = psp.ntok - pchunk * TOK;
     const bool first = pchunk == 0, last = pchunk == pnch - 1;
     if (lane == 0) {
@@ -151,6 +153,11 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
           ptx::tma_load_2d(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage]);
         }
       }
+    }
+    prow += TOK;
+    if (prow >= Bm) {
+      prow -= Bm;
+      ++plb;
     }
     if (++pchunk == pnch) {
       ptask = grab();

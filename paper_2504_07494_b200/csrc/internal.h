@@ -39,6 +39,7 @@ struct Tuning {
   int z_cfg = 1282;      // HC_Z_CFG (absorbed variant)
   int score_st = 2;      // HC_SCORE_ST (absorbed variant)
   int qt_bn = 128;       // HC_QT_BN (absorbed variant)
+  int attn_sms = 0;      // HC_ATTN_SMS: stand-alone attention kernel on at most this many SMs (measurement)
   int diag_epi = 0;      // -DHC_DIAG builds only: HC_DIAG_EPI (wrong outputs, timing only)
   int diag_box = 0;      // -DHC_DIAG builds only: HC_DIAG_BOX (wrong outputs, timing only)
   int diag_attn = 0;     // -DHC_DIAG builds only: HC_DIAG_ATTN (wrong outputs, timing only)

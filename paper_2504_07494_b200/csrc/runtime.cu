@@ -193,6 +193,7 @@ Tuning tuning_from_env() {
   t.z_cfg = env_int("HC_Z_CFG", t.z_cfg);
   t.score_st = env_int("HC_SCORE_ST", t.score_st);
   t.qt_bn = env_int("HC_QT_BN", t.qt_bn);
+  t.attn_sms = env_int("HC_ATTN_SMS", t.attn_sms);
 #ifdef HC_DIAG
   t.diag_epi = env_int("HC_DIAG_EPI", 0);
   t.diag_box = env_int("HC_DIAG_BOX", 0);

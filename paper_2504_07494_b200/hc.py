@@ -16,6 +16,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # HC_LIB_VARIANT=diag loads the diagnostic build (build.py --diag: timing modes, timeline
 # stamps) for experiments; the default is the shipped library.
 LIB_PATH = os.path.join(_HERE, "libhc_diag.so" if os.environ.get("HC_LIB_VARIANT") == "diag" else "libhc.so")
+# HC_LIB_FILE=<name>.so (same directory): another build of the library, for same-box A/B runs of
+# two code versions (scripts/env_ab.sh)
+if os.environ.get("HC_LIB_FILE"):
+    LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ["HC_LIB_FILE"]))
 
 HC_OK, HC_E_INVALID, HC_E_OOM, HC_E_UNKNOWN_REQ, HC_E_MODE_MISMATCH, HC_E_CUDA, HC_E_UNSUPPORTED, \
     HC_E_WORKSPACE = range(8)

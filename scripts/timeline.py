@@ -44,10 +44,16 @@ for name in sys.argv[1:]:
         spans.append(rel)
     rel = np.median(np.stack(spans), axis=0)
     kv_tasks = sum(-(-n // 512) for n, m in zip(w.n, w.modes) if m == 0) * w.shape.H
-    res = {"config": name, "diag_attn": os.environ.get("HC_DIAG_ATTN", "0"), "span_us": float(rel[:, 2].max()),
+    res = {"config": name, "diag_attn": os.environ.get("HC_DIAG_ATTN", "0"), "span_us": float(max(rel[:, 2].max(), rel[:, 1].max())),
            "gemm_drain_us": [float(np.min(rel[:, 1])), float(np.median(rel[:, 1])), float(np.max(rel[:, 1]))],
            "attn_first_warp_done_us": [float(np.min(rel[:, 4])), float(np.median(rel[:, 4]))],
            "attn_done_us": [float(np.min(rel[:, 2])), float(np.median(rel[:, 2])), float(np.max(rel[:, 2]))],
            "tasks_taken_at_median_drain": float(np.median(rel[:, 3])), "kv_tasks_total_approx": kv_tasks}
+    kvp = int(os.environ.get("HC_KV_PAIRS", "0"))
+    if kvp > 0:   # spatial split: CTAs [0, 2G) run the GEMM, the rest only stream KV
+        g = rel.shape[0] - 2 * kvp
+        res["gemm_ctas_drain_us"] = [float(np.min(rel[:g, 1])), float(np.median(rel[:g, 1])), float(np.max(rel[:g, 1]))]
+        res["kv_ctas_attn_done_us"] = [float(np.min(rel[g:, 2])), float(np.median(rel[g:, 2])), float(np.max(rel[g:, 2]))]
+        res["gemm_ctas_attn_done_us"] = [float(np.min(rel[:g, 2])), float(np.median(rel[:g, 2])), float(np.max(rel[:g, 2]))]
     print(json.dumps(res), flush=True)
     del pool
