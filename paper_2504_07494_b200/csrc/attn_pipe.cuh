@@ -186,7 +186,6 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     }
   };
   load_task(ptask);
-  const uint64_t kv_pol = (lane == 0 && p.kv_evict_first) ? ptx::policy_evict_first() : 0;
   uint4 qr0 = make_uint4(0, 0, 0, 0), qr1 = qr0, qr2 = qr0;   // QREG: q_h slot per stage
 
   // issue the next chunk of the producer stream into `stage`; false when no work is left
@@ -217,26 +216,10 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
       uint8_t* sb = stage_base + stage * C::STAGE;
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive_expect_tx(&bars[stage], 2 * C::CHUNK + (first ? C::QB : 0));
-      if (p.kv_evict_first && prq.mode == 0) {   // KV-mode chunks are read exactly once
-        ptx::bulk_g2s_hint(sb, ksrc, C::CHUNK, &bars[stage], kv_pol);
-        ptx::bulk_g2s_hint(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage], kv_pol);
-      } else {
-        ptx::bulk_g2s(sb, ksrc, C::CHUNK, &bars[stage]);
-        ptx::bulk_g2s(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage]);
-      }
+      ptx::bulk_g2s(sb, ksrc, C::CHUNK, &bars[stage]);
+      ptx::bulk_g2s(sb + C::CHUNK, vsrc, C::CHUNK, &bars[stage]);
       if (!QREG && first)
         ptx::bulk_g2s(sb + 2 * C::CHUNK, qg + (size_t)psp.req * d + phead * DH, C::QB, &bars[stage]);
-      if (p.kv_prefetch > 0 && prq.mode == 0) {   // L2 prefetch of a chunk kv_prefetch ahead (same task)
-        const int pc = pchunk + p.kv_prefetch;
-        if (pc < pnch) {
-          const int ptok = psp.lb0 * Bm + pc * TOK;
-          const int plb = ptok / Bm, prow = ptok - plb * Bm;
-          const int pkb = p.tables[prq.tab_off + 2 * plb], pvb = p.tables[prq.tab_off + 2 * plb + 1];
-          ptx::bulk_prefetch_l2(pool + (size_t)pkb * blk_elems + hk * kv_head_elems + (size_t)prow * DH, C::CHUNK);
-          ptx::bulk_prefetch_l2(pool + (size_t)pvb * blk_elems + p.v_off + hk * kv_head_elems + (size_t)prow * DH,
-                                C::CHUNK);
-        }
-      }
     }
     if (QREG && first) {   // every lane: its 8 dims of q_h (consumed when this stage is)
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(qg + (size_t)psp.req * d + phead * DH) + lane % LPR);
@@ -320,7 +303,11 @@ __device__ __forceinline__ void attn_warp_run(const AttnParams& p, uint8_t* wb, 
     const int row = idx * RPI + lg;
     const bool valid = row < mt.z;
     const float s = valid ? part[0] * p.scale_log2 : -INFINITY;
-    const float m_new = fmaxf(m_run, warp_max(s));
+    // lanes 2k and 2k+1 hold the same score: the max over the warp needs 4 levels, not 5
+    float smax = s;
+#pragma unroll
+    for (int o = 16; o > 1; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(FULL, smax, o));
+    const float m_new = fmaxf(m_run, smax);
     const uint16_t pj16 = bf16_bits(valid ? fast_exp2(s - m_new) : 0.f);   // the weight Σ p v uses
     const float pj = bf16_val(pj16);
     const float alpha = fast_exp2(m_run - m_new);   // 0 when m_run = -inf

@@ -96,7 +96,6 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
   const int64_t rows_per_unit = (int64_t)p.B * p.d / DH;   // pool rows of DH elements per unit block
   const int64_t v_rows = p.v_off / DH;
   const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q);
-  const uint64_t pol = (lane == 0 && p.kv_evict_first) ? ptx::policy_evict_first() : 0;
 
   // ---- producer (lane 0 issues; state warp-uniform)
   auto grab = [&]() -> int {
@@ -145,13 +144,8 @@ __device__ __forceinline__ void attn_warp_run_tc(const AttnParams& p, const CUte
       ptx::mbar_arrive_expect_tx(&bars[stage], C::STAGE);
 #pragma unroll
       for (int b = 0; b < C::NB; ++b) {
-        if (p.kv_evict_first && !hid) {
-          ptx::tma_load_2d_hint(sb + b * C::BOX, tk, b * 64, rk, &bars[stage], pol);
-          ptx::tma_load_2d_hint(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage], pol);
-        } else {
-          ptx::tma_load_2d(sb + b * C::BOX, tk, b * 64, rk, &bars[stage]);
-          ptx::tma_load_2d(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage]);
-        }
+        ptx::tma_load_2d(sb + b * C::BOX, tk, b * 64, rk, &bars[stage]);
+        ptx::tma_load_2d(sb + C::CHUNK + b * C::BOX, tv, b * 64, rv, &bars[stage]);
       }
     }
     prow += TOK;

@@ -22,8 +22,6 @@ struct Tuning {
   int sync_w = -1;       // HC_SYNC_W: partner k-lockstep window (-1: kernel default, 0 off)
   int group_m = -2;      // HC_GROUP_M: raster of the stand-alone reconstruction GEMM
   int l2_hint = 0;       // HC_L2HINT: L2 policy of the GEMM operand loads (pair_gemm.cuh TcArgs)
-  int kv_evict_first = 0;   // HC_KV_EF: KV-mode chunks streamed with L2 evict-first
-  int kv_prefetch = 0;   // HC_KV_PF: KV chunks (of the current task) prefetched into L2 ahead of the smem ring
   int block_runs = 0;    // HC_BLOCK_RUNS: 1 = runs of consecutive hidden blocks as one 128-row TMA box
                          // (off: at cfg4 with request-by-request fills it lifted the tensor pipe to 93% but
                          // raised L2/DRAM traffic 309 -> 418 / 46 -> 81 GB and the capped clock fell 10%)
@@ -93,11 +91,9 @@ struct AttnParams {
   const int32_t* tile_done;      // [gemm_m_tiles][gemm_n_tiles] finished epilogue warps (8 = ready)
   int32_t gemm_n_tiles, gemm_tile_m, gemm_tile_n;
   int32_t tile_target;           // finished epilogue warps per GEMM tile (8, or 16 with extra epilogue warps)
-  int32_t kv_evict_first;        // 1: KV chunks are streamed with an L2 evict-first policy
   int32_t th;                    // heads per split in the task numbering: H (SIMT loop) or Hk (tensor-core loop)
   int32_t tc;                    // 1: every task is a KV-mode split and runs attn_tc.cuh (task = split * Hk + kvhead)
   int32_t diag;                  // -DHC_DIAG builds only (HC_DIAG_ATTN): 1 skip the math, 2 read block 0 only
-  int32_t kv_prefetch;           // KV chunks ahead of the ring prefetched into L2 (0 = off)
 };
 
 struct CombineParams {

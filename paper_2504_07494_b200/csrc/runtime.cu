@@ -179,9 +179,7 @@ Tuning tuning_from_env() {
   t.sync_w = env_int("HC_SYNC_W", t.sync_w);
   t.group_m = env_int("HC_GROUP_M", t.group_m);
   t.l2_hint = env_int("HC_L2HINT", t.l2_hint);
-  t.kv_evict_first = env_int("HC_KV_EF", t.kv_evict_first);
   t.attn_tc = env_int("HC_ATTN_TC", t.attn_tc);
-  t.kv_prefetch = env_int("HC_KV_PF", t.kv_prefetch);
   t.gqa_scratch = env_int("HC_GQA_SCRATCH", t.gqa_scratch);
   t.block_runs = env_int("HC_BLOCK_RUNS", t.block_runs);
   t.tc_1sm = env_int("HC_TC_1SM", t.tc_1sm);
@@ -1054,9 +1052,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   ap.Bkv = Bkv;
   ap.v_off = pool->kv.v_off;
   ap.scale_log2 = scale * 1.4426950408889634f;
-  ap.kv_evict_first = pool->tune.kv_evict_first;
   ap.diag = pool->tune.diag_attn;
-  ap.kv_prefetch = pool->tune.kv_prefetch;
   pool->last_path = P.absorb && P.n_h > 0 ? 3 : (P.fused ? 1 : (P.n_hb > 0 ? 0 : 2));
   pool->last_cfg = 0;
   // tensor-core KV loop over the rebuilt-K/V scratch (GQA scratch mode): rows of dh elements

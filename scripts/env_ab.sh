@@ -1,6 +1,6 @@
 #!/bin/bash
 # Generic same-box A/B of library knobs (internal.h Tuning; read at pool create).
-#   VARIANTS="base|HC_KV_EF=1|HC_L2HINT=3" STEPS=100 bash scripts/env_ab.sh cfg5:1/32 cfg4
+#   VARIANTS="base|HC_L2HINT=3|HC_LIB_FILE=libhc_base.so" STEPS=100 bash scripts/env_ab.sh cfg5:1/32 cfg4
 # Each variant runs REPS times, interleaved, so box state (power, clocks) drifts evenly.
 VARIANTS=${VARIANTS:-base}
 IFS='|' read -ra VS <<< "$VARIANTS"
