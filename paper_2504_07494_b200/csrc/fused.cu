@@ -257,6 +257,10 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
   // HC_SYNC_W=<w> re-enables it with window w (the stand-alone GEMM keeps w = 8).
   a.sync_w = t.sync_w > 0 ? t.sync_w : 0;
   a.sync = (a.sync_w > 0 && num_sms / 2 <= pg::kMaxSyncPairs) ? rp.sync_counter : nullptr;
+  // Dynamic tile schedule (pair_gemm.cuh pair_roles): the pairs that share an A panel start its
+  // tiles together instead of drifting apart; the partner lockstep assumes the static stride.
+  a.tile_counter = t.dyn_tiles ? rp.tile_counter : nullptr;
+  if (a.tile_counter) a.sync = nullptr;
   if (rp.epi_attend) {   // hidden rows become partials in the GEMM epilogue: no hidden tasks
     a.epi = pg::EPI_ATTEND;
     a.hblk_req = rp.hblk_req;

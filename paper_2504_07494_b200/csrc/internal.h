@@ -37,6 +37,7 @@ struct Tuning {
   int z_cfg = 1282;      // HC_Z_CFG (absorbed variant)
   int score_st = 2;      // HC_SCORE_ST (absorbed variant)
   int qt_bn = 128;       // HC_QT_BN (absorbed variant)
+  int dyn_tiles = 1;     // HC_DYN_TILES: fused kernel takes GEMM tiles from a global counter (0: static stride)
   int attn_sms = 0;      // HC_ATTN_SMS: stand-alone attention kernel on at most this many SMs (measurement)
   int diag_epi = 0;      // -DHC_DIAG builds only: HC_DIAG_EPI (wrong outputs, timing only)
   int diag_box = 0;      // -DHC_DIAG builds only: HC_DIAG_BOX (wrong outputs, timing only)
@@ -117,6 +118,7 @@ struct ReconParams {
   int32_t d, H, dh, B;
   int32_t Hk, dk;         // K/V heads and K (or V) row width Hk*dh (GEMM N = 2 dk; GQA, R18)
   int32_t* sync_counter;  // >= 32*num_sms zeroed ints (pair progress words)
+  int32_t* tile_counter;  // one zeroed int: dynamic GEMM tile schedule of the fused kernel
   const int32_t* hblk_pos;  // token position of row 0 of each hidden block (RoPE / attend; nullable)
   const double* rope_inv;   // RoPE: inv_freq table [dh/2] (nullable = no RoPE)
   // ---- fused reconstruct-and-attend (epi_attend): the GEMM epilogue turns each segment of

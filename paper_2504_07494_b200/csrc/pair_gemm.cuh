@@ -70,6 +70,7 @@ struct TcArgs {
   int32_t epi_split;        // epilogue warps per TMEM lane quarter (1, or 2 with the fused kernel's extra
                             // epilogue warps: each takes every other head / column chunk)
   int32_t diag;             // -DHC_DIAG builds only (HC_DIAG_EPI): timing diagnostics with wrong outputs
+  int32_t* tile_counter;    // nullable: zeroed per launch; tiles handed out dynamically (see pair_roles)
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -450,7 +451,13 @@ struct PairSmem {
   uint64_t* tempty;
   uint32_t* tmem_slot;
   int32_t* prow;   // 16 gathered pool rows of the producer's current tile
+  // dynamic tile queue (TcArgs::tile_counter): the leader's producer grabs tile ids and hands
+  // them to every role of both CTAs through TQ slots
+  int32_t* tq;
+  uint64_t* tq_full;
+  uint64_t* tq_empty;
 };
+constexpr int TQ = 4;
 
 template <int NSUB, int NSTAGE>
 __device__ __forceinline__ PairSmem pair_carve(uint8_t* base /*1024-aligned*/) {
@@ -463,6 +470,11 @@ __device__ __forceinline__ PairSmem pair_carve(uint8_t* base /*1024-aligned*/) {
   s.tempty = s.tfull + 2;
   s.tmem_slot = reinterpret_cast<uint32_t*>(s.tempty + 2);
   s.prow = reinterpret_cast<int32_t*>(s.tempty + 4);
+  uint8_t* bar_base = base + PC::STAGES * PC::STAGE_BYTES;   // 512 B of barriers / control
+  static_assert(16 * NSTAGE + 112 <= 256, "pair barrier block");
+  s.tq = reinterpret_cast<int32_t*>(bar_base + 256);
+  s.tq_full = reinterpret_cast<uint64_t*>(bar_base + 256 + 16);
+  s.tq_empty = s.tq_full + TQ;
   return s;
 }
 
@@ -482,6 +494,12 @@ __device__ __forceinline__ void pair_setup(const PairSmem& s, int warp, int lane
       ptx::mbar_init(&s.tfull[i], 1);
       ptx::mbar_init(&s.tempty[i], 8 * EPI_SPLIT);   // 4 (or 8) epilogue warps x 2 CTAs (used on the leader)
     }
+    for (int i = 0; i < TQ; ++i) {
+      ptx::mbar_init(&s.tq_full[i], 1);
+      // released by every reader of the slot (used on the leader): the epilogue warps of both
+      // CTAs, the partner's producer and the MMA issuer
+      ptx::mbar_init(&s.tq_empty[i], 8 * EPI_SPLIT + 2);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_cg2<TMEM_COLS>(s.tmem_slot);
@@ -499,6 +517,26 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int n_tiles_total = a.m_tiles * a.n_tiles;
+  // Tile schedule.  Static: pair p takes tiles p, p + n_pairs, ...  Dynamic (a.tile_counter):
+  // the leader's producer takes the next tile id from a global counter when it starts a tile
+  // and publishes it in the TQ-slot queue to the partner's producer (st.shared::cluster +
+  // remote arrive), the MMA issuer and the epilogue warps of both CTAs; a tile id
+  // >= n_tiles_total ends every role.  Consecutive ids (the tiles that share an A panel in the
+  // n-major raster) then start at about the same time on whichever pairs are free, so the
+  // pairs that read an A panel stay together instead of drifting apart over hundreds of
+  // waves, and the panel is read from DRAM about once.
+  const bool dyn = a.tile_counter != nullptr;
+  int q_it = 0;   // queue slots consumed by this role
+  // consumer side of the queue (partner producer, MMA issuer, epilogue warps; the caller
+  // arrives on the leader's empty barrier after reading)
+  auto q_read = [&](int& t) -> uint32_t {
+    const int slot = q_it & (TQ - 1);
+    const uint32_t ph = (uint32_t)(q_it / TQ) & 1u;
+    ++q_it;
+    ptx::mbar_wait_cluster(&s.tq_full[slot], ph);
+    t = *reinterpret_cast<volatile int32_t*>(&s.tq[slot]);
+    return ptx::mapa(ptx::smem_u32(&s.tq_empty[slot]), 0);   // the leader's empty barrier
+  };
 
   if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
@@ -518,7 +556,25 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       // lowest free first) are fetched as ONE 128-row box instead of 128/B gathered ones: the
       // smem image is identical (the 128-B swizzle repeats every 8 rows).
       const bool runs_ok = tmap_x128 != nullptr && a.gather != nullptr && nbox > 1;
-      for (int t = pair; t < n_tiles_total; t += n_pairs) {
+      for (int t = pair;; t += n_pairs) {
+        if (dyn) {
+          if (leader) {
+            const int slot = q_it & (TQ - 1);
+            const uint32_t ph = (uint32_t)(q_it / TQ) & 1u;
+            ++q_it;
+            ptx::mbar_wait(&s.tq_empty[slot], ph ^ 1);
+            t = atomicAdd(a.tile_counter, 1);
+            if (t > n_tiles_total) t = n_tiles_total;
+            s.tq[slot] = t;
+            ptx::st_shared_cluster_u32(ptx::mapa(ptx::smem_u32(&s.tq[slot]), 1), (uint32_t)t);
+            ptx::mbar_arrive(&s.tq_full[slot]);
+            ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&s.tq_full[slot]), 1));
+          } else {
+            const uint32_t e = q_read(t);
+            ptx::mbar_arrive_cluster(e);
+          }
+        }
+        if (t >= n_tiles_total) break;
         int mt, nt;
         tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
         for (int i = 0; i < nbox; ++i) {
@@ -590,7 +646,9 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
+      for (int t = pair;; t += n_pairs, ++it) {
+        if (dyn) ptx::mbar_arrive_cluster(q_read(t));
+        if (t >= n_tiles_total) break;
         const int acc = it % NACC;
         const uint32_t acc_phase = (it / NACC) & 1;
         ptx::mbar_wait(&s.tempty[acc], acc_phase ^ 1);
@@ -627,7 +685,13 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
     const int row_in_tile = (int)rank * 128 + q * 32 + lane;
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&s.tempty[0]), 0);
     int it = 0;
-    for (int t = pair; t < n_tiles_total; t += n_pairs, ++it) {
+    for (int t = pair;; t += n_pairs, ++it) {
+      if (dyn) {
+        const uint32_t e = q_read(t);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(e);
+      }
+      if (t >= n_tiles_total) break;
       int mt, nt;
       tile_coords_p(t, a.m_tiles, a.n_tiles, a.group_m, mt, nt);
       const int acc = it % NACC;

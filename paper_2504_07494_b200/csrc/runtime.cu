@@ -42,7 +42,8 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 constexpr size_t kStagingBytes = 4u << 20;  // append descriptor staging inside storage
 constexpr int kRing = 16;  // pinned host staging buffers: the host may run up to 16 calls ahead
                            // of the GPU (absorbs host-side stalls, e.g. NVML polling)
-constexpr size_t kHeaderBytes = 128 + 128 * 80;  // zeroed each call: counter + 80 progress lines
+constexpr size_t kHeaderBytes = 128 + 128 * 80;  // zeroed each call: attention task counter (byte 0), GEMM
+                                                 // tile counter (byte 64), 80 pair-progress lines
 
 struct Req {
   int32_t mode = 0;
@@ -192,6 +193,7 @@ Tuning tuning_from_env() {
   t.score_st = env_int("HC_SCORE_ST", t.score_st);
   t.qt_bn = env_int("HC_QT_BN", t.qt_bn);
   t.attn_sms = env_int("HC_ATTN_SMS", t.attn_sms);
+  t.dyn_tiles = env_int("HC_DYN_TILES", t.dyn_tiles);
 #ifdef HC_DIAG
   t.diag_epi = env_int("HC_DIAG_EPI", 0);
   t.diag_box = env_int("HC_DIAG_BOX", 0);
@@ -1016,6 +1018,7 @@ hc_status hc_decode_attention(hc_pool* pool, int32_t n_req, const int64_t* req_i
   rp.dh = pool->cfg.head_dim;
   rp.B = B;
   rp.sync_counter = reinterpret_cast<int32_t*>(ws + 128);
+  rp.tile_counter = reinterpret_cast<int32_t*>(ws + 64);   // header word, zeroed per call
   rp.hblk_pos = (rope || P.attend) ? reinterpret_cast<const int32_t*>(ws + P.off_hpos) : nullptr;
   rp.rope_inv = rope ? reinterpret_cast<const double*>(pool->storage + pool->L.rope_off) : nullptr;
   rp.epi_attend = P.attend;
