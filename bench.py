@@ -781,6 +781,10 @@ def main():
                 "peak_kind": "HBM copy, " + peak_src}
     elif dom != "attention":
         peak = tf_peak
+        if k["achieved"] > tf_sus and peak == tf_sus:
+            # faster than the capped steady state: the clock dipped below 90% of max without the
+            # cap binding, so the burst peak is the honest denominator (never report frac > 1)
+            peak, tf_kind = tf_burst, "bf16 burst (achieved exceeds the sustained figure), " + peak_src
         fcfg = str(kernel_cfg % 10000)
         fname = (f"fused_step_kernel<{fcfg[0]},{fcfg[1]},{fcfg[2]}" + (f",+{fcfg[3]} epilogue warps" if len(fcfg) > 3 else "")
                  + (", 256x256 tiles" if kernel_cfg >= 10000 else "") + ">")
@@ -796,7 +800,10 @@ def main():
         roof = {"bound": "hbm", "kernel": "attn_pipe_kernel<128,8,3>", "achieved": k["achieved"], "peak": peak,
                 "unit": "GB/s", "frac": k["achieved"] / peak, "traffic": TRAFFIC.get(w.name, {}).get("attention"),
                 "peak_kind": "HBM copy, " + peak_src}
-    T_roof = max(F_alg / (tf_peak * 1e12), B_alg / (hbm * 1e9))
+    # the step's own FLOP rate above the sustained figure means it never reached the capped
+    # steady state: bound it by the burst peak (T_roof / T stays <= 1 for a tensor-bound step)
+    tf_step = tf_burst if (tf_peak == tf_sus and ms > 0 and F_alg / (ms * 1e-3) / 1e12 > tf_sus) else tf_peak
+    T_roof = max(F_alg / (tf_step * 1e12), B_alg / (hbm * 1e9))
     line = {
         "metric": METRIC, "value": value, "unit": "req-layers/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "step_ms_percentiles": pct, "higher_is_better": True,
