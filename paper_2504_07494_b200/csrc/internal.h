@@ -37,6 +37,7 @@ struct Tuning {
   int z_cfg = 1282;      // HC_Z_CFG (absorbed variant)
   int score_st = 2;      // HC_SCORE_ST (absorbed variant)
   int qt_bn = 128;       // HC_QT_BN (absorbed variant)
+  int epi_mma = 1;       // HC_EPI_MMA: attend epilogue on mma.sync (attend_tile_mma): 0 off, 1 GQA, 2 always
   int dyn_tiles = 1;     // HC_DYN_TILES: fused kernel takes GEMM tiles from a global counter (0: static stride)
   int attn_sms = 0;      // HC_ATTN_SMS: stand-alone attention kernel on at most this many SMs (measurement)
   int diag_epi = 0;      // -DHC_DIAG builds only: HC_DIAG_EPI (wrong outputs, timing only)

@@ -71,6 +71,7 @@ struct TcArgs {
                             // epilogue warps: each takes every other head / column chunk)
   int32_t diag;             // -DHC_DIAG builds only (HC_DIAG_EPI): timing diagnostics with wrong outputs
   int32_t* tile_counter;    // nullable: zeroed per launch; tiles handed out dynamically (see pair_roles)
+  int32_t epi_mma;          // EPI_ATTEND on mma.sync (attend_tile_mma): dh = 128, no RoPE, seg 16 or 32
 };
 
 // Epilogue modes.  gather == nullptr means dense A rows (row = m index, no block gather).
@@ -443,6 +444,183 @@ __device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc,
   }
 }
 
+// Attend epilogue on mma.sync (dh = 128, no RoPE; default for GQA).  Per 16 rows (tokens) of
+// the warp's TMEM lane quarter and per K/V head of the tile:
+//   S = K Q^T   m16n8k16 over dh: the K rows come out of a tcgen05.ld.16x256b load already in
+//               the A-fragment order (+ bias, split into bf16 hi + lo terms: two MMAs, scores as
+//               accurate as the fp32 path); Q^T of the segment's request (its G <= 8 query
+//               heads) is the B operand
+//   softmax per query head over the segment's tokens (3 shuffle levels), p rounded to bf16
+//   O = P^T V   P^T re-laid from the score fragment by 4 shuffles + prmt (A operand, rows =
+//               query heads); V's B fragments are the 16x256b load transposed by movmatrix
+// A segment (S tokens, never straddling a block) becomes one (m, l, acc[dh]) partial per query
+// head, as in attend_tile.  V is rounded to bf16 here (the per-row path keeps fp32).
+template <int S, int TILE_N, int NSPLIT>
+__device__ __forceinline__ void attend_tile_mma(const TcArgs& a, uint32_t tq, int nt, int row0, int lane, int sub) {
+  constexpr int DH = 128;
+  constexpr int HT = TILE_N / (2 * DH);
+  constexpr int NG = S / 16;   // 16-row groups per segment
+  static_assert(S == 16 || S == 32, "segments of 16 or 32 tokens");
+  const int g = lane >> 2, t = lane & 3;
+  const int G = a.grp;
+  const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+  const int srcA = 4 * (2 * t) + (g >> 1), srcB = 4 * (2 * t + 1) + (g >> 1);
+#pragma unroll 1
+  for (int j = sub; j < HT; j += NSPLIT) {
+    const int hk = nt * HT + j;
+    const int nk = nt * TILE_N + j * 2 * DH;   // bias column of K_hk; V_hk at + DH
+    const uint32_t tk = tq + j * 2 * DH;
+#pragma unroll 1
+    for (int sg = 0; sg < 32 / S; ++sg) {
+      const int r_seg = row0 + sg * S;   // first row of the segment (warp-uniform)
+      if (r_seg >= a.M) continue;
+      const int blk = r_seg / a.B;
+      const int req = a.hblk_req[blk];
+      const int tok0 = a.row_pos[blk] + (r_seg - blk * a.B);
+      const int n = a.reqs[req].n;
+      if (tok0 >= n) continue;   // a segment past n writes nothing
+      const bool qv = g < G;
+      const __nv_bfloat16* qh = a.q + (size_t)req * a.d + (size_t)(hk * G + (qv ? g : 0)) * DH;
+      uint32_t qb[8][2];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qb[kk][0] = qv ? __ldg(reinterpret_cast<const uint32_t*>(qh + 16 * kk + 2 * t)) : 0u;
+        qb[kk][1] = qv ? __ldg(reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8 + 2 * t)) : 0u;
+      }
+      // ---- scores
+      float sc[NG][4];
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+        sc[gi][0] = sc[gi][1] = sc[gi][2] = sc[gi][3] = 0.f;
+        const uint32_t tg = tk + ((uint32_t)(16 * (sg * NG + gi)) << 16);
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {   // 4 k-slices per TMEM wait
+          uint32_t r[4][8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ptx::tmem_ld_16x256b_x2(tg + 64 * kb + 16 * i, r[i]);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kk = 4 * kb + i;
+            float2 b0 = make_float2(0.f, 0.f), b1 = b0;
+            if (a.bias) {
+              b0 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * kk + 2 * t));
+              b1 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * kk + 8 + 2 * t));
+            }
+            // k = k_hi + k_lo (two bf16 terms: ~16 mantissa bits), so q.k keeps fp32-level
+            // accuracy — the softmax exponentiates score errors (peaky scores)
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 bb = e < 2 ? b0 : b1;
+              const float x0 = __uint_as_float(r[i][2 * e]) + bb.x, x1 = __uint_as_float(r[i][2 * e + 1]) + bb.y;
+              hi[e] = pack_bf16(x0, x1);
+              lo[e] = pack_bf16(x0 - __uint_as_float(hi[e] << 16), x1 - __uint_as_float(hi[e] & 0xffff0000u));
+            }
+            ptx::mma_bf16_16816(sc[gi], hi[0], hi[1], hi[2], hi[3], qb[kk][0], qb[kk][1]);
+            ptx::mma_bf16_16816(sc[gi], lo[0], lo[1], lo[2], lo[3], qb[kk][0], qb[kk][1]);
+          }
+        }
+      }
+      // ---- mask, scale, per-query-head max over the segment's tokens
+      const bool cv0 = 2 * t < G, cv1 = 2 * t + 1 < G;
+      float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = gi * 16 + g + (e >= 2 ? 8 : 0);
+          const bool ok = (tok0 + row < n) && (r_seg + row < a.M) && ((e & 1) ? cv1 : cv0);
+          sc[gi][e] = ok ? sc[gi][e] * a.scale_log2 : -INFINITY;
+        }
+        m0 = fmaxf(m0, fmaxf(sc[gi][0], sc[gi][2]));
+        m1 = fmaxf(m1, fmaxf(sc[gi][1], sc[gi][3]));
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(kFull, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(kFull, m1, o));
+      }
+      // ---- p (rounded once to bf16: the weight P^T V uses and the one l sums)
+      float l0 = 0.f, l1 = 0.f;
+      uint32_t pk[NG][2];
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+        float pv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float mm = (e & 1) ? m1 : m0;
+          pv[e] = sc[gi][e] == -INFINITY ? 0.f : __bfloat162float(__float2bfloat16_rn(exp2f(sc[gi][e] - mm)));
+        }
+        l0 += pv[0] + pv[2];
+        l1 += pv[1] + pv[3];
+        pk[gi][0] = pack_bf16(pv[0], pv[1]);
+        pk[gi][1] = pack_bf16(pv[2], pv[3]);
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(kFull, l0, o);
+        l1 += __shfl_xor_sync(kFull, l1, o);
+      }
+      // ---- O = P^T V over the segment's 16-token groups, 64 output dims at a time
+      uint32_t pa[NG][2];
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+        const uint32_t X = __shfl_sync(kFull, pk[gi][0], srcA), Y = __shfl_sync(kFull, pk[gi][0], srcB);
+        const uint32_t Z = __shfl_sync(kFull, pk[gi][1], srcA), W = __shfl_sync(kFull, pk[gi][1], srcB);
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(pa[gi][0]) : "r"(X), "r"(Y), "r"(sel));
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(pa[gi][1]) : "r"(Z), "r"(W), "r"(sel));
+      }
+      const float mA = __shfl_sync(kFull, m0, g >> 1), mB = __shfl_sync(kFull, m1, g >> 1);
+      const float lA = __shfl_sync(kFull, l0, g >> 1), lB = __shfl_sync(kFull, l1, g >> 1);
+      const int split = a.reqs[req].split_begin + tok0 / S;
+      const size_t task = (size_t)(hk * G + (qv ? g : 0)) * a.n_splits_all + split;   // head-major partial index
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        float o[8][4];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+          const uint32_t tg = tk + DH + half * 64 + ((uint32_t)(16 * (sg * NG + gi)) << 16);
+          uint32_t rv[4][8];
+#pragma unroll
+          for (int c2 = 0; c2 < 4; ++c2) ptx::tmem_ld_16x256b_x2(tg + 16 * c2, rv[c2]);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 4; ++c2) {
+            const uint32_t (&r)[8] = rv[c2];
+            float2 b0 = make_float2(0.f, 0.f), b1 = b0;
+            if (a.bias) {
+              const float* bv = a.bias + nk + DH + half * 64 + 16 * c2 + 2 * t;
+              b0 = __ldg(reinterpret_cast<const float2*>(bv));
+              b1 = __ldg(reinterpret_cast<const float2*>(bv + 8));
+            }
+            const uint32_t u0 = pack_bf16(__uint_as_float(r[0]) + b0.x, __uint_as_float(r[1]) + b0.y);
+            const uint32_t u1 = pack_bf16(__uint_as_float(r[2]) + b0.x, __uint_as_float(r[3]) + b0.y);
+            const uint32_t u2 = pack_bf16(__uint_as_float(r[4]) + b1.x, __uint_as_float(r[5]) + b1.y);
+            const uint32_t u3 = pack_bf16(__uint_as_float(r[6]) + b1.x, __uint_as_float(r[7]) + b1.y);
+            ptx::mma_bf16_16816(o[2 * c2], pa[gi][0], 0u, pa[gi][1], 0u, ptx::movmatrix_trans(u0),
+                                ptx::movmatrix_trans(u1));
+            ptx::mma_bf16_16816(o[2 * c2 + 1], pa[gi][0], 0u, pa[gi][1], 0u, ptx::movmatrix_trans(u2),
+                                ptx::movmatrix_trans(u3));
+          }
+        }
+        // ---- emit: lane (g, t) holds O[query head g][dims half*64 + 8 nb + 2t, + 1]
+        if (qv) {
+          float* dst = a.part_acc + task * DH + half * 64 + 2 * t;
+#pragma unroll
+          for (int nb = 0; nb < 8; ++nb) *reinterpret_cast<float2*>(dst + 8 * nb) = make_float2(o[nb][0], o[nb][1]);
+        }
+      }
+      if (qv && t == 0) {
+        a.part_ml[2 * task] = (g & 1) ? mB : mA;
+        a.part_ml[2 * task + 1] = (g & 1) ? lB : lA;
+      }
+    }
+  }
+}
+
 struct PairSmem {
   uint8_t* stages;
   uint64_t* full;
@@ -719,8 +897,14 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
 #endif
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
         bool done = false;
+        if (a.epi_mma) {   // mma.sync attend epilogue (the runtime checked dh = 128, no RoPE)
+          const int row0 = mt * P_BM + (int)rank * 128 + q * 32;
+          if (a.seg == 16) attend_tile_mma<16, PC::TILE_N, ESPLIT>(a, tacc, nt, row0, lane, esub);
+          else attend_tile_mma<32, PC::TILE_N, ESPLIT>(a, tacc, nt, row0, lane, esub);
+          done = true;
+        }
         if constexpr (GQA2) {
-          if (a.grp % 2 == 0) {   // GQA: query heads two at a time
+          if (!done && a.grp % 2 == 0) {   // GQA: query heads two at a time
             if (a.seg == 8) attend_tile_gqa2<8, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
             else if (a.seg == 16) attend_tile_gqa2<16, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);
             else attend_tile_gqa2<32, PC::TILE_N, ESPLIT>(a, tacc, nt, grow, lane, esub);

@@ -1024,3 +1024,45 @@ def test_tensor_core_kv_loop_on_multihead(hc, monkeypatch, shape):
     _, out, lse = _run(w4)
     err, lerr = T.compare(w4, out, lse, range(len(n)))
     assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+
+
+# ------------------------------------------------------------------ attend epilogue on mma.sync
+EPI_MMA_SHAPES = [
+    (4096, 32, 128, 16, 8),    # LLaMA-3-8B layer, G = 4, 16-token segments
+    (4096, 32, 128, 16, 4),    # Yi-6B layer, G = 8 (attend path now, not the scratch mode)
+    (2048, 16, 128, 32, 4),    # B = 32: 32-token segments (two 16-row groups per segment)
+]
+
+
+@pytest.mark.parametrize("q_scale", [1.0, 4.0, 32.0])
+@pytest.mark.parametrize("d,H,dh,B,Hk", EPI_MMA_SHAPES)
+def test_gqa_mma_epilogue_vs_oracle(hc, d, H, dh, B, Hk, q_scale):
+    """The GQA attend epilogue on mma.sync (pair_gemm.cuh attend_tile_mma, default for GQA):
+    S = (K_hi + K_lo) Q^T, per-segment softmax, O = P^T V with movmatrix-transposed V fragments.
+    Normal, peaky (q x4) and argmax-like (q x32) scores; segment lengths 16 and 32; ragged
+    requests (tokens past n inside the last block, rows past M in the last tile)."""
+    n = [1, 17, 300, 129, 64, 511, 33, 1000, 16, 15]
+    modes = [MODE_HIDDEN if i % 3 != 1 else MODE_KV for i in range(len(n))]
+    shape = LayerShape(f"mma-{d}-gqa{Hk}", d, H, dh, Hk)
+    w = Workload(f"mma-{d}-{B}", shape, B, "bf16", 23 + int(q_scale), n, modes, list(range(len(n))), True,
+                 q_scale=q_scale)
+    pool, out, lse = _run(w)
+    assert pool.last_decode_path() == 1
+    assert np.isfinite(out).all() and np.isfinite(lse).all()
+    err, lerr = T.compare(w, out, lse, range(len(n)))
+    assert err <= TOL_BF16, err
+    assert lerr <= TOL_LSE * max(1.0, float(np.abs(lse).max()) / 10), lerr
+
+
+def test_gqa_mma_epilogue_agrees_with_the_per_row_epilogue(hc, monkeypatch):
+    """HC_EPI_MMA=0 restores the per-row (fp32 CUDA-core) attend epilogue: both within the bf16
+    bar of each other, KV-mode rows (same KV warps) bit-identical."""
+    d, H, dh, B, Hk = 4096, 32, 128, 16, 8
+    w = _bf16_workload(d, H, dh, B, n=[5, 300, 129, 1000, 64], bias=True, Hk=Hk)
+    _, a, la = _run(w)
+    monkeypatch.setenv("HC_EPI_MMA", "0")
+    _, b, lb = _run(w)
+    from oracle import hc_oracle as O
+    assert O.max_rel_err(a, b, H) <= 2 * TOL_BF16
+    kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
+    assert np.array_equal(a[kv], b[kv]) and np.array_equal(la[kv], lb[kv])
