@@ -273,8 +273,8 @@ cudaError_t launch_fused(const ReconParams& rp, AttnParams ap_, const void* tmap
     a.seg = rp.seg;
     tile_done = nullptr;
     a.diag = t.diag_epi;
-    // the attend epilogue on mma.sync (pair_gemm.cuh attend_tile_mma): dh = 128, no RoPE
-    a.epi_mma = (rp.dh == 128 && rp.rope_inv == nullptr && (rp.seg == 16 || rp.seg == 32) &&
+    // the attend epilogue on mma.sync (pair_gemm.cuh attend_tile_mma): dh = 128
+    a.epi_mma = (rp.dh == 128 && (rp.seg == 16 || rp.seg == 32) &&
                  (t.epi_mma == 2 || (t.epi_mma == 1 && rp.H > rp.Hk))) ? 1 : 0;
   }
   a.epi_split = 1;

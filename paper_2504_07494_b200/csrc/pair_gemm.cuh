@@ -444,7 +444,7 @@ __device__ __forceinline__ void attend_tile_gqa2(const TcArgs& a, uint32_t tacc,
   }
 }
 
-// Attend epilogue on mma.sync (dh = 128, no RoPE; default for GQA).  Per 16 rows (tokens) of
+// Attend epilogue on mma.sync (dh = 128; default for GQA).  Per 16 rows (tokens) of
 // the warp's TMEM lane quarter and per K/V head of the tile:
 //   S = K Q^T   m16n8k16 over dh: the K rows come out of a tcgen05.ld.16x256b load already in
 //               the A-fragment order (+ bias, split into bf16 hi + lo terms: two MMAs, scores as
@@ -493,32 +493,63 @@ __device__ __forceinline__ void attend_tile_mma(const TcArgs& a, uint32_t tq, in
       for (int gi = 0; gi < NG; ++gi) {
         sc[gi][0] = sc[gi][1] = sc[gi][2] = sc[gi][3] = 0.f;
         const uint32_t tg = tk + ((uint32_t)(16 * (sg * NG + gi)) << 16);
+        // slices kk and kk + 4 hold columns c and c + 64 = the RoPE partners (dh = 128)
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb) {   // 4 k-slices per TMEM wait
           uint32_t r[4][8];
+          const int ks[4] = {2 * kb, 2 * kb + 1, 2 * kb + 4, 2 * kb + 5};
 #pragma unroll
-          for (int i = 0; i < 4; ++i) ptx::tmem_ld_16x256b_x2(tg + 64 * kb + 16 * i, r[i]);
+          for (int i = 0; i < 4; ++i) ptx::tmem_ld_16x256b_x2(tg + 16 * ks[i], r[i]);
           ptx::tmem_ld_wait();
+          float x[4][8];   // fp32 K (+ bias): x[i][2e + h] = row (e & 1 ? g + 8 : g), col 16 ks[i] + 2t + h (+ 8 if e >= 2)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int kk = 4 * kb + i;
             float2 b0 = make_float2(0.f, 0.f), b1 = b0;
             if (a.bias) {
-              b0 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * kk + 2 * t));
-              b1 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * kk + 8 + 2 * t));
+              b0 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * ks[i] + 2 * t));
+              b1 = __ldg(reinterpret_cast<const float2*>(a.bias + nk + 16 * ks[i] + 8 + 2 * t));
             }
-            // k = k_hi + k_lo (two bf16 terms: ~16 mantissa bits), so q.k keeps fp32-level
-            // accuracy — the softmax exponentiates score errors (peaky scores)
+            x[i][0] = __uint_as_float(r[i][0]) + b0.x;   // row g,   col 2t
+            x[i][1] = __uint_as_float(r[i][1]) + b0.y;   // row g,   col 2t+1
+            x[i][2] = __uint_as_float(r[i][2]) + b0.x;   // row g+8, col 2t
+            x[i][3] = __uint_as_float(r[i][3]) + b0.y;   // row g+8, col 2t+1
+            x[i][4] = __uint_as_float(r[i][4]) + b1.x;   // row g,   col 2t+8
+            x[i][5] = __uint_as_float(r[i][5]) + b1.y;
+            x[i][6] = __uint_as_float(r[i][6]) + b1.x;   // row g+8, col 2t+8
+            x[i][7] = __uint_as_float(r[i][7]) + b1.y;
+          }
+          if (a.rope_inv != nullptr) {   // rotate (c, c + 64) by pos * inv_freq[c] (rope_rotate's convention)
+            constexpr double kTwoPi = 6.283185307179586476925286766559;
+            const int pos0 = tok0 + gi * 16 + g;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int c = 16 * ks[i] + 2 * t + (e & 1) + (e >= 4 ? 8 : 0);
+                const int pos = pos0 + ((e >> 1) & 1) * 8;
+                const double ang = (double)pos * __ldg(a.rope_inv + c);
+                const double kq = rint(ang * (1.0 / kTwoPi));
+                float sn, cs;
+                __sincosf((float)fma(-kq, kTwoPi, ang), &sn, &cs);
+                const float x0 = x[i][e], y0 = x[i + 2][e];
+                x[i][e] = x0 * cs - y0 * sn;
+                x[i + 2][e] = y0 * cs + x0 * sn;
+              }
+            }
+          }
+          // k = k_hi + k_lo (two bf16 terms: ~16 mantissa bits), so q.k keeps fp32-level
+          // accuracy — the softmax exponentiates score errors (peaky scores)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 bb = e < 2 ? b0 : b1;
-              const float x0 = __uint_as_float(r[i][2 * e]) + bb.x, x1 = __uint_as_float(r[i][2 * e + 1]) + bb.y;
+              const float x0 = x[i][2 * e], x1 = x[i][2 * e + 1];
               hi[e] = pack_bf16(x0, x1);
               lo[e] = pack_bf16(x0 - __uint_as_float(hi[e] << 16), x1 - __uint_as_float(hi[e] & 0xffff0000u));
             }
-            ptx::mma_bf16_16816(sc[gi], hi[0], hi[1], hi[2], hi[3], qb[kk][0], qb[kk][1]);
-            ptx::mma_bf16_16816(sc[gi], lo[0], lo[1], lo[2], lo[3], qb[kk][0], qb[kk][1]);
+            ptx::mma_bf16_16816(sc[gi], hi[0], hi[1], hi[2], hi[3], qb[ks[i]][0], qb[ks[i]][1]);
+            ptx::mma_bf16_16816(sc[gi], lo[0], lo[1], lo[2], lo[3], qb[ks[i]][0], qb[ks[i]][1]);
           }
         }
       }
@@ -897,7 +928,7 @@ __device__ __forceinline__ void pair_roles(const PairSmem& s, int warp, int lane
 #endif
         const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * PC::TILE_N;
         bool done = false;
-        if (a.epi_mma) {   // mma.sync attend epilogue (the runtime checked dh = 128, no RoPE)
+        if (a.epi_mma) {   // mma.sync attend epilogue (the runtime checked dh = 128)
           const int row0 = mt * P_BM + (int)rank * 128 + q * 32;
           if (a.seg == 16) attend_tile_mma<16, PC::TILE_N, ESPLIT>(a, tacc, nt, row0, lane, esub);
           else attend_tile_mma<32, PC::TILE_N, ESPLIT>(a, tacc, nt, row0, lane, esub);

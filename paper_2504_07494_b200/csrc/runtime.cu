@@ -382,9 +382,9 @@ struct hc_pool {
     // whole query group per task instead of the attend epilogue serving G heads per K/V head
     // (auto for G >= 8: the attend epilogue's cost grows with G while the scratch round trip
     // does not — same-box A/B: Yi-6B (G 8) 1.27 vs 1.40-1.44 ms, LLaMA-3-8B (G 4) 2.54 vs 2.51 ms)
-    // With the attend epilogue on mma.sync (HC_EPI_MMA, dh 128 without RoPE) the epilogue's cost
-    // no longer grows with G and the attend path wins for G = 8 too (Yi-6B 1.23-1.25 vs 1.27 ms).
-    const bool epi_mma_ok = tune.epi_mma != 0 && dh == 128 && cfg.rope_theta <= 0.f;
+    // With the attend epilogue on mma.sync (HC_EPI_MMA, dh 128) the epilogue's cost no longer
+    // grows with G and the attend path wins for G = 8 too (Yi-6B 1.24-1.25 vs 1.29-1.32 ms).
+    const bool epi_mma_ok = tune.epi_mma != 0 && dh == 128;
     P.gqa_scratch = !P.absorb && tc_ok && attn_tc_ok && kv.Hk < H && tune.attn_tc != 0 &&
                     (tune.gqa_scratch == 1 || (tune.gqa_scratch < 0 && H / kv.Hk >= 8 && !epi_mma_ok));
     P.attend = !P.absorb && tc_ok && cfg.dtype == HC_BF16 && tune.epi_attend != 0 && recon_pair_mode(B, tune) &&

@@ -1066,3 +1066,20 @@ def test_gqa_mma_epilogue_agrees_with_the_per_row_epilogue(hc, monkeypatch):
     assert O.max_rel_err(a, b, H) <= 2 * TOL_BF16
     kv = [i for i in range(len(w.n)) if w.modes[i] == MODE_KV]
     assert np.array_equal(a[kv], b[kv]) and np.array_equal(la[kv], lb[kv])
+
+
+@pytest.mark.parametrize("d,H,dh,B,Hk", EPI_MMA_SHAPES)
+def test_gqa_mma_epilogue_with_rope(hc, d, H, dh, B, Hk):
+    """RoPE inside the mma epilogue: columns c and c + 64 of K are the 16x256b slices kk and
+    kk + 4, rotated in registers at each row's token position before the hi/lo split; long
+    contexts (positions into the thousands) and ragged last blocks."""
+    n = [1, 17, 300, 4000, 129, 64, 2049, 33]
+    modes = [MODE_HIDDEN if i % 3 != 1 else MODE_KV for i in range(len(n))]
+    shape = LayerShape(f"mma-rope-{d}-gqa{Hk}", d, H, dh, Hk)
+    w = Workload(f"mma-rope-{d}-{B}", shape, B, "bf16", 31, n, modes, list(range(len(n))), True)
+    pool = T.make_pool(w, rope_theta=ROPE_THETA)
+    T.fill(pool, w)
+    out, lse = T.decode(pool, w, T.queries(w))
+    assert pool.last_decode_path() == 1
+    err, lerr = T.compare(w, out, lse, range(len(n)), rope_theta=ROPE_THETA)
+    assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
