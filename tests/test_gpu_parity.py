@@ -1031,6 +1031,8 @@ EPI_MMA_SHAPES = [
     (4096, 32, 128, 16, 8),    # LLaMA-3-8B layer, G = 4, 16-token segments
     (4096, 32, 128, 16, 4),    # Yi-6B layer, G = 8 (attend path now, not the scratch mode)
     (2048, 16, 128, 32, 4),    # B = 32: 32-token segments (two 16-row groups per segment)
+    (1024, 8, 128, 64, 4),     # B = 64: blocks of two segments, G = 2
+    (2048, 16, 128, 256, 2),   # B = 256: a block spans a whole M tile, G = 8
 ]
 
 
