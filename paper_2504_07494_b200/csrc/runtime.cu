@@ -360,7 +360,8 @@ struct hc_pool {
 
   int32_t split_tokens_auto(const std::vector<const Req*>& rs) const {
     const int B = cfg.block_size, H = cfg.n_heads;
-    int spb = std::max(1, 512 / B);   // 512-token splits (256: +0.7% at cfg5 h=0, scripts/splittok_ab.sh)
+    int spb = std::max(1, 512 / B);   // 512-token splits (256: +0.7% at cfg5 h=0; 1024 / 2048 within noise at
+                                      // 1/64, 1/32 and cfg4: profiles/r02_split_size_ab.txt)
     const int64_t target = 4LL * num_sms * 6;  // ~4 tasks per resident warp
     while (spb > 1) {
       int64_t ns = 0;
