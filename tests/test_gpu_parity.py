@@ -304,7 +304,8 @@ def test_fused_and_unfused_agree_bitwise(hc, monkeypatch):
 @pytest.mark.parametrize("env", [{"HC_GROUP_N": "2"}, {"HC_GROUP_N": "3"}, {"HC_SYNC_W": "8"},
                                  {"HC_GROUP_N": "2", "HC_SYNC_W": "8"}, {"HC_GROUP_N": "-3"},
                                  {"HC_FUSED_CFG": "352"}, {"HC_FUSED_CFG": "282"}, {"HC_FUSED_CFG": "342"},
-                                 {"HC_FUSED_CFG": "3424"}, {"HC_FUSED_CFG": "3224"}])
+                                 {"HC_FUSED_CFG": "3424"}, {"HC_FUSED_CFG": "3224"},
+                                 {"HC_DYN_TILES": "0"}, {"HC_DYN_TILES": "0", "HC_SYNC_W": "8"}])
 def test_fused_schedules_agree_bitwise(hc, monkeypatch, env):
     """The fused kernel's raster (n-tiles per group, m-major groups), partner lockstep and
     configuration (GEMM stages, attention warps, extra epilogue warps that split a tile's
@@ -1085,3 +1086,20 @@ def test_gqa_mma_epilogue_with_rope(hc, d, H, dh, B, Hk):
     assert pool.last_decode_path() == 1
     err, lerr = T.compare(w, out, lse, range(len(n)), rope_theta=ROPE_THETA)
     assert err <= TOL_BF16 and lerr <= TOL_LSE, (err, lerr)
+
+
+@pytest.mark.parametrize("env", [{"HC_DYN_TILES": "0"}, {"HC_FUSED_CFG": "3424"}, {"HC_GROUP_N": "2"}])
+def test_gqa_mma_epilogue_schedules_agree_bitwise(hc, monkeypatch, env):
+    """GQA through the mma epilogue: the static tile stride vs the dynamic tile queue, another
+    fused configuration, another raster — only the order of whole tiles / tasks changes =>
+    identical bits."""
+    d, H, dh, B, Hk = 2048, 16, 128, 16, 4
+    n = [700, 33, 511, 1, 257, 96, 129, 64, 300, 17]
+    modes = [MODE_HIDDEN if i % 4 != 1 else MODE_KV for i in range(len(n))]
+    w = _bf16_workload(d, H, dh, B, n=n, modes=modes, bias=True, Hk=Hk)
+    _, a, la = _run(w, split_tokens=64)
+    assert T.compare(w, a, la, range(len(n)))[0] <= TOL_BF16
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, b, lb = _run(w, split_tokens=64)
+    assert np.array_equal(a, b) and np.array_equal(la, lb)
